@@ -1,0 +1,279 @@
+"""Generate golden fixtures by running the UNMODIFIED reference `sparsekern`.
+
+Run in the build container (the reference is mounted read-only at
+/root/reference; it does not exist on the GPU box, so the outputs are committed
+as small compressed .npz files next to this script):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Every case stores its inputs and the reference outputs.  The oracle
+(oracle/skc_oracle.c) is pinned against these in tests/test_oracle.py, and the
+host-side restatements in paper_2512_04556_b200 (kernel rasteriser, bracket,
+canvas rules) are pinned in tests/test_host.py.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import sparsekern as sk  # noqa: E402
+from sparsekern import engine, optim, svfilter  # noqa: E402
+from sparsekern._fastpath import HAVE_NUMBA, ir_batch_compiled, sv_filter_compiled  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def f32(a):
+    """Inputs are fp32-rounded first: the GPU sees exactly these values."""
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def rand_complex(rng, layout, reach):
+    layers = []
+    for n in layout:
+        off = f32(rng.uniform(-reach, reach, size=(n, 2)))
+        w = rng.uniform(0.05, 1.0, size=n)
+        layers.append(sk.SparseLayer(off, f32(w / w.sum())))
+    return sk.KernelComplex(tuple(layers))
+
+
+def cpx_arrays(cpx):
+    off = np.concatenate([l.offsets for l in cpx.layers])
+    w = np.concatenate([l.weights for l in cpx.layers])
+    return off, w, np.array(cpx.layout, dtype=np.int64)
+
+
+def clamp_layer(img, layer):
+    """SURVEY D1 clamp-to-edge wrapper: edge-pad P, reference layer, crop."""
+    p = int(math.floor(np.abs(layer.offsets).max())) + 1
+    pad = ((p, p), (p, p)) + (((0, 0),) if img.ndim == 3 else ())
+    out = sk.apply_sparse_layer(np.pad(img, pad, mode="edge"), layer)
+    return out[p:-p, p:-p]
+
+
+def clamp_complex(img, cpx):
+    out = np.asarray(img, dtype=np.float64)
+    for layer in cpx.layers:
+        out = clamp_layer(out, layer)
+    return out
+
+
+def gen_engine():
+    rng = np.random.default_rng(1001)
+    cases = {}
+    specs = [
+        ((23, 31), (3,), 2.5),
+        ((19, 17, 3), (4, 2), 3.0),
+        ((32, 40, 3), (12, 12, 12, 12), 6.0),
+        ((16, 16, 4), (4, 4, 4), 1.5),
+        ((9, 11, 1), (5,), 7.5),           # reach comparable to the image
+        ((40, 13, 2), (2, 6, 3), 4.0),
+    ]
+    for k, (shape, layout, reach) in enumerate(specs):
+        img = f32(rng.uniform(size=shape))
+        cpx = rand_complex(rng, layout, reach)
+        off, w, lay = cpx_arrays(cpx)
+        cases[f"c{k}_img"] = img
+        cases[f"c{k}_off"] = off
+        cases[f"c{k}_w"] = w
+        cases[f"c{k}_layout"] = lay
+        cases[f"c{k}_zero"] = sk.apply_complex(img, cpx)
+        cases[f"c{k}_layer0"] = sk.apply_sparse_layer(img, cpx.layers[0])
+        cases[f"c{k}_clamp"] = clamp_complex(img, cpx)
+    # exact integer and half-pixel taps, negative weights, duplicate taps
+    img = f32(rng.uniform(size=(12, 14, 3)))
+    cpx = sk.KernelComplex((
+        sk.SparseLayer(np.array([[1.0, 0.0], [0.0, -2.0], [0.5, 0.5], [0.5, 0.5]]),
+                       np.array([0.5, -0.25, 0.5, 0.25])),
+        sk.SparseLayer(np.array([[-1.5, 2.0], [3.0, -0.5]]), np.array([0.75, 0.25])),
+    ))
+    off, w, lay = cpx_arrays(cpx)
+    cases.update(k_img=img, k_off=off, k_w=w, k_layout=lay, k_zero=sk.apply_complex(img, cpx),
+                 k_clamp=clamp_complex(img, cpx))
+    np.savez_compressed(OUT / "engine.npz", **cases)
+
+
+def gen_ir():
+    rng = np.random.default_rng(1002)
+    cases = {}
+    for k, (layout, reach) in enumerate([((3,), 2.5), ((4, 4), 3.0), ((5, 3, 4), 2.0),
+                                          ((8, 8, 8, 8), 4.0)]):
+        cpx = rand_complex(rng, layout, reach)
+        off, w, lay = cpx_arrays(cpx)
+        ir = sk.synthesize_ir(cpx)
+        cases[f"i{k}_off"] = off
+        cases[f"i{k}_w"] = w
+        cases[f"i{k}_layout"] = lay
+        cases[f"i{k}_ir"] = ir.weights
+        cases[f"i{k}_canvas"] = np.int64(ir.size)
+        cases[f"i{k}_required"] = np.int64(sk.required_canvas(cpx))
+    # Kawase 6x4 chain: reference canvas truncation
+    layers = []
+    for l in range(6):
+        r = 0.5 + l
+        layers.append(sk.SparseLayer(np.array([[r, r], [-r, r], [-r, -r], [r, -r]]),
+                                     np.full(4, 0.25)))
+    kaw = sk.KernelComplex(tuple(layers))
+    cases["kawase_auto"] = sk.synthesize_ir(kaw).weights
+    cases["kawase_61"] = sk.synthesize_ir(kaw, canvas=61).weights
+    # batched IR (numpy and numba paths), ragged layout via zero weights
+    off = f32(rng.uniform(-3, 3, (4, 3, 5, 2)))
+    wts = f32(rng.uniform(-0.2, 0.5, (4, 3, 5)))
+    wts[1, 2, 3:] = 0.0
+    cases["batch_off"] = off
+    cases["batch_w"] = wts
+    cases["batch_ir"] = engine.synthesize_ir_batch(off, wts, 41)
+    if HAVE_NUMBA:
+        cases["batch_ir_numba"] = ir_batch_compiled(off, wts, 41)
+    np.savez_compressed(OUT / "ir.npz", **cases)
+
+
+def stacked(basis):
+    ox, oy, w = svfilter._stacked_params(basis)
+    return np.stack([ox, oy, w], axis=-1)
+
+
+def gen_sv():
+    rng = np.random.default_rng(1003)
+    cases = {}
+    layout = (4, 3, 5)
+    base = rand_complex(rng, layout, 3.0)
+    filters = []
+    for k in range(3):
+        layers = []
+        for lay in base.layers:
+            off = f32(lay.offsets * (0.5 + 0.75 * k) + rng.uniform(-0.3, 0.3, lay.offsets.shape))
+            w = lay.weights * rng.uniform(0.8, 1.2, lay.weights.shape)
+            layers.append(sk.SparseLayer(off, f32(w / w.sum())))
+        filters.append(sk.KernelComplex(tuple(layers)))
+    ps = np.array([0.0, 0.4, 1.0])
+    basis = sk.FilterBasis(ps, tuple(filters))
+    img = f32(rng.uniform(size=(29, 37, 3)))
+    yy, xx = np.mgrid[0:29, 0:37]
+    pmap = f32(np.clip(np.hypot(xx - 18, yy - 14) / 20.0 - 0.1, -0.2, 1.2))
+    pmap[3:7, 20:25] = 0.4   # exact knot hits
+    cases.update(img=img, pmap=pmap, params=ps, basis=stacked(basis),
+                 layout=np.array(layout, dtype=np.int64), out=sk.sv_filter(img, basis, pmap))
+    # clamp mode: per layer, sv_filter_compiled on edge-padded img/k0/k1/t, crop
+    k0, k1, t = svfilter._bracket(pmap, basis.params)
+    ox, oy, w = svfilter._stacked_params(basis)
+    outc = []
+    for c in range(3):
+        cur = img[:, :, c]
+        for l, n in enumerate(layout):
+            p = int(math.floor(max(np.abs(ox[:, l]).max(), np.abs(oy[:, l]).max()))) + 2
+            cp = np.pad(cur, p, mode="edge")
+            nxt = sv_filter_compiled(cp, np.pad(k0, p, mode="edge"), np.pad(k1, p, mode="edge"),
+                                     np.pad(t, p, mode="edge"), ox[:, l:l + 1], oy[:, l:l + 1],
+                                     w[:, l:l + 1], (n,))
+            cur = nxt[p:-p, p:-p]
+        outc.append(cur)
+    cases["out_clamp"] = np.stack(outc, axis=2)
+    # single-entry basis, 2-D image
+    b1 = sk.FilterBasis(np.array([0.3]), (filters[1],))
+    img2 = f32(rng.uniform(size=(15, 12)))
+    pm2 = f32(rng.uniform(-1, 2, size=(15, 12)))
+    cases.update(img1=img2, pmap1=pm2, params1=b1.params, basis1=stacked(b1),
+                 out1=sk.sv_filter(img2, b1, pm2))
+    # bracket KAT
+    probe = np.array([-1.0, 0.0, 0.2, 0.4, 0.7, 1.0, 3.0])
+    k0p, k1p, tp = svfilter._bracket(probe, ps)
+    cases.update(bracket_p=probe, bracket_k0=k0p, bracket_t=tp)
+    np.savez_compressed(OUT / "sv.npz", **cases)
+
+
+def gen_optim():
+    rng = np.random.default_rng(1004)
+    cases = {}
+    kinds = [sk.LossKind("charbonnier", 1e-3), sk.LossKind("l1"), sk.LossKind("l2"),
+             sk.LossKind("charbonnier", 1e-6)]
+    k = 0
+    for layout, reach, tsize in [((3,), 2.0, 9), ((4, 2), 2.0, 9), ((2, 3, 4), 1.7, 11),
+                                 ((8, 8, 8, 8), 3.0, 21)]:
+        for kind in kinds:
+            cpx = rand_complex(rng, layout, reach)
+            tgt = sk.DenseKernel(rng.uniform(size=(tsize, tsize))).normalized()
+            tgt = sk.DenseKernel(f32(tgt.weights))
+            value, grads = sk.backward(cpx, tgt, kind)
+            off, w, lay = cpx_arrays(cpx)
+            canvas = max(sk.auto_canvas(cpx), tgt.size)
+            cases[f"b{k}_off"] = off
+            cases[f"b{k}_w"] = w
+            cases[f"b{k}_layout"] = lay
+            cases[f"b{k}_tgt"] = tgt.weights
+            cases[f"b{k}_kind"] = np.array(kind.kind)
+            cases[f"b{k}_eps"] = np.float64(kind.epsilon)
+            cases[f"b{k}_canvas"] = np.int64(canvas)
+            cases[f"b{k}_value"] = np.float64(value)
+            cases[f"b{k}_doff"] = np.concatenate([g[0] for g in grads])
+            cases[f"b{k}_dw"] = np.concatenate([g[1] for g in grads])
+            k += 1
+    cases["n_backward"] = np.int64(k)
+    # short fits with explicit init (optim.py:404-405)
+    fits = [
+        ("sum", "none", "l1", (8, 8, 8), 25, 1e-3, 1e-4),
+        ("none", "none", "l2", (4, 4), 30, 1e-3, 1e-4),
+        ("sofm", "none", "charbonnier", (6, 6), 30, 1e-3, 1e-4),
+        ("sum", "kws", "charbonnier", (8, 4), 30, 2e-3, 1e-4),
+        ("sum", "none", "l1", (4, 4), 12, 1e-2, 1e-2),   # canvas growth
+    ]
+    for j, (wn, sym, lk, layout, steps, lr0, lr1) in enumerate(fits):
+        tgt = sk.disk_kernel(4.0 + j, 2 * (6 + j) + 1)
+        tgt = sk.DenseKernel(f32(tgt.weights))
+        cpx = rand_complex(rng, layout, 2.0 + j)
+        cfg = sk.TrainConfig(steps=steps, lr_start=lr0, lr_end=lr1)
+        res = sk.fit(tgt, layout, cpx, cfg, sk.ConstraintConfig(wn, sym), sk.LossKind(lk))
+        off, w, lay = cpx_arrays(cpx)
+        boff, bw, _ = cpx_arrays(res.complex)
+        cases.update({
+            f"f{j}_tgt": tgt.weights, f"f{j}_off": off, f"f{j}_w": w, f"f{j}_layout": lay,
+            f"f{j}_wn": np.array(wn), f"f{j}_sym": np.array(sym), f"f{j}_loss": np.array(lk),
+            f"f{j}_steps": np.int64(steps), f"f{j}_lr": np.array([lr0, lr1]),
+            f"f{j}_trace": res.trace, f"f{j}_best_off": boff, f"f{j}_best_w": bw,
+            f"f{j}_best_loss": np.float64(res.best_loss), f"f{j}_best_step": np.int64(res.best_step),
+            f"f{j}_canvas": np.int64(res.canvas),
+        })
+    cases["n_fit"] = np.int64(len(fits))
+    # adam KATs (test_optim.py:186-199)
+    cfg = sk.TrainConfig(steps=10, lr_start=1e-3, lr_end=1e-3)
+    params = [[np.zeros((1, 2)), np.zeros(1)]]
+    st = sk.AdamState.for_params(params)
+    out = sk.adam_step(params, [[np.zeros((1, 2)), np.ones(1)]], st, 0, cfg,
+                       sk.ConstraintConfig("none"))
+    cases["adam_first_w"] = out[0][1]
+    np.savez_compressed(OUT / "optim.npz", **cases)
+
+
+def gen_kernels():
+    rng = np.random.default_rng(1005)
+    cases = {}
+    cases["disk_60_129"] = sk.disk_kernel(60.0, 129).weights
+    r = float(rng.uniform(20, 60))
+    rot = float(rng.uniform(0, 2 * np.pi))
+    cases["params"] = np.array([r, rot])
+    cases["square_129"] = sk.polygon_kernel(4, r, 129, rot).weights
+    cases["hex_129"] = sk.polygon_kernel(6, r, 129, rot).weights
+    cases["ring_129"] = sk.ring_kernel(0.6 * r, r, 129).weights
+    cases["star_129"] = sk.star_kernel(4, r, 129, rotation=rot).weights
+    cases["disk_7"] = sk.disk_kernel(2.5).weights
+    cases["gauss_15"] = sk.gaussian_kernel(1.5).weights
+    cases["gauss_2_11"] = sk.gaussian_kernel(1.7, 11).weights
+    np.savez_compressed(OUT / "kernels.npz", **cases)
+
+
+if __name__ == "__main__":
+    gen_engine()
+    gen_ir()
+    gen_sv()
+    gen_optim()
+    gen_kernels()
+    for p in sorted(OUT.glob("*.npz")):
+        print(p.name, p.stat().st_size)
