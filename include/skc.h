@@ -1,0 +1,173 @@
+/*
+ * skc.h -- C ABI of libskc.so, the B200 (sm_100a) Sparse Kernel Complex hot path.
+ *
+ * Drop-in boundary for the reference `sparsekern` package
+ * (/root/reference/pkg/src/sparsekern).  The reference switches its compiled
+ * fast path in at call time through `_fastpath.HAVE_NUMBA`
+ * (svfilter.py:18, svfilter.py:189-190, baselines.py:17, baselines.py:173);
+ * paper_2512_04556_b200 does the same through `HAVE_CUDA`, and every entry
+ * point below replaces the bottom of one reference call chain (cited per
+ * function).  Binding recipe (ctypes) is in INTEGRATION.md.
+ *
+ * Conventions
+ *   - plain C types only; images/maps/parameters live in device memory unless
+ *     the argument is documented as a host array (small tap tables);
+ *   - images are HWC interleaved (the reference's (H, W, C) layout,
+ *     engine.py:133-136), batched as (B, H, W, C), contiguous;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream), re-entrant, and keeps no global mutable state; scratch
+ *     comes from the device's stream-ordered memory pool;
+ *   - the return value is a status code; no C++ exception crosses the ABI;
+ *     skc_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef SKC_H
+#define SKC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SKC_OK 0
+#define SKC_EBADARG 1      /* maps to EngineError / OptimError (argument)   */
+#define SKC_ENONFINITE 2   /* maps to OptimError "non-finite intermediate"  */
+#define SKC_ETRUNC 3       /* maps to TruncationError                        */
+#define SKC_ECUDA 4        /* CUDA runtime failure; see skc_last_error()     */
+#define SKC_EDEGENERATE 5  /* maps to OptimError "SUM normalization degenerate" */
+
+/* storage dtypes (arithmetic is always fp32) */
+#define SKC_F32 0
+#define SKC_F16 1
+
+/* boundary modes: ZERO = reference zero padding (engine.py:106-115);
+ * CLAMP = clamp-to-edge (BASELINE config 0) */
+#define SKC_ZERO 0
+#define SKC_CLAMP 1
+
+/* loss kinds (optim.py:59-68) and weight normalisations (optim.py:71-80) */
+#define SKC_LOSS_CHARBONNIER 0
+#define SKC_LOSS_L1 1
+#define SKC_LOSS_L2 2
+#define SKC_WN_NONE 0
+#define SKC_WN_SUM 1
+#define SKC_WN_SOFM 2
+
+int skc_version(void);
+const char *skc_last_error(void);
+
+/* Upper bound on taps per layer accepted by the filter entry points. */
+int skc_max_taps(void);
+
+/*
+ * One sparse layer, out[b,y,x,c] = sum_i w_i * bilinear(in[b], x+ox_i, y+oy_i)[c].
+ * Replaces engine.apply_sparse_layer (engine.py:160-170) and its inner
+ * sample_shifted/_accum_shift (engine.py:106-130).
+ *   in/out : device, (B, H, W, C) of in_dtype / out_dtype
+ *   taps   : HOST float64 array (S, 3) = (ox, oy, w) per tap
+ */
+int skc_layer_fwd(const void *in, int in_dtype, void *out, int out_dtype,
+                  int B, int H, int W, int C,
+                  const double *taps, int S, int boundary, void *stream);
+
+/*
+ * A chain of L layers (engine.apply_complex, engine.py:173-178).  Intermediate
+ * images stay fp32 in pool scratch; only `in` and `out` use the given dtypes.
+ *   taps   : HOST float64 (sum(layout), 3), layers concatenated in order
+ *   layout : HOST int32 (L,) taps per layer
+ */
+int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype,
+                  int B, int H, int W, int C,
+                  const double *taps, const int *layout, int L, int boundary, void *stream);
+
+/*
+ * Spatially varying filtering (svfilter.sv_filter, svfilter.py:171-203 ->
+ * _fastpath.sv_filter_compiled / _sv_pass_loop, _fastpath.py:97-150).
+ *   pmap   : device float32 (H, W) per-pixel parameter
+ *   params : HOST float64 (Mb,) strictly increasing basis parameters
+ *   basis  : HOST float64 (Mb, L, nmax, 3) = (ox, oy, w), zero padded
+ *            (svfilter._stacked_params, svfilter.py:155-168)
+ *   layout : HOST int32 (L,)
+ */
+int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype,
+               int H, int W, int C, const float *pmap,
+               const double *params, int Mb, const double *basis, int nmax,
+               const int *layout, int L, int boundary, void *stream);
+
+/*
+ * Batched impulse responses (engine.synthesize_ir / synthesize_ir_batch,
+ * engine.py:191-209, 251-303; _fastpath.ir_batch_compiled, _fastpath.py:33-94).
+ *   taps : device float32 (B, L, nmax, 3) = (ox, oy, w); zero weights inert
+ *   out  : device float32 (B, canvas, canvas)
+ *   layout : HOST int32 (L,)
+ */
+int skc_ir_batch(const float *taps, int B, const int *layout, int L, int nmax,
+                 int canvas, float *out, void *stream);
+
+/* Fit configuration (optim.TrainConfig, ConstraintConfig, LossKind). */
+typedef struct skc_fit_cfg {
+    int steps;            /* TrainConfig.steps                          */
+    float lr_start;       /* TrainConfig.lr_start                       */
+    float lr_end;         /* TrainConfig.lr_end                         */
+    float beta1, beta2, eps;
+    int weight_norm;      /* SKC_WN_*                                   */
+    int kws;              /* ConstraintConfig.symmetry == "kws"         */
+    int loss_kind;        /* SKC_LOSS_*                                 */
+    float loss_eps;       /* LossKind.epsilon                           */
+} skc_fit_cfg;
+
+/*
+ * Loss and gradients of B independent complexes (optim.backward,
+ * optim.py:278-292 -> _forward_ir 204-222, _loss_value/_loss_grad 133-146,
+ * _backward_pass 231-263), each against its own target embedded in `canvas`.
+ *   taps    : device float32 (B, L, nmax, 3), effective weights
+ *   tgts    : device float32 (B, M, M), M odd, M <= canvas
+ *   loss    : device float32 (B,)
+ *   grads   : device float32 (B, L, nmax, 3) = (d_ox, d_oy, d_w)
+ *   status  : device int32 (B, 4) = (code, layer, sample, 0)
+ */
+int skc_backward_batch(const float *taps, int B, const int *layout, int L, int nmax,
+                       const float *tgts, int M, int canvas, int loss_kind, float loss_eps,
+                       float *loss, float *grads, int *status, void *stream);
+
+/*
+ * Persistent batched fitting (optim.fit, optim.py:390-469 with an explicit
+ * KernelComplex init, optim.py:404-405): one CTA owns one target kernel and
+ * runs every step on device -- forward on the impulse, loss, backward, Adam
+ * (optim.py:338-369) with the offset learning-rate scale M (optim.py:411),
+ * KWS/SUM projections (312-335), best-so-far tracking (442-445) and the
+ * canvas growth rule (429-434).
+ *   state  : device float32 (B, SKC_FIT_STATE_FLOATS(L, nmax)); initialise
+ *            with skc_fit_init, read back with the SKC_FIT_OFF_* accessors
+ *   tgts   : device float32 (B, M, M)
+ *   trace  : device float32 (B, steps + 1) per-step loss
+ *   status : device int32 (B, 4) = (code, layer, sample, step)
+ * Returns SKC_OK when every kernel finished; per-kernel failures are in
+ * status (code SKC_ENONFINITE / SKC_EDEGENERATE).
+ */
+#define SKC_FIT_HDR 8
+#define SKC_FIT_STATE_FLOATS(L, nmax) (SKC_FIT_HDR + 6 * (L) * (nmax) * 3)
+/* state layout (floats): hdr[0]=step done, hdr[1]=canvas, hdr[2]=best loss,
+ * hdr[3]=best step; then params, adam m, adam v, best params, scratch, scratch
+ * each (L, nmax, 3) = (ox, oy, wparam). */
+int skc_fit_init(float *state, const float *init_taps, int B, const int *layout, int L,
+                 int nmax, int M, const skc_fit_cfg *cfg, int *status, void *stream);
+int skc_fit_run(float *state, int B, const int *layout, int L, int nmax,
+                const float *tgts, int M, const skc_fit_cfg *cfg,
+                float *trace, int *status, void *stream);
+
+/*
+ * One Adam update with projections (optim.adam_step, optim.py:338-369) on
+ * device arrays of one complex: params/grads/m/v float32 (P, 3) rows
+ * (ox, oy, wparam), P = sum(layout).  status int32 (4,).
+ */
+int skc_adam_step(float *params, const float *grads, float *m, float *v, const int *layout,
+                  int L, int step_index, const skc_fit_cfg *cfg, float offset_lr_scale,
+                  int *status, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKC_H */

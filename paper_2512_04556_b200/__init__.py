@@ -1,0 +1,55 @@
+"""paper_2512_04556_b200: the Sparse Kernel Complex hot path on NVIDIA B200 (sm_100a).
+
+A drop-in for the filtering, spatially varying filtering and kernel-fitting
+API of the reference `sparsekern` package (arXiv 2512.04556): same names,
+signatures and errors, with the arithmetic in hand-written CUDA kernels
+(libskc.so, C ABI in include/skc.h).  `HAVE_CUDA` mirrors the reference's
+`_fastpath.HAVE_NUMBA` switch; there is no CPU fallback.
+"""
+
+from ._native import HAVE_CUDA, NativeError, NativeUnavailable
+from .engine import (
+    EngineError,
+    KernelComplex,
+    SparseLayer,
+    TruncationError,
+    apply_complex,
+    apply_complex_batch,
+    apply_sparse_layer,
+    auto_canvas,
+    psnr,
+    required_canvas,
+    sse,
+    synthesize_ir,
+    synthesize_ir_batch,
+)
+from .kernels import (
+    DenseKernel,
+    KernelError,
+    delta_kernel,
+    disk_kernel,
+    gaussian_kernel,
+    polygon_kernel,
+    ring_kernel,
+    star_kernel,
+)
+from .optim import (
+    AdamState,
+    ConstraintConfig,
+    FitResult,
+    LossKind,
+    OptimError,
+    TrainConfig,
+    adam_step,
+    backward,
+    backward_batch,
+    fit,
+    fit_batch,
+    load_theta,
+    loss,
+    parse_layout,
+    save_theta,
+)
+from .svfilter import FilterBasis, interp_weights, sv_filter, synthesize_filter
+
+__version__ = "0.1.0"

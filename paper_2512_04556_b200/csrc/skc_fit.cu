@@ -1,0 +1,877 @@
+// skc_fit.cu -- impulse-response synthesis, analytic backward and the
+// persistent batched fitting loop for sm_100a.
+//
+// Reference (citations into /root/reference/pkg/src/sparsekern):
+//   synthesize_ir (engine.py:191-209), synthesize_ir_batch (251-303),
+//   _ir_batch_loop (_fastpath.py:33-85); optim.py: _loss_value/_loss_grad
+//   (133-146), _forward_ir (204-222), _first_nonfinite_sample (225-228),
+//   _backward_pass (231-263), _chain_weight_norm (266-275), backward
+//   (278-292), _project_kws (312-325), _project_sum (328-335), adam_step
+//   (338-369), fit (390-469).
+//
+// One CTA owns one complex (one target kernel) for the whole call.  Every
+// step runs on device: effective weights, the canvas growth rule, per-layer
+// live boxes (the support of each intermediate, clipped to the canvas -- the
+// reference's "live region", _fastpath.py:42-56), the forward chain, the
+// loss, the reverse sweep (per-tap <g, sample>, <g, d sample/dx>,
+// <g, d sample/dy> reductions in float64, then the adjoint gather at negated
+// offsets), the weight-norm chain rule, Adam and the projections.  Reductions
+// are fixed-order (warp shuffle tree, then warps in index order), so results
+// are bit-reproducible run to run.  The per-step loss goes to a device trace;
+// the host reads it once at the end.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "skc_common.cuh"
+
+namespace skc {
+
+constexpr int kFitThreads = 512;
+constexpr int kFitWarps = kFitThreads / 32;
+constexpr int kFitMaxL = 8;
+constexpr int kFitMaxP = 256;     // total taps per complex
+constexpr int kFitChunk = 64;     // taps per reduction chunk
+constexpr int kNeedGrow = 100;    // internal status: scratch canvas too small
+
+enum FitMode { MODE_FIT = 0, MODE_BACKWARD = 1, MODE_IR = 2 };
+
+struct Box {
+    int x0, x1, y0, y1;  // inclusive bounds; empty when x1 < x0 or y1 < y0
+};
+
+struct FitParams {
+    int B, L, nmax, P, M, mode;
+    int layout[kFitMaxL];
+    int start[kFitMaxL + 1];
+    skc_fit_cfg cfg;
+    int cap;            // scratch canvas capacity
+    int canvas_fixed;   // MODE_BACKWARD / MODE_IR canvas
+    float *state;       // MODE_FIT
+    const float *tgts;  // (B, M, M)
+    float *trace;       // (B, steps+1)
+    int *status;        // (B, 4)
+    float *scratch;     // (B, L+2, cap, cap)
+    const float *taps_in;  // MODE_BACKWARD / MODE_IR: (B, L, nmax, 3)
+    float *loss_out;       // MODE_BACKWARD
+    float *grads_out;      // MODE_BACKWARD: (B, L, nmax, 3)
+    float *ir_out;         // MODE_IR: (B, canvas, canvas)
+};
+
+struct FitSmem {
+    float2 off[kFitMaxP];   // current offsets
+    float wp[kFitMaxP];     // weight parameters (weights or logits)
+    float w[kFitMaxP];      // effective weights
+    float4 cw[kFitMaxP];    // corner weights
+    float2 frac[kFitMaxP];  // fx, fy
+    int2 ixy[kFitMaxP];     // floor(ox), floor(oy)
+    float3 grad[kFitMaxP];  // d_ox, d_oy, d_w
+    double part[kFitWarps][3][kFitChunk];
+    double red[kFitWarps];
+    Box box[kFitMaxL + 1];
+    int canvas;
+    int flag;
+    int bad_layer, bad_sample;
+};
+
+__device__ __forceinline__ bool inbox(const Box &b, int y, int x) {
+    return y >= b.y0 && y <= b.y1 && x >= b.x0 && x <= b.x1;
+}
+
+__device__ __forceinline__ float rd(const float *buf, int cap, const Box &b, int y, int x) {
+    return inbox(b, y, x) ? buf[y * cap + x] : 0.f;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum of one double (result valid in thread 0 and returned to all).
+__device__ double block_sum(FitSmem &S, double v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) S.red[warp] = v;
+    __syncthreads();
+    double tot = 0.0;
+    for (int k = 0; k < kFitWarps; ++k) tot += S.red[k];
+    return tot;
+}
+
+// optim.py:133-146
+__device__ __forceinline__ float loss_term(float d, int kind, float eps) {
+    if (kind == SKC_LOSS_CHARBONNIER) return sqrtf(d * d + eps * eps);
+    if (kind == SKC_LOSS_L1) return fabsf(d);
+    return d * d;
+}
+__device__ __forceinline__ float loss_grad(float d, int kind, float eps) {
+    if (kind == SKC_LOSS_CHARBONNIER) return d / sqrtf(d * d + eps * eps);
+    if (kind == SKC_LOSS_L1) return d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+    return 2.f * d;
+}
+
+__device__ __forceinline__ float *sbuf(const FitParams &p, int b, int k) {
+    return p.scratch + ((size_t)b * (p.L + 2) + k) * (size_t)p.cap * p.cap;
+}
+
+// Effective weights (optim.py:164-165; softmax 159-161) -- one thread per layer.
+__device__ void effective_weights(const FitParams &p, FitSmem &S) {
+    const int l = threadIdx.x;
+    if (l < p.L) {
+        const int s0 = p.start[l], n = p.layout[l];
+        if (p.cfg.weight_norm == SKC_WN_SOFM) {
+            float m = S.wp[s0];
+            for (int i = 1; i < n; ++i) m = fmaxf(m, S.wp[s0 + i]);
+            float sum = 0.f;
+            for (int i = 0; i < n; ++i) {
+                const float e = expf(S.wp[s0 + i] - m);
+                S.w[s0 + i] = e;
+                sum += e;
+            }
+            for (int i = 0; i < n; ++i) S.w[s0 + i] /= sum;
+        } else {
+            for (int i = 0; i < n; ++i) S.w[s0 + i] = S.wp[s0 + i];
+        }
+    }
+    __syncthreads();
+}
+
+// Tap tables (sample_shifted, engine.py:118-130) and live boxes.
+__device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S) {
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        const float ox = S.off[q].x, oy = S.off[q].y, w = S.w[q];
+        const float fx0 = floorf(ox), fy0 = floorf(oy);
+        const float fx = ox - fx0, fy = oy - fy0;
+        S.ixy[q] = make_int2((int)fx0, (int)fy0);
+        S.frac[q] = make_float2(fx, fy);
+        S.cw[q] = make_float4(w * (1.f - fx) * (1.f - fy), w * fx * (1.f - fy),
+                              w * (1.f - fx) * fy, w * fx * fy);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int c = S.canvas / 2, last = S.canvas - 1;
+        S.box[0] = Box{c, c, c, c};
+        for (int l = 0; l < p.L; ++l) {
+            int dxmin = 1 << 30, dxmax = -(1 << 30), dymin = 1 << 30, dymax = -(1 << 30);
+            for (int i = 0; i < p.layout[l]; ++i) {
+                const int2 d = S.ixy[p.start[l] + i];
+                dxmin = min(dxmin, d.x);
+                dxmax = max(dxmax, d.x + 1);
+                dymin = min(dymin, d.y);
+                dymax = max(dymax, d.y + 1);
+            }
+            const Box &a = S.box[l];
+            Box nb;
+            // I_{l+1}[y] = sum cw I_l[y + d]  =>  support of I_{l+1} = support(I_l) - d
+            nb.x0 = max(0, a.x0 - dxmax);
+            nb.x1 = min(last, a.x1 - dxmin);
+            nb.y0 = max(0, a.y0 - dymax);
+            nb.y1 = min(last, a.y1 - dymin);
+            if (a.x1 < a.x0 || a.y1 < a.y0) nb = Box{0, -1, 0, -1};
+            S.box[l + 1] = nb;
+        }
+    }
+    __syncthreads();
+}
+
+// Forward chain on the live boxes (_forward_ir, optim.py:204-222).  Returns
+// false (and fills bad_layer/bad_sample) on a non-finite intermediate.
+__device__ bool forward(const FitParams &p, FitSmem &S, int b) {
+    const int cap = p.cap;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    float *b0 = sbuf(p, b, 0);
+    const int c = S.canvas / 2;
+    if (threadIdx.x == 0) b0[c * cap + c] = 1.f;
+    __syncthreads();
+    for (int l = 0; l < p.L; ++l) {
+        const float *src = sbuf(p, b, l);
+        float *dst = sbuf(p, b, l + 1);
+        const Box a = S.box[l], o = S.box[l + 1];
+        const int s0 = p.start[l], n = p.layout[l];
+        int bad = 0;
+        for (int y = o.y0 + ty; y <= o.y1; y += kFitWarps) {
+            for (int x = o.x0 + tx; x <= o.x1; x += 32) {
+                float acc = 0.f;
+                for (int i = 0; i < n; ++i) {
+                    const int2 d = S.ixy[s0 + i];
+                    const float4 w = S.cw[s0 + i];
+                    const int yy = y + d.y, xx = x + d.x;
+                    acc = fmaf(w.x, rd(src, cap, a, yy, xx), acc);
+                    acc = fmaf(w.y, rd(src, cap, a, yy, xx + 1), acc);
+                    acc = fmaf(w.z, rd(src, cap, a, yy + 1, xx), acc);
+                    acc = fmaf(w.w, rd(src, cap, a, yy + 1, xx + 1), acc);
+                }
+                dst[y * cap + x] = acc;
+                bad |= !isfinite(acc);
+            }
+        }
+        if (__syncthreads_or(bad)) {
+            if (threadIdx.x == 0) {
+                S.bad_layer = l;
+                S.bad_sample = -1;
+                for (int i = 0; i < n; ++i) {
+                    const int q = s0 + i;
+                    if (!(isfinite(S.off[q].x) && isfinite(S.off[q].y) && isfinite(S.w[q]))) {
+                        S.bad_sample = i;
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ float tgt_at(const FitParams &p, int b, int canvas, int y, int x) {
+    const int pad = (canvas - p.M) / 2;   // DenseKernel.embedded (kernels.py:75-82)
+    const int ty = y - pad, tx = x - pad;
+    if (ty < 0 || ty >= p.M || tx < 0 || tx >= p.M) return 0.f;
+    return __ldg(p.tgts + ((size_t)b * p.M + ty) * p.M + tx);
+}
+
+// Loss over the whole canvas (the IR is zero outside its live box); the
+// loss gradient is stored over the live box of the IR only -- the reverse
+// sweep never reads it elsewhere.
+__device__ double loss_and_grad(const FitParams &p, FitSmem &S, int b) {
+    const int cap = p.cap, canvas = S.canvas;
+    float *ir = sbuf(p, b, p.L);
+    const Box o = S.box[p.L];
+    double part = 0.0;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int y = ty; y < canvas; y += kFitWarps) {
+        for (int x = tx; x < canvas; x += 32) {
+            const bool in = inbox(o, y, x);
+            const float v = in ? ir[y * cap + x] : 0.f;
+            const float d = v - tgt_at(p, b, canvas, y, x);
+            part += (double)loss_term(d, p.cfg.loss_kind, p.cfg.loss_eps);
+            if (in) ir[y * cap + x] = loss_grad(d, p.cfg.loss_kind, p.cfg.loss_eps);
+        }
+    }
+    return block_sum(S, part);
+}
+
+// Reverse sweep (_backward_pass, optim.py:231-263).  Writes S.grad.
+__device__ void backward_sweep(const FitParams &p, FitSmem &S, int b) {
+    const int cap = p.cap;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tx = lane, ty = warp;
+    int gcur = p.L;          // buffer holding g_{l+1}
+    for (int l = p.L - 1; l >= 0; --l) {
+        const float *I = sbuf(p, b, l);
+        const float *g = sbuf(p, b, gcur);
+        const Box bi = S.box[l], bg = S.box[l + 1];
+        const int s0 = p.start[l], n = p.layout[l];
+        for (int c0 = 0; c0 < n; c0 += kFitChunk) {
+            const int c1 = min(n, c0 + kFitChunk);
+            for (int i = c0; i < c1; ++i) {
+                const int2 d = S.ixy[s0 + i];
+                const float fx = S.frac[s0 + i].x, fy = S.frac[s0 + i].y;
+                const float a00 = (1.f - fx) * (1.f - fy), a10 = fx * (1.f - fy);
+                const float a01 = (1.f - fx) * fy, a11 = fx * fy;
+                double sw = 0.0, sx = 0.0, sy = 0.0;
+                for (int y = bg.y0 + ty; y <= bg.y1; y += kFitWarps) {
+                    for (int x = bg.x0 + tx; x <= bg.x1; x += 32) {
+                        const float gv = g[y * cap + x];
+                        const int yy = y + d.y, xx = x + d.x;
+                        const float s00 = rd(I, cap, bi, yy, xx), s10 = rd(I, cap, bi, yy, xx + 1);
+                        const float s01 = rd(I, cap, bi, yy + 1, xx), s11 = rd(I, cap, bi, yy + 1, xx + 1);
+                        const float smp = a00 * s00 + a10 * s10 + a01 * s01 + a11 * s11;
+                        const float ddx = (1.f - fy) * (s10 - s00) + fy * (s11 - s01);
+                        const float ddy = (1.f - fx) * (s01 - s00) + fx * (s11 - s10);
+                        sw += (double)(gv * smp);
+                        sx += (double)(gv * ddx);
+                        sy += (double)(gv * ddy);
+                    }
+                }
+                sw = warp_sum(sw);
+                sx = warp_sum(sx);
+                sy = warp_sum(sy);
+                if (lane == 0) {
+                    S.part[warp][0][i - c0] = sw;
+                    S.part[warp][1][i - c0] = sx;
+                    S.part[warp][2][i - c0] = sy;
+                }
+            }
+            __syncthreads();
+            for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+                double tw = 0.0, txx = 0.0, tyy = 0.0;
+                for (int k = 0; k < kFitWarps; ++k) {
+                    tw += S.part[k][0][i - c0];
+                    txx += S.part[k][1][i - c0];
+                    tyy += S.part[k][2][i - c0];
+                }
+                const float w = S.w[s0 + i];
+                S.grad[s0 + i] = make_float3((float)(w * txx), (float)(w * tyy), (float)tw);
+            }
+            __syncthreads();
+        }
+        if (l > 0) {
+            // adjoint: g_l[q] = sum_i w_i bilinear(g_{l+1}, q - o_i) on the box of I_l
+            const int gnext = (gcur == p.L) ? p.L + 1 : p.L;
+            float *gn = sbuf(p, b, gnext);
+            for (int y = bi.y0 + ty; y <= bi.y1; y += kFitWarps) {
+                for (int x = bi.x0 + tx; x <= bi.x1; x += 32) {
+                    float acc = 0.f;
+                    for (int i = 0; i < n; ++i) {
+                        const int2 d = S.ixy[s0 + i];
+                        const float4 w = S.cw[s0 + i];
+                        const int yy = y - d.y, xx = x - d.x;
+                        acc = fmaf(w.x, rd(g, cap, bg, yy, xx), acc);
+                        acc = fmaf(w.y, rd(g, cap, bg, yy, xx - 1), acc);
+                        acc = fmaf(w.z, rd(g, cap, bg, yy - 1, xx), acc);
+                        acc = fmaf(w.w, rd(g, cap, bg, yy - 1, xx - 1), acc);
+                    }
+                    gn[y * cap + x] = acc;
+                }
+            }
+            __syncthreads();
+            gcur = gnext;
+        }
+    }
+}
+
+__device__ __forceinline__ int param_index(const FitParams &p, int q) {
+    // flat tap q -> (l, i) -> row in the (L, nmax) parameter block
+    int l = 0;
+    while (l + 1 < p.L && q >= p.start[l + 1]) ++l;
+    return l * p.nmax + (q - p.start[l]);
+}
+
+// KWS tie (optim.py:312-325) then SUM projection (328-335).  Returns the
+// degenerate layer or -1.
+__device__ int project(const FitParams &p, FitSmem &S) {
+    if (p.cfg.kws) {
+        const int ngroups = p.P / 4;
+        for (int gq = threadIdx.x; gq < ngroups; gq += blockDim.x) {
+            const int q = 4 * gq;  // layers are multiples of 4, so groups never straddle layers
+            const float sx[4] = {1.f, -1.f, -1.f, 1.f}, sy[4] = {1.f, 1.f, -1.f, -1.f};
+            float dx = 0.f, dy = 0.f, mw = 0.f;
+            for (int k = 0; k < 4; ++k) {
+                dx += sx[k] * S.off[q + k].x;
+                dy += sy[k] * S.off[q + k].y;
+                mw += S.wp[q + k];
+            }
+            dx /= 4.f;
+            dy /= 4.f;
+            mw /= 4.f;
+            for (int k = 0; k < 4; ++k) {
+                S.off[q + k] = make_float2(sx[k] * dx, sy[k] * dy);
+                S.wp[q + k] = mw;
+            }
+        }
+        __syncthreads();
+    }
+    int bad = -1;
+    if (p.cfg.weight_norm == SKC_WN_SUM) {
+        if (threadIdx.x == 0) {
+            S.flag = -1;
+            for (int l = 0; l < p.L; ++l) {
+                float s = 0.f;
+                for (int i = 0; i < p.layout[l]; ++i) s += S.wp[p.start[l] + i];
+                if (fabsf(s) < 1e-8f) { S.flag = l; break; }
+                for (int i = 0; i < p.layout[l]; ++i) S.wp[p.start[l] + i] /= s;
+            }
+        }
+        __syncthreads();
+        bad = S.flag;
+        __syncthreads();
+    }
+    return bad;
+}
+
+__device__ __forceinline__ int &hdr_i(float *st, int k) { return reinterpret_cast<int *>(st)[k]; }
+
+__global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant__ FitParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
+    const int b = blockIdx.x;
+    const int blk = p.L * p.nmax * 3;
+    int *status = p.status + 4 * b;
+
+    if (p.mode != MODE_FIT) {
+        // backward()/synthesize_ir(): parameters come in as effective weights
+        const float *t = p.taps_in + (size_t)b * blk;
+        for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+            const int r = param_index(p, q);
+            S.off[q] = make_float2(t[3 * r], t[3 * r + 1]);
+            S.w[q] = t[3 * r + 2];
+            S.wp[q] = S.w[q];
+        }
+        if (threadIdx.x == 0) S.canvas = p.canvas_fixed;
+        __syncthreads();
+        build_taps_and_boxes(p, S);
+        const bool ok = forward(p, S, b);
+        if (!ok) {
+            if (threadIdx.x == 0) {
+                status[0] = SKC_ENONFINITE;
+                status[1] = S.bad_layer;
+                status[2] = S.bad_sample;
+                status[3] = 0;
+            }
+            return;
+        }
+        if (p.mode == MODE_IR) {
+            const int cv = S.canvas;
+            const Box o = S.box[p.L];
+            const float *ir = sbuf(p, b, p.L);
+            float *out = p.ir_out + (size_t)b * cv * cv;
+            for (int e = threadIdx.x; e < cv * cv; e += blockDim.x) {
+                const int y = e / cv, x = e - y * cv;
+                out[e] = inbox(o, y, x) ? ir[y * p.cap + x] : 0.f;
+            }
+            if (threadIdx.x == 0) status[0] = SKC_OK;
+            return;
+        }
+        const double loss = loss_and_grad(p, S, b);
+        __syncthreads();
+        backward_sweep(p, S, b);
+        float *go = p.grads_out + (size_t)b * blk;
+        for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+            const int r = param_index(p, q);
+            go[3 * r] = S.grad[q].x;
+            go[3 * r + 1] = S.grad[q].y;
+            go[3 * r + 2] = S.grad[q].z;
+        }
+        if (threadIdx.x == 0) {
+            p.loss_out[b] = (float)loss;
+            status[0] = SKC_OK;
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- MODE_FIT ---
+    float *st = p.state + (size_t)b * SKC_FIT_STATE_FLOATS(p.L, p.nmax);
+    float *prm = st + SKC_FIT_HDR;
+    float *am = prm + blk;
+    float *av = am + blk;
+    float *best = av + blk;
+    float *trace = p.trace + (size_t)b * (p.cfg.steps + 1);
+    if (status[0] != SKC_OK && status[0] != kNeedGrow) return;  // failed earlier
+    int step = hdr_i(st, 0);
+    if (step > p.cfg.steps) return;                              // finished
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        const int r = param_index(p, q);
+        S.off[q] = make_float2(prm[3 * r], prm[3 * r + 1]);
+        S.wp[q] = prm[3 * r + 2];
+    }
+    if (threadIdx.x == 0) S.canvas = hdr_i(st, 1);
+    __syncthreads();
+    float best_loss = st[2];
+    int best_step = hdr_i(st, 3);
+    const float scale = (float)p.M;  // offset_lr_scale = k_tgt.size (optim.py:411)
+    int code = SKC_OK, err_layer = 0, err_sample = -1;
+
+    for (;; ++step) {
+        effective_weights(p, S);
+        // embed_if_grown (optim.py:429-434): reach = sum_l max |o| (engine.py:68-71, 101-103)
+        if (threadIdx.x == 0) {
+            float reach = 0.f;
+            for (int l = 0; l < p.L; ++l) {
+                float m = 0.f;
+                for (int i = 0; i < p.layout[l]; ++i) {
+                    const float2 o = S.off[p.start[l] + i];
+                    m = fmaxf(m, fmaxf(fabsf(o.x), fabsf(o.y)));
+                }
+                reach += m;
+            }
+            const int need = 2 * (int)ceilf(reach) + 1;
+            if (need > S.canvas) S.canvas = need + 4;
+            S.flag = S.canvas > p.cap;
+        }
+        __syncthreads();
+        if (S.flag) { code = kNeedGrow; break; }
+        build_taps_and_boxes(p, S);
+        if (!forward(p, S, b)) {
+            code = SKC_ENONFINITE;
+            err_layer = S.bad_layer;
+            err_sample = S.bad_sample;
+            break;
+        }
+        const double loss = loss_and_grad(p, S, b);
+        const float lossf = (float)loss;
+        if (threadIdx.x == 0) trace[step] = lossf;
+        if (lossf < best_loss) {   // strict improvement, optim.py:442-445
+            best_loss = lossf;
+            best_step = step;
+            for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+                const int r = param_index(p, q);
+                best[3 * r] = S.off[q].x;
+                best[3 * r + 1] = S.off[q].y;
+                best[3 * r + 2] = S.w[q];
+            }
+        }
+        if (step == p.cfg.steps) { step = p.cfg.steps + 1; break; }
+        __syncthreads();
+        backward_sweep(p, S, b);
+        // _chain_weight_norm (optim.py:266-275)
+        if (p.cfg.weight_norm == SKC_WN_SOFM) {
+            if (threadIdx.x < p.L) {
+                const int s0 = p.start[threadIdx.x], n = p.layout[threadIdx.x];
+                float dot = 0.f;
+                for (int i = 0; i < n; ++i) dot += S.grad[s0 + i].z * S.w[s0 + i];
+                for (int i = 0; i < n; ++i) S.grad[s0 + i].z = S.w[s0 + i] * (S.grad[s0 + i].z - dot);
+            }
+            __syncthreads();
+        }
+        // adam_step (optim.py:338-369), bias correction at t = step + 1
+        {
+            const int T = p.cfg.steps;
+            const int tc = min(max(step, 0), T - 1);
+            const double lr = (T == 1) ? (double)p.cfg.lr_start
+                                       : (double)p.cfg.lr_start + ((double)p.cfg.lr_end - (double)p.cfg.lr_start) * tc / (double)(T - 1);
+            const double tt = (double)(step + 1);
+            const float c1 = (float)(1.0 - pow((double)p.cfg.beta1, tt));
+            const float c2 = (float)(1.0 - pow((double)p.cfg.beta2, tt));
+            const float b1 = p.cfg.beta1, b2 = p.cfg.beta2, eps = p.cfg.eps;
+            const float lrf = (float)lr;
+            for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+                const int r = param_index(p, q);
+                const float g3[3] = {S.grad[q].x, S.grad[q].y, S.grad[q].z};
+                float pv[3] = {S.off[q].x, S.off[q].y, S.wp[q]};
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float g = g3[k];
+                    const float m = am[3 * r + k] * b1 + (1.f - b1) * g;
+                    const float v = av[3 * r + k] * b2 + (1.f - b2) * g * g;
+                    am[3 * r + k] = m;
+                    av[3 * r + k] = v;
+                    const float s = k < 2 ? scale : 1.f;
+                    pv[k] = pv[k] - s * lrf * (m / c1) / (sqrtf(v / c2) + eps);
+                }
+                S.off[q] = make_float2(pv[0], pv[1]);
+                S.wp[q] = pv[2];
+            }
+            __syncthreads();
+        }
+        const int badl = project(p, S);
+        if (badl >= 0) {
+            code = SKC_EDEGENERATE;
+            err_layer = badl;
+            break;
+        }
+    }
+
+    // persist state (resumable after kNeedGrow)
+    __syncthreads();
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        const int r = param_index(p, q);
+        prm[3 * r] = S.off[q].x;
+        prm[3 * r + 1] = S.off[q].y;
+        prm[3 * r + 2] = S.wp[q];
+    }
+    if (threadIdx.x == 0) {
+        hdr_i(st, 0) = step;
+        hdr_i(st, 1) = S.canvas;
+        st[2] = best_loss;
+        hdr_i(st, 3) = best_step;
+        status[0] = code;
+        status[1] = err_layer;
+        status[2] = err_sample;
+        status[3] = step;
+    }
+}
+
+// Initialise fit state from an explicit init complex: parameters
+// (_params_from_complex, optim.py:168-176), KWS/SUM projections (414-417),
+// the initial canvas max(auto_canvas, M) (419-420).
+__global__ void fit_init_kernel(const __grid_constant__ FitParams p, const float *init) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
+    const int b = blockIdx.x;
+    const int blk = p.L * p.nmax * 3;
+    float *st = p.state + (size_t)b * SKC_FIT_STATE_FLOATS(p.L, p.nmax);
+    float *prm = st + SKC_FIT_HDR;
+    const float *t = init + (size_t)b * blk;
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        const int r = param_index(p, q);
+        S.off[q] = make_float2(t[3 * r], t[3 * r + 1]);
+        const float w = t[3 * r + 2];
+        S.wp[q] = (p.cfg.weight_norm == SKC_WN_SOFM) ? logf(fmaxf(w, 1e-12f)) : w;
+    }
+    for (int e = threadIdx.x; e < SKC_FIT_STATE_FLOATS(p.L, p.nmax) - SKC_FIT_HDR; e += blockDim.x)
+        prm[e] = 0.f;
+    __syncthreads();
+    const int bad = project(p, S);
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        const int r = param_index(p, q);
+        prm[3 * r] = S.off[q].x;
+        prm[3 * r + 1] = S.off[q].y;
+        prm[3 * r + 2] = S.wp[q];
+    }
+    if (threadIdx.x == 0) {
+        float reach = 0.f;
+        for (int l = 0; l < p.L; ++l) {
+            float m = 0.f;
+            for (int i = 0; i < p.layout[l]; ++i) {
+                const float2 o = S.off[p.start[l] + i];
+                m = fmaxf(m, fmaxf(fabsf(o.x), fabsf(o.y)));
+            }
+            reach += m;
+        }
+        const int canvas = max(2 * (int)ceilf(reach) + 1 + 4, p.M);
+        hdr_i(st, 0) = 0;
+        hdr_i(st, 1) = canvas;
+        st[2] = INFINITY;
+        hdr_i(st, 3) = 0;
+        int *status = p.status + 4 * b;
+        status[0] = bad >= 0 ? SKC_EDEGENERATE : SKC_OK;
+        status[1] = bad >= 0 ? bad : 0;
+        status[2] = -1;
+        status[3] = 0;
+    }
+}
+
+// Standalone Adam step on one complex (optim.adam_step): a single CTA.
+__global__ void adam_kernel(float *params, const float *grads, float *m, float *v,
+                            const __grid_constant__ FitParams p, int step, float scale, int *status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
+    const int T = p.cfg.steps;
+    const int tc = min(max(step, 0), T - 1);
+    const double lr = (T == 1) ? (double)p.cfg.lr_start
+                               : (double)p.cfg.lr_start + ((double)p.cfg.lr_end - (double)p.cfg.lr_start) * tc / (double)(T - 1);
+    const double tt = (double)(step + 1);
+    const float c1 = (float)(1.0 - pow((double)p.cfg.beta1, tt));
+    const float c2 = (float)(1.0 - pow((double)p.cfg.beta2, tt));
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        float pv[3];
+        for (int k = 0; k < 3; ++k) {
+            const float g = grads[3 * q + k];
+            const float mm = m[3 * q + k] * p.cfg.beta1 + (1.f - p.cfg.beta1) * g;
+            const float vv = v[3 * q + k] * p.cfg.beta2 + (1.f - p.cfg.beta2) * g * g;
+            m[3 * q + k] = mm;
+            v[3 * q + k] = vv;
+            const float s = k < 2 ? scale : 1.f;
+            pv[k] = params[3 * q + k] - s * (float)lr * (mm / c1) / (sqrtf(vv / c2) + p.cfg.eps);
+        }
+        S.off[q] = make_float2(pv[0], pv[1]);
+        S.wp[q] = pv[2];
+    }
+    __syncthreads();
+    const int bad = project(p, S);
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
+        params[3 * q] = S.off[q].x;
+        params[3 * q + 1] = S.off[q].y;
+        params[3 * q + 2] = S.wp[q];
+    }
+    if (threadIdx.x == 0) {
+        status[0] = bad >= 0 ? SKC_EDEGENERATE : SKC_OK;
+        status[1] = bad >= 0 ? bad : 0;
+        status[2] = -1;
+        status[3] = step;
+    }
+}
+
+static int fill_params(FitParams &p, int B, const int *layout, int L, int nmax, int M) {
+    if (B < 1) return fail(SKC_EBADARG, "batch must be positive");
+    if (L < 1 || L > kFitMaxL) return fail(SKC_EBADARG, "fit supports 1..8 layers");
+    if (!layout) return fail(SKC_EBADARG, "null layout");
+    std::memset(&p, 0, sizeof(p));
+    p.B = B;
+    p.L = L;
+    p.nmax = nmax;
+    p.M = M;
+    p.start[0] = 0;
+    for (int l = 0; l < L; ++l) {
+        if (layout[l] < 1 || layout[l] > nmax) return fail(SKC_EBADARG, "layout entries must be 1..nmax");
+        p.layout[l] = layout[l];
+        p.start[l + 1] = p.start[l] + layout[l];
+    }
+    p.P = p.start[L];
+    if (p.P > kFitMaxP) return fail(SKC_EBADARG, "fit supports at most 256 taps per complex");
+    return SKC_OK;
+}
+
+static int set_fit_attrs() {
+    static bool attr = false;
+    const int smem = (int)sizeof(FitSmem);
+    if (!attr) {
+        SKC_CUDA(cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SKC_CUDA(cudaFuncSetAttribute(fit_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SKC_CUDA(cudaFuncSetAttribute(adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    return SKC_OK;
+}
+
+static int fit_launch(const FitParams &p, cudaStream_t s) {
+    int rc = set_fit_attrs();
+    if (rc) return rc;
+    fit_kernel<<<p.B, kFitThreads, sizeof(FitSmem), s>>>(p);
+    SKC_LAUNCH_CHECK("fit_kernel");
+    return SKC_OK;
+}
+
+static int alloc_scratch(FitParams &p, int cap, cudaStream_t s) {
+    p.cap = cap;
+    const size_t bytes = (size_t)p.B * (p.L + 2) * cap * cap * sizeof(float);
+    void *ptr = nullptr;
+    int rc = pool_alloc(&ptr, bytes, s);
+    if (rc) return rc;
+    p.scratch = (float *)ptr;
+    return SKC_OK;
+}
+
+static bool cfg_ok(const skc_fit_cfg *c) {
+    return c && c->steps >= 1 && c->lr_start >= c->lr_end && c->lr_end > 0 &&
+           (c->weight_norm == SKC_WN_NONE || c->weight_norm == SKC_WN_SUM || c->weight_norm == SKC_WN_SOFM) &&
+           (c->loss_kind >= 0 && c->loss_kind <= 2) && c->loss_eps > 0;
+}
+
+}  // namespace skc
+
+using namespace skc;
+
+extern "C" {
+
+int skc_ir_batch(const float *taps, int B, const int *layout, int L, int nmax, int canvas,
+                 float *out, void *stream) {
+    FitParams p;
+    int rc = fill_params(p, B, layout, L, nmax, 1);
+    if (rc) return rc;
+    if (!taps || !out) return fail(SKC_EBADARG, "null pointer");
+    if (canvas < 1 || (canvas & 1) == 0) return fail(SKC_EBADARG, "canvas must be odd");
+    cudaStream_t s = (cudaStream_t)stream;
+    p.mode = MODE_IR;
+    p.canvas_fixed = canvas;
+    p.taps_in = taps;
+    p.ir_out = out;
+    p.cfg.steps = 1;
+    void *st = nullptr;
+    if ((rc = pool_alloc(&st, (size_t)B * 4 * sizeof(int), s))) return rc;
+    p.status = (int *)st;
+    if ((rc = alloc_scratch(p, canvas, s))) { pool_free(st, s); return rc; }
+    rc = fit_launch(p, s);
+    std::vector<int> hs((size_t)B * 4);
+    if (rc == SKC_OK) {
+        cudaError_t e = cudaMemcpyAsync(hs.data(), st, hs.size() * sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "skc_ir_batch status");
+    }
+    pool_free(p.scratch, s);
+    pool_free(st, s);
+    if (rc) return rc;
+    for (int b = 0; b < B; ++b)
+        if (hs[4 * b] == SKC_ENONFINITE)
+            return fail(SKC_ENONFINITE, "non-finite intermediate at layer " + std::to_string(hs[4 * b + 1]));
+    return SKC_OK;
+}
+
+int skc_backward_batch(const float *taps, int B, const int *layout, int L, int nmax,
+                       const float *tgts, int M, int canvas, int loss_kind, float loss_eps,
+                       float *loss, float *grads, int *status, void *stream) {
+    FitParams p;
+    int rc = fill_params(p, B, layout, L, nmax, M);
+    if (rc) return rc;
+    if (!taps || !tgts || !loss || !grads || !status) return fail(SKC_EBADARG, "null pointer");
+    if (canvas < M || (canvas & 1) == 0 || (M & 1) == 0) return fail(SKC_EBADARG, "canvas/target must be odd, canvas >= M");
+    if (loss_kind < 0 || loss_kind > 2 || !(loss_eps > 0)) return fail(SKC_EBADARG, "bad loss kind");
+    cudaStream_t s = (cudaStream_t)stream;
+    p.mode = MODE_BACKWARD;
+    p.canvas_fixed = canvas;
+    p.taps_in = taps;
+    p.tgts = tgts;
+    p.loss_out = loss;
+    p.grads_out = grads;
+    p.status = status;
+    p.cfg.steps = 1;
+    p.cfg.loss_kind = loss_kind;
+    p.cfg.loss_eps = loss_eps;
+    if ((rc = alloc_scratch(p, canvas, s))) return rc;
+    SKC_CUDA(cudaMemsetAsync(grads, 0, (size_t)B * L * nmax * 3 * sizeof(float), s));
+    rc = fit_launch(p, s);
+    pool_free(p.scratch, s);
+    return rc;
+}
+
+int skc_fit_init(float *state, const float *init_taps, int B, const int *layout, int L, int nmax,
+                 int M, const skc_fit_cfg *cfg, int *status, void *stream) {
+    FitParams p;
+    int rc = fill_params(p, B, layout, L, nmax, M);
+    if (rc) return rc;
+    if (!state || !init_taps || !status) return fail(SKC_EBADARG, "null pointer");
+    if (!cfg_ok(cfg)) return fail(SKC_EBADARG, "invalid fit configuration");
+    if (cfg->kws)
+        for (int l = 0; l < L; ++l)
+            if (layout[l] % 4) return fail(SKC_EBADARG, "KWS symmetry needs sample counts divisible by 4");
+    cudaStream_t s = (cudaStream_t)stream;
+    p.mode = MODE_FIT;
+    p.cfg = *cfg;
+    p.state = state;
+    p.status = status;
+    if ((rc = set_fit_attrs())) return rc;
+    fit_init_kernel<<<B, kFitThreads, sizeof(FitSmem), s>>>(p, init_taps);
+    SKC_LAUNCH_CHECK("fit_init_kernel");
+    return SKC_OK;
+}
+
+int skc_fit_run(float *state, int B, const int *layout, int L, int nmax, const float *tgts, int M,
+                const skc_fit_cfg *cfg, float *trace, int *status, void *stream) {
+    FitParams p;
+    int rc = fill_params(p, B, layout, L, nmax, M);
+    if (rc) return rc;
+    if (!state || !tgts || !trace || !status) return fail(SKC_EBADARG, "null pointer");
+    if (!cfg_ok(cfg)) return fail(SKC_EBADARG, "invalid fit configuration");
+    cudaStream_t s = (cudaStream_t)stream;
+    p.mode = MODE_FIT;
+    p.cfg = *cfg;
+    p.state = state;
+    p.tgts = tgts;
+    p.trace = trace;
+    p.status = status;
+    const size_t stride = SKC_FIT_STATE_FLOATS(L, nmax);
+    std::vector<int> hdr((size_t)B * 4), hs((size_t)B * 4);
+    // scratch capacity from the current canvases (+ growth slack); kernels
+    // that outgrow it park with kNeedGrow and are resumed with a larger one
+    for (int attempt = 0; attempt < 64; ++attempt) {
+        SKC_CUDA(cudaMemcpy2DAsync(hdr.data(), 4 * sizeof(int), state, stride * sizeof(float),
+                                   4 * sizeof(int), B, cudaMemcpyDeviceToHost, s));
+        SKC_CUDA(cudaStreamSynchronize(s));
+        int cap = 1;
+        for (int b = 0; b < B; ++b) cap = std::max(cap, hdr[4 * b + 1]);
+        cap += 32 + attempt * 64;
+        if ((rc = alloc_scratch(p, cap, s))) return rc;
+        rc = fit_launch(p, s);
+        if (rc == SKC_OK) {
+            cudaError_t e = cudaMemcpyAsync(hs.data(), status, hs.size() * sizeof(int),
+                                            cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) rc = cuda_fail(e, "skc_fit_run status");
+        }
+        pool_free(p.scratch, s);
+        if (rc) return rc;
+        bool again = false;
+        for (int b = 0; b < B; ++b) again |= hs[4 * b] == kNeedGrow;
+        if (!again) return SKC_OK;
+    }
+    return fail(SKC_ECUDA, "fit canvas kept growing (diverging fit?)");
+}
+
+int skc_adam_step(float *params, const float *grads, float *m, float *v, const int *layout, int L,
+                  int step_index, const skc_fit_cfg *cfg, float offset_lr_scale, int *status,
+                  void *stream) {
+    FitParams p;
+    int nmax = 1;
+    for (int l = 0; layout && l < L; ++l) nmax = std::max(nmax, layout[l]);
+    int rc = fill_params(p, 1, layout, L, nmax, 1);
+    if (rc) return rc;
+    if (!params || !grads || !m || !v || !status) return fail(SKC_EBADARG, "null pointer");
+    if (!cfg_ok(cfg)) return fail(SKC_EBADARG, "invalid fit configuration");
+    if (cfg->kws)
+        for (int l = 0; l < L; ++l)
+            if (layout[l] % 4) return fail(SKC_EBADARG, "KWS symmetry needs sample counts divisible by 4");
+    p.cfg = *cfg;
+    if ((rc = set_fit_attrs())) return rc;
+    adam_kernel<<<1, kFitThreads, sizeof(FitSmem), (cudaStream_t)stream>>>(
+        params, grads, m, v, p, step_index, offset_lr_scale, status);
+    SKC_LAUNCH_CHECK("adam_kernel");
+    return SKC_OK;
+}
+
+}  // extern "C"

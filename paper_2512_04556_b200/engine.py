@@ -1,0 +1,266 @@
+"""Uniform sparse-layer filtering and impulse responses on the B200.
+
+Drop-in for the reference engine (/root/reference/pkg/src/sparsekern/
+engine.py): same types, names, validation and errors; the arithmetic runs in
+libskc.so (csrc/skc_filter.cu, csrc/skc_fit.cu) through the C ABI.  New
+keywords: `boundary` ("zero" = the reference's zero padding, "clamp" =
+clamp-to-edge for BASELINE config 0) and the batched `apply_complex_batch`.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from ._tensors import Image, torch
+from .kernels import DenseKernel
+
+__all__ = [
+    "EngineError",
+    "TruncationError",
+    "SparseLayer",
+    "KernelComplex",
+    "apply_sparse_layer",
+    "apply_complex",
+    "apply_complex_batch",
+    "synthesize_ir",
+    "synthesize_ir_batch",
+    "required_canvas",
+    "auto_canvas",
+    "psnr",
+    "sse",
+    "BOUNDARIES",
+]
+
+BOUNDARIES = {"zero": nat.SKC_ZERO, "clamp": nat.SKC_CLAMP}
+
+
+class EngineError(ValueError):
+    """engine.py:35-36"""
+
+
+class TruncationError(EngineError):
+    """Requested impulse-response canvas cannot hold the composed support (engine.py:39-40)."""
+
+
+@dataclass(frozen=True, eq=False)
+class SparseLayer:
+    """N taps: offsets (N, 2) as (ox, oy) pixels and weights (N,) (engine.py:43-71)."""
+
+    offsets: np.ndarray
+    weights: np.ndarray
+
+    def __post_init__(self):
+        off = np.array(self.offsets, dtype=np.float64, copy=True).reshape(-1, 2)
+        wts = np.array(self.weights, dtype=np.float64, copy=True).reshape(-1)
+        if off.shape[0] < 1:
+            raise EngineError("sparse layer needs at least one sample")
+        if off.shape[0] != wts.shape[0]:
+            raise EngineError(f"offset/weight count mismatch: {off.shape[0]} vs {wts.shape[0]}")
+        if not (np.isfinite(off).all() and np.isfinite(wts).all()):
+            raise EngineError("sparse layer parameters must be finite")
+        off.flags.writeable = False
+        wts.flags.writeable = False
+        object.__setattr__(self, "offsets", off)
+        object.__setattr__(self, "weights", wts)
+
+    @property
+    def sample_count(self) -> int:
+        return int(self.offsets.shape[0])
+
+    @property
+    def reach(self) -> float:
+        """Max Chebyshev extent of the offsets."""
+        return float(np.abs(self.offsets).max())
+
+    def taps(self) -> np.ndarray:
+        """(N, 3) float64 rows (ox, oy, w) -- the C ABI's tap table."""
+        return np.ascontiguousarray(np.concatenate([self.offsets, self.weights[:, None]], axis=1))
+
+
+@dataclass(frozen=True, eq=False)
+class KernelComplex:
+    """Layers applied input to output (engine.py:74-103)."""
+
+    layers: tuple
+
+    def __post_init__(self):
+        layers = tuple(self.layers)
+        if len(layers) < 1:
+            raise EngineError("kernel complex needs at least one layer")
+        if not all(isinstance(l, SparseLayer) for l in layers):
+            raise EngineError("kernel complex layers must be SparseLayer instances")
+        object.__setattr__(self, "layers", layers)
+
+    @property
+    def layer_count(self) -> int:
+        return len(self.layers)
+
+    @property
+    def layout(self) -> tuple:
+        return tuple(l.sample_count for l in self.layers)
+
+    @property
+    def total_samples(self) -> int:
+        return sum(self.layout)
+
+    @property
+    def reach(self) -> float:
+        return sum(l.reach for l in self.layers)
+
+    def taps(self) -> np.ndarray:
+        return np.ascontiguousarray(np.concatenate([l.taps() for l in self.layers], axis=0))
+
+    def padded(self, nmax: int | None = None) -> np.ndarray:
+        """(L, nmax, 3) float32 (ox, oy, w), zero-padded (zero weights are inert)."""
+        nmax = max(self.layout) if nmax is None else nmax
+        out = np.zeros((self.layer_count, nmax, 3), dtype=np.float32)
+        for l, lay in enumerate(self.layers):
+            out[l, :lay.sample_count] = lay.taps()
+        return out
+
+
+def _boundary(boundary) -> int:
+    try:
+        return BOUNDARIES[boundary]
+    except KeyError:
+        raise EngineError(f"boundary must be one of {sorted(BOUNDARIES)}, got {boundary!r}") from None
+
+
+def _raise(rc: int, what: str):
+    msg = f"{what}: {nat.last_error()}"
+    if rc == nat.SKC_EBADARG:
+        raise EngineError(msg)
+    if rc == nat.SKC_ETRUNC:
+        raise TruncationError(msg)
+    raise nat.NativeError(rc, msg)
+
+
+def apply_sparse_layer(img, layer: SparseLayer, boundary: str = "zero"):
+    """out[y,x] = sum_i w_i bilinear(img, x+ox_i, y+oy_i) (engine.py:160-170)."""
+    lib = nat.lib()
+    im = Image(img)
+    b, h, w, c = im.dims
+    out = im.empty_like()
+    taps = layer.taps()
+    rc = lib.skc_layer_fwd(nat.ptr(im.tensor), im.dtype_id, nat.ptr(out), im.dtype_id, b, h, w, c,
+                           nat.dbl(taps), taps.shape[0], _boundary(boundary), nat.stream_ptr())
+    if rc:
+        _raise(rc, "apply_sparse_layer")
+    return im.restore(out)
+
+
+def _chain(im: Image, cpx: KernelComplex, boundary: str, out_dtype=None):
+    lib = nat.lib()
+    b, h, w, c = im.dims
+    out = im.empty_like(out_dtype)
+    odt = nat.SKC_F16 if out.dtype == torch().float16 else nat.SKC_F32
+    taps = cpx.taps()
+    layout = np.ascontiguousarray(cpx.layout, dtype=np.int32)
+    rc = lib.skc_chain_fwd(nat.ptr(im.tensor), im.dtype_id, nat.ptr(out), odt, b, h, w, c,
+                           nat.dbl(taps), nat.ints(layout), layout.size, _boundary(boundary),
+                           nat.stream_ptr())
+    if rc:
+        _raise(rc, "apply_complex")
+    return out
+
+
+def apply_complex(img, cpx: KernelComplex, boundary: str = "zero"):
+    """All layers in order (engine.py:173-178); intermediates stay fp32 on device."""
+    im = Image(img)
+    return im.restore(_chain(im, cpx, boundary))
+
+
+def apply_complex_batch(imgs, cpx: KernelComplex, boundary: str = "zero", out=None):
+    """Batched frames (B, H, W[, C]) through one complex in a single call per layer."""
+    im = Image(imgs, batched=True)
+    res = _chain(im, cpx, boundary)
+    if out is not None:
+        if isinstance(out, np.ndarray):
+            out[...] = im.restore(res)
+        else:
+            out.copy_(res.view(out.shape))
+        return out
+    return im.restore(res)
+
+
+def required_canvas(cpx: KernelComplex) -> int:
+    """Smallest odd canvas for the composed response (engine.py:181-183)."""
+    return 2 * math.ceil(cpx.reach) + 1
+
+
+def auto_canvas(cpx: KernelComplex) -> int:
+    """required_canvas plus a 2-pixel guard (engine.py:186-188)."""
+    return required_canvas(cpx) + 4
+
+
+def _ir_device(padded: np.ndarray, layout, canvas: int):
+    """padded (B, L, nmax, 3) float32 -> (B, canvas, canvas) CUDA float32."""
+    t = torch()
+    lib = nat.lib()
+    taps = t.from_numpy(np.ascontiguousarray(padded, dtype=np.float32)).cuda()
+    bsz, nl, nmax, _ = padded.shape
+    out = t.empty((bsz, canvas, canvas), dtype=t.float32, device=taps.device)
+    lay = np.ascontiguousarray(layout, dtype=np.int32)
+    rc = lib.skc_ir_batch(nat.ptr(taps), bsz, nat.ints(lay), nl, nmax, canvas, nat.ptr(out),
+                          nat.stream_ptr())
+    if rc == nat.SKC_ENONFINITE:
+        raise EngineError(f"synthesize_ir: {nat.last_error()}")
+    if rc:
+        _raise(rc, "synthesize_ir")
+    return out
+
+
+def synthesize_ir(cpx: KernelComplex, canvas: int | None = None) -> DenseKernel:
+    """Impulse response on a centred delta canvas (engine.py:191-209)."""
+    if canvas is None:
+        canvas = auto_canvas(cpx)
+    else:
+        if canvas % 2 == 0:
+            raise EngineError(f"canvas must be odd, got {canvas}")
+        if canvas < required_canvas(cpx):
+            raise TruncationError(f"canvas {canvas} would truncate impulse response "
+                                  f"(needs >= {required_canvas(cpx)})")
+    ir = _ir_device(cpx.padded()[None], cpx.layout, canvas)
+    return DenseKernel(ir[0].cpu().numpy().astype(np.float64))
+
+
+def synthesize_ir_batch(offsets, weights, canvas: int) -> np.ndarray:
+    """Batched responses (engine.py:251-303): offsets (B,L,N,2), weights (B,L,N)."""
+    off = np.asarray(offsets, dtype=np.float64)
+    wts = np.asarray(weights, dtype=np.float64)
+    bsz, nl, ns, _ = off.shape
+    if canvas % 2 == 0:
+        raise EngineError(f"canvas must be odd, got {canvas}")
+    padded = np.concatenate([off, wts[..., None]], axis=-1).astype(np.float32)
+    ir = _ir_device(padded, (ns,) * nl, canvas)
+    return ir.cpu().numpy().astype(np.float64)
+
+
+def sse(a, b) -> float:
+    """Sum of squared differences (engine.py:306-313); host metric."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise EngineError(f"dimension mismatch: {a.shape} vs {b.shape}")
+    d = a - b
+    return float(np.sum(d * d))
+
+
+PSNR_CAP_DB = 99.0
+
+
+def psnr(a, b) -> float:
+    """PSNR with peak max(|a|, 1), capped at 99 dB (engine.py:316-329); host metric."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise EngineError(f"dimension mismatch: {a.shape} vs {b.shape}")
+    peak = max(float(np.abs(a).max(initial=0.0)), 1.0)
+    mse = float(np.mean((a - b) ** 2))
+    if mse == 0.0:
+        return PSNR_CAP_DB
+    return min(PSNR_CAP_DB, 10.0 * math.log10(peak * peak / mse))

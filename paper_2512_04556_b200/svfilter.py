@@ -1,0 +1,142 @@
+"""Spatially varying filtering through filter-space interpolation, on the B200.
+
+Drop-in for the reference svfilter (/root/reference/pkg/src/sparsekern/
+svfilter.py): `FilterBasis`, `interp_weights`, `synthesize_filter` and
+`sv_filter` keep the reference names, validation and semantics; the per-pixel
+bracket, slotwise lerp of offsets/weights and the bilinear gather of every
+pass run in csrc/skc_filter.cu (sv_tile_kernel) through `skc_sv_fwd`.
+Offline basis building (`build_basis`, a loop over `fit`) lives in optim's
+batched fit; `sv_ground_truth` and the 2-D grid basis are SURVEY section 8(f)
+"next" rows.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from ._tensors import Image, torch
+from .engine import BOUNDARIES, EngineError, KernelComplex, SparseLayer
+
+__all__ = [
+    "FilterBasis",
+    "interp_weights",
+    "synthesize_filter",
+    "sv_filter",
+    "stacked_params",
+]
+
+
+def _check_shared_layout(filters) -> tuple:
+    layouts = {f.layout for f in filters}
+    if len(layouts) != 1:
+        raise EngineError(f"basis filters must share one layout, got {sorted(layouts)}")
+    return layouts.pop()
+
+
+@dataclass(frozen=True, eq=False)
+class FilterBasis:
+    """Basis complexes at strictly increasing scalar parameters (svfilter.py:53-78)."""
+
+    params: np.ndarray
+    filters: tuple
+
+    def __post_init__(self):
+        ps = np.array(self.params, dtype=np.float64).reshape(-1)
+        filters = tuple(self.filters)
+        if ps.size != len(filters) or ps.size < 1:
+            raise EngineError("basis needs one filter per parameter")
+        if ps.size > 1 and not (np.diff(ps) > 0).all():
+            raise EngineError("basis parameters must be strictly increasing")
+        _check_shared_layout(filters)
+        ps.flags.writeable = False
+        object.__setattr__(self, "params", ps)
+        object.__setattr__(self, "filters", filters)
+
+    @property
+    def size(self) -> int:
+        return int(self.params.size)
+
+    @property
+    def layout(self) -> tuple:
+        return self.filters[0].layout
+
+
+def _bracket(p, ps: np.ndarray):
+    """Bracketing entries and blend factor (svfilter.py:129-137), host version
+    used by interp_weights; the per-pixel version runs on device."""
+    if ps.size == 1:
+        z = np.zeros_like(p, dtype=np.int64)
+        return z, z, np.zeros_like(p, dtype=np.float64)
+    pc = np.clip(p, ps[0], ps[-1])
+    k0 = np.clip(np.searchsorted(ps, pc, side="right") - 1, 0, ps.size - 2)
+    t = (pc - ps[k0]) / (ps[k0 + 1] - ps[k0])
+    return k0, k0 + 1, t
+
+
+def interp_weights(p: float, basis: FilterBasis) -> np.ndarray:
+    """Hat weights over the grid, at most 2 nonzeros (svfilter.py:116-126)."""
+    alpha = np.zeros(basis.size)
+    k0, k1, t = _bracket(np.asarray(p, dtype=np.float64), basis.params)
+    alpha[int(k0)] += 1.0 - float(t)
+    alpha[int(k1)] += float(t)
+    return alpha
+
+
+def synthesize_filter(alpha, basis: FilterBasis) -> KernelComplex:
+    """Slotwise convex blend of the basis (svfilter.py:140-152)."""
+    alpha = np.asarray(alpha, dtype=np.float64).reshape(-1)
+    if alpha.size != basis.size:
+        raise EngineError(f"alpha has {alpha.size} entries for a basis of {basis.size}")
+    if abs(float(alpha.sum()) - 1.0) > 1e-9 or (alpha < -1e-12).any():
+        raise EngineError("alpha must be convex: nonnegative and summing to 1")
+    layers = []
+    for l in range(len(basis.layout)):
+        off = sum(a * f.layers[l].offsets for a, f in zip(alpha, basis.filters))
+        wts = sum(a * f.layers[l].weights for a, f in zip(alpha, basis.filters))
+        layers.append(SparseLayer(off, wts))
+    return KernelComplex(tuple(layers))
+
+
+def stacked_params(basis: FilterBasis) -> np.ndarray:
+    """(Mb, L, Nmax, 3) float64 (ox, oy, w), zero-padded (svfilter.py:155-168)."""
+    layout = basis.layout
+    out = np.zeros((basis.size, len(layout), max(layout), 3))
+    for k, f in enumerate(basis.filters):
+        for l, lay in enumerate(f.layers):
+            out[k, l, :lay.sample_count] = lay.taps()
+    return out
+
+
+def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero"):
+    """Per-pixel blended sparse filtering guided by a parameter map (svfilter.py:171-203).
+
+    Each pass re-interpolates that layer's taps per pixel between the two
+    bracketing basis entries and gathers bilinearly from the previous pass.
+    """
+    t = torch()
+    lib = nat.lib()
+    im = Image(img)
+    b, h, w, c = im.dims
+    pm_shape = tuple(pmap.shape)
+    if pm_shape != (h, w):
+        raise EngineError(f"parameter map {pm_shape} must match image {(h, w)}")
+    if isinstance(pmap, t.Tensor):
+        pm = pmap.to(device=im.tensor.device, dtype=t.float32).contiguous()
+    else:
+        pm = t.from_numpy(np.ascontiguousarray(pmap, dtype=np.float32)).to(im.tensor.device)
+    if boundary not in BOUNDARIES:
+        raise EngineError(f"boundary must be one of {sorted(BOUNDARIES)}, got {boundary!r}")
+    stack = np.ascontiguousarray(stacked_params(basis))
+    ps = np.ascontiguousarray(basis.params, dtype=np.float64)
+    layout = np.ascontiguousarray(basis.layout, dtype=np.int32)
+    out = im.empty_like()
+    rc = lib.skc_sv_fwd(nat.ptr(im.tensor), im.dtype_id, nat.ptr(out), im.dtype_id, h, w, c,
+                        nat.ptr(pm), nat.dbl(ps), ps.size, nat.dbl(stack), stack.shape[2],
+                        nat.ints(layout), layout.size, BOUNDARIES[boundary], nat.stream_ptr())
+    if rc == nat.SKC_EBADARG:
+        raise EngineError(f"sv_filter: {nat.last_error()}")
+    nat.check(rc, "sv_filter")
+    return im.restore(out)

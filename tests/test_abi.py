@@ -1,0 +1,52 @@
+"""The C-ABI library builds, loads and exports exactly what include/skc.h declares (CPU only)."""
+
+import re
+import subprocess
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "skc.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*|size_t)\s*\*?\s*(skc_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entry_points():
+    names = declared_symbols()
+    assert "skc_chain_fwd" in names and "skc_fit_run" in names and len(names) >= 10
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_2512_04556_b200 import _build, _native
+    lib_path = _build.build()
+    lib = _native.load_library()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert set(declared_symbols()) == set(_native.EXPORTS)
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(lib_path)], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (skc_\w+)", nm))
+    assert set(declared_symbols()) <= exported
+    assert lib.skc_version() == 100
+    assert lib.skc_max_taps() >= 128
+
+
+def test_sm100a_cubin_in_library():
+    from paper_2512_04556_b200 import _build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_build.LIB)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_bad_arguments_fail_without_a_device():
+    """Argument validation happens before any CUDA call."""
+    import ctypes
+    import numpy as np
+    from paper_2512_04556_b200 import _native as nat
+    lib = nat.load_library()
+    taps = np.zeros((1, 3))
+    rc = lib.skc_layer_fwd(None, 0, None, 0, 1, 4, 4, 3, nat.dbl(taps), 1, 0, None)
+    assert rc == nat.SKC_EBADARG
+    assert b"null" in lib.skc_last_error()
+    rc = lib.skc_layer_fwd(ctypes.c_void_p(16), 0, ctypes.c_void_p(16), 0, 1, 4, 4, 7, nat.dbl(taps), 1, 0, None)
+    assert rc == nat.SKC_EBADARG

@@ -1,0 +1,199 @@
+"""GPU parity: uniform filtering and impulse responses through the C ABI.
+
+Tolerance (north star / SURVEY D7): normwise max|gpu - ref| <= 1e-5 max|ref|
+for fp32 storage, 2e-3 for fp16 storage.  References are the reference's own
+outputs (tests/golden) and the float64 oracle on the same fp32 inputs.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import normwise, split_layers
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 1e-5
+TOL16 = 2e-3
+
+
+@pytest.fixture(scope="module")
+def skc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2512_04556_b200 as m
+    assert m.HAVE_CUDA
+    return m
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle
+    return oracle
+
+
+def cpx_from(skc, off, w, layout):
+    return skc.KernelComplex(tuple(skc.SparseLayer(o, ww) for o, ww in split_layers(off, w, layout)))
+
+
+def test_golden_complexes_zero_and_clamp(skc, golden):
+    g = golden("engine")
+    for k in range(6):
+        cpx = cpx_from(skc, g[f"c{k}_off"], g[f"c{k}_w"], g[f"c{k}_layout"])
+        img = g[f"c{k}_img"]
+        assert normwise(skc.apply_complex(img, cpx), g[f"c{k}_zero"]) < TOL32
+        assert normwise(skc.apply_complex(img, cpx, boundary="clamp"), g[f"c{k}_clamp"]) < TOL32
+        assert normwise(skc.apply_sparse_layer(img, cpx.layers[0]), g[f"c{k}_layer0"]) < TOL32
+    cpx = cpx_from(skc, g["k_off"], g["k_w"], g["k_layout"])
+    assert normwise(skc.apply_complex(g["k_img"], cpx), g["k_zero"]) < TOL32
+    assert normwise(skc.apply_complex(g["k_img"], cpx, "clamp"), g["k_clamp"]) < TOL32
+
+
+def test_reference_known_answers(skc):
+    # test_engine.py:84-105 -- integer shift, half-pixel mean, duplicate taps
+    rng = np.random.default_rng(7)
+    img = rng.uniform(size=(6, 7))
+    out = skc.apply_sparse_layer(img, skc.SparseLayer(np.array([[1.0, 0.0]]), np.array([1.0])))
+    np.testing.assert_allclose(out[:, :-1], img[:, 1:], rtol=1e-6)
+    assert np.all(out[:, -1] == 0)
+    img = rng.uniform(size=(5, 6))
+    out = skc.apply_sparse_layer(img, skc.SparseLayer(np.array([[0.5, 0.0]]), np.array([1.0])))
+    expect = 0.5 * img.copy()
+    expect[:, :-1] += 0.5 * img[:, 1:]
+    np.testing.assert_allclose(out, expect, atol=1e-6)
+    out = skc.apply_sparse_layer(img, skc.SparseLayer(np.zeros((2, 2)), np.array([0.5, 0.5])))
+    np.testing.assert_allclose(out, img, rtol=1e-6)
+
+
+def test_c0_full_size_both_boundaries(skc, orc):
+    from paper_2512_04556_b200 import synth
+    img = synth.c0_image()
+    cpx = synth.c0_complex()
+    layers = [(l.offsets, l.weights) for l in cpx.layers]
+    for mode, oid in (("clamp", orc.CLAMP), ("zero", orc.ZERO)):
+        ref = orc.apply_complex(img.astype(np.float64), layers, oid)
+        assert normwise(skc.apply_complex(img, cpx, boundary=mode), ref) < TOL32
+
+
+def test_c1_frame_and_batch_consistency(skc, orc):
+    import torch
+    from paper_2512_04556_b200 import synth
+    cpx = synth.c1_complex()
+    frames = np.stack([synth.c1_frame(b) for b in (0, 1)])
+    dev = torch.from_numpy(frames).cuda()
+    batched = skc.apply_complex_batch(dev, cpx)
+    single = skc.apply_complex(dev[1], cpx)
+    assert torch.equal(batched[1], single)           # batching never changes a frame
+    layers = [(l.offsets, l.weights) for l in cpx.layers]
+    # oracle on a 512-row window of frame 0: the bottom 3*34 rows are exact
+    # because the complex's corner reach is 3+5+9+17 = 34 px per layer chain
+    win = frames[0, :600].astype(np.float64)
+    ref = orc.apply_complex(win, layers, orc.ZERO)
+    got = batched[0, :600].cpu().numpy()
+    assert normwise(got[:600 - 34 * 4 - 1], ref[:600 - 34 * 4 - 1]) < TOL32
+
+
+def test_fp16_storage_kawase(skc, orc):
+    from paper_2512_04556_b200 import synth
+    cpx = synth.kawase_complex()
+    frame = synth.value_noise_frame(200, 260, 4, seed=5, rects=20, dtype=np.float16)
+    out = skc.apply_complex(frame, cpx)
+    assert out.dtype == np.float16
+    ref = orc.apply_complex(frame.astype(np.float64), [(l.offsets, l.weights) for l in cpx.layers])
+    assert normwise(out.astype(np.float64), ref) < TOL16
+    outc = skc.apply_complex(frame, cpx, boundary="clamp")
+    refc = orc.apply_complex(frame.astype(np.float64), [(l.offsets, l.weights) for l in cpx.layers],
+                             orc.CLAMP)
+    assert normwise(outc.astype(np.float64), refc) < TOL16
+
+
+def test_many_taps_chunked(skc, orc):
+    rng = np.random.default_rng(11)
+    n = 600  # > skc_max_taps: exercises accumulate chunks
+    off = rng.uniform(-4, 4, (n, 2)).astype(np.float32).astype(np.float64)
+    w = rng.uniform(0, 1, n)
+    w /= w.sum()
+    lay = skc.SparseLayer(off, w)
+    img = rng.random((40, 50, 2)).astype(np.float32)
+    ref = orc.apply_layer(img.astype(np.float64), off, w)
+    assert normwise(skc.apply_sparse_layer(img, lay), ref) < TOL32
+    h = skc.apply_sparse_layer(img.astype(np.float16), lay)
+    assert normwise(h.astype(np.float64), ref) < TOL16
+
+
+def test_huge_reach_direct_path(skc, orc):
+    rng = np.random.default_rng(12)
+    off = np.array([[150.25, -3.5], [-140.75, 120.5], [0.5, 0.25]])
+    w = np.array([0.3, 0.3, 0.4])
+    img = rng.random((310, 300, 3)).astype(np.float32)
+    lay = skc.SparseLayer(off, w)
+    for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+        ref = orc.apply_layer(img.astype(np.float64), off, w, oid)
+        assert normwise(skc.apply_sparse_layer(img, lay, boundary=mode), ref) < TOL32
+
+
+def test_ragged_and_tiny_images(skc, orc):
+    rng = np.random.default_rng(13)
+    for shape in [(1, 1), (1, 17), (33, 1, 3), (7, 5, 4), (65, 129, 1)]:
+        img = rng.random(shape).astype(np.float32)
+        cpx = skc.KernelComplex((skc.SparseLayer(rng.uniform(-3, 3, (5, 2)), rng.random(5)),
+                                 skc.SparseLayer(rng.uniform(-2, 2, (3, 2)), rng.random(3))))
+        layers = [(l.offsets, l.weights) for l in cpx.layers]
+        for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+            ref = orc.apply_complex(img.astype(np.float64), layers, oid)
+            got = skc.apply_complex(img, cpx, boundary=mode)
+            assert got.shape == img.shape
+            assert normwise(got, ref) < TOL32, (shape, mode)
+
+
+def test_linearity_and_conservation_full_size(skc):
+    import torch
+    from paper_2512_04556_b200 import synth
+    cpx = synth.c1_complex()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.rand((2665, 1264, 3), device="cuda", generator=g)
+    b = torch.rand((2665, 1264, 3), device="cuda", generator=g)
+    lhs = skc.apply_complex(1.5 * a - 0.25 * b, cpx)
+    rhs = 1.5 * skc.apply_complex(a, cpx) - 0.25 * skc.apply_complex(b, cpx)
+    assert (lhs - rhs).abs().max().item() < 1e-5 * rhs.abs().max().item()
+    # unit-sum layers conserve mass of an interior-supported image
+    img = torch.zeros((600, 600, 3), device="cuda")
+    img[250:350, 250:350] = torch.rand((100, 100, 3), device="cuda", generator=g)
+    out = skc.apply_complex(img, cpx)
+    assert abs(out.double().sum().item() / img.double().sum().item() - 1.0) < 1e-5
+
+
+def test_ir_goldens(skc, golden):
+    g = golden("ir")
+    for k in range(4):
+        cpx = cpx_from(skc, g[f"i{k}_off"], g[f"i{k}_w"], g[f"i{k}_layout"])
+        ir = skc.synthesize_ir(cpx)
+        assert ir.size == int(g[f"i{k}_canvas"])
+        assert normwise(ir.weights, g[f"i{k}_ir"]) < TOL32
+    kaw = skc.KernelComplex(tuple(
+        skc.SparseLayer(np.array([[r, r], [-r, r], [-r, -r], [r, -r]]), np.full(4, 0.25))
+        for r in (0.5 + l for l in range(6))))
+    assert normwise(skc.synthesize_ir(kaw).weights, g["kawase_auto"]) < TOL32
+    assert normwise(skc.synthesize_ir(kaw, canvas=61).weights, g["kawase_61"]) < TOL32
+    irs = skc.synthesize_ir_batch(g["batch_off"], g["batch_w"], 41)
+    assert normwise(irs, g["batch_ir"]) < TOL32
+
+
+def test_ir_errors(skc):
+    layer = skc.SparseLayer(np.array([[3.0, 0.0]]), np.array([1.0]))
+    cpx = skc.KernelComplex((layer,))
+    with pytest.raises(skc.TruncationError):
+        skc.synthesize_ir(cpx, canvas=5)
+    assert skc.synthesize_ir(cpx, canvas=7).size == 7
+    with pytest.raises(skc.EngineError):
+        skc.synthesize_ir(cpx, canvas=8)
+
+
+def test_torch_in_torch_out_zero_copy(skc):
+    import torch
+    x = torch.rand((64, 70, 3), device="cuda")
+    cpx = skc.KernelComplex((skc.SparseLayer(np.array([[0.25, -1.5]]), np.array([1.0])),))
+    y = skc.apply_complex(x, cpx)
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.shape == x.shape
+    h = skc.apply_complex(x.half(), cpx)
+    assert h.dtype == torch.float16
