@@ -1,0 +1,131 @@
+"""Host-side logic of the package (no GPU): types, validation, rasterisers, recipes."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2512_04556_b200 as skc
+from paper_2512_04556_b200 import synth
+from paper_2512_04556_b200.svfilter import _bracket, stacked_params
+
+
+def test_rasterisers_bit_exact_vs_reference(golden):
+    g = golden("kernels")
+    r, rot = g["params"]
+    assert np.array_equal(skc.disk_kernel(60.0, 129).weights, g["disk_60_129"])
+    assert np.array_equal(skc.polygon_kernel(4, r, 129, rot).weights, g["square_129"])
+    assert np.array_equal(skc.polygon_kernel(6, r, 129, rot).weights, g["hex_129"])
+    assert np.array_equal(skc.ring_kernel(0.6 * r, r, 129).weights, g["ring_129"])
+    assert np.array_equal(skc.star_kernel(4, r, 129, rotation=rot).weights, g["star_129"])
+    assert np.array_equal(skc.disk_kernel(2.5).weights, g["disk_7"])
+    assert np.array_equal(skc.gaussian_kernel(1.5).weights, g["gauss_15"])
+    assert np.array_equal(skc.gaussian_kernel(1.7, 11).weights, g["gauss_2_11"])
+
+
+def test_dense_kernel_invariants():
+    k = skc.DenseKernel(np.ones((3, 3)))
+    assert k.normalized().weights.sum() == pytest.approx(1.0)
+    e = k.embedded(7)
+    assert e.size == 7 and e.weights[2:5, 2:5].sum() == 9
+    with pytest.raises(skc.KernelError):
+        skc.DenseKernel(np.ones((4, 4)))
+    with pytest.raises(skc.KernelError):
+        k.embedded(2)
+    with pytest.raises(skc.KernelError):
+        skc.disk_kernel(10.0, 21)   # violates the one-pixel border
+
+
+def test_layer_and_complex_validation():
+    with pytest.raises(skc.EngineError):
+        skc.SparseLayer(np.zeros((0, 2)), np.zeros(0))
+    with pytest.raises(skc.EngineError):
+        skc.SparseLayer(np.array([[np.inf, 0.0]]), np.array([1.0]))
+    with pytest.raises(skc.EngineError):
+        skc.KernelComplex(())
+    lay = skc.SparseLayer(np.array([[1.2, -0.4]]), np.array([1.0]))
+    cpx = skc.KernelComplex((lay, lay))
+    assert skc.required_canvas(cpx) == 7 and skc.auto_canvas(cpx) == 11
+    assert cpx.taps().shape == (2, 3) and cpx.padded(4).shape == (2, 4, 3)
+
+
+def test_config_recipes_deterministic_and_in_range():
+    a = synth.disk_complex(4, 32, seed=1)
+    b = synth.disk_complex(4, 32, seed=1)
+    for la, lb in zip(a.layers, b.layers):
+        assert np.array_equal(la.offsets, lb.offsets)
+    for l, lay in enumerate(a.layers):
+        assert np.hypot(*lay.offsets.T).max() <= 2 * 2 ** l + 1e-5
+        assert abs(lay.weights.sum() - 1) < 1e-6 and (lay.weights > 0).all()
+    kaw = synth.kawase_complex()
+    assert kaw.layout == (4,) * 6 and kaw.reach == sum(0.5 + l for l in range(6))
+    basis = synth.c2_basis()
+    st = stacked_params(basis)
+    np.testing.assert_allclose(st[2, :, :, :2], 4 * st[0, :, :, :2], rtol=1e-6, atol=1e-6)
+    f = synth.value_noise_frame(300, 200, 3, seed=4)
+    assert f.dtype == np.float32 and f.min() >= 0 and f.max() == 1.0
+    assert np.array_equal(f, synth.value_noise_frame(300, 200, 3, seed=4))
+    pm = synth.c2_pmap(200, 150)
+    assert pm.min() >= 0 and pm.max() <= 1
+    for i in range(5):
+        t = synth.c4_target(i)
+        assert t.size == 129 and abs(t.weights.sum() - 1) < 1e-12
+
+
+def test_bracket_and_interp(golden):
+    g = golden("sv")
+    k0, k1, t = _bracket(g["bracket_p"], g["params"])
+    assert np.array_equal(k0, g["bracket_k0"]) and np.array_equal(t, g["bracket_t"])
+    basis = synth.c2_basis()
+    np.testing.assert_array_equal(skc.interp_weights(0.5, basis), [0, 1, 0])
+    np.testing.assert_allclose(skc.interp_weights(0.25, basis), [0.5, 0.5, 0])
+    np.testing.assert_array_equal(skc.interp_weights(-3, basis), [1, 0, 0])
+    np.testing.assert_array_equal(skc.interp_weights(9, basis), [0, 0, 1])
+    f = skc.synthesize_filter([0, 0, 1], basis)
+    assert np.array_equal(f.layers[0].offsets, basis.filters[2].layers[0].offsets)
+    with pytest.raises(skc.EngineError, match="convex"):
+        skc.synthesize_filter([0.7, 0.6, -0.3], basis)
+    with pytest.raises(skc.EngineError, match="increasing"):
+        skc.FilterBasis(np.array([1.0, 1.0]), basis.filters[:2])
+
+
+def test_train_config_and_layout():
+    cfg = skc.TrainConfig(steps=101, lr_start=1e-3, lr_end=1e-4)
+    assert cfg.lr_at(0) == 1e-3
+    assert cfg.lr_at(100) == pytest.approx(1e-4)
+    assert cfg.lr_at(50) == pytest.approx((1e-3 + 1e-4) / 2)
+    assert skc.parse_layout("4x32") == (32,) * 4
+    for bad in ("0x4", "12", "3x-2"):
+        with pytest.raises(skc.OptimError):
+            skc.parse_layout(bad)
+    with pytest.raises(skc.OptimError):
+        skc.LossKind("huber")
+    with pytest.raises(skc.OptimError):
+        skc.TrainConfig(steps=0)
+
+
+def test_loss_metric_known_answers():
+    k = skc.gaussian_kernel(5)
+    assert skc.loss(k, k, skc.LossKind("charbonnier", 1e-6)) == pytest.approx(961e-6, rel=1e-12)
+    a = np.zeros((5, 5))
+    b = a.copy()
+    b[2, 3] = 0.3
+    assert skc.loss(skc.DenseKernel(a), skc.DenseKernel(b), skc.LossKind("l2")) == pytest.approx(0.09)
+    assert skc.psnr(a, a) == 99.0
+
+
+def test_theta_roundtrip(tmp_path):
+    cpx = synth.disk_complex(3, 5, seed=9)
+    p = tmp_path / "t.json"
+    skc.save_theta(cpx, p)
+    back = skc.load_theta(p)
+    for la, lb in zip(cpx.layers, back.layers):
+        assert np.array_equal(la.offsets, lb.offsets) and np.array_equal(la.weights, lb.weights)
+
+
+def test_kawase_exact_reach():
+    """the strip halo is the exact corner reach sum(floor|o|+1) = 21."""
+    from paper_2512_04556_b200.dist import corner_reach
+    kaw = synth.kawase_complex()
+    assert corner_reach(kaw) == (21, 21, 21, 21)
+    assert math.ceil(kaw.reach) == 18
