@@ -22,14 +22,14 @@
 //     global-gather kernel (L1/L2 cached) with identical arithmetic.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
-#include "skc_common.cuh"
+#include "skc_tile.cuh"
 
 namespace skc {
 
 constexpr int kMaxTaps = 256;        // taps per launch; longer layers are chunked
-constexpr int kMaxSmem = 227 * 1024;
 
 struct TapTable {
     float4 cw[kMaxTaps];  // corner weights (00, 10, 01, 11) = w(1-fx)(1-fy), w fx(1-fy), ...
@@ -38,98 +38,6 @@ struct TapTable {
     int iy[kMaxTaps];
     int n;
 };
-
-struct Geom {
-    int H, W;
-    int dx0, dy0;      // global offset of smem (0,0) relative to the tile origin
-    int pitch, rows;   // smem tile geometry (pitch odd)
-    int boundary;
-    int accumulate;    // out += result (fp32 outputs only; tap chunking)
-    long long in_fs, out_fs;  // frame strides (elements)
-};
-
-// ------------------------------------------------------------ tile loader ---
-// Stage rows [gy0, gy0+rows) x cols [gx0, gx0+pitch) of an HWC image into C
-// planar smem planes; out-of-image texels are 0 (ZERO) or the clamped texel.
-// fp32: every element is one 4-byte cp.async (LDGSTS) with zero-fill for
-// out-of-image texels, so the whole halo tile is in flight at once instead of
-// one dependent LDG->STS round trip per element.  fp16: batches of 8
-// independent loads per thread before the stores.
-__device__ __forceinline__ void cp_async4(float *dst, const float *src, bool valid) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
-                 "r"(valid ? 4 : 0));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-
-template <int C, typename TI>
-__device__ __forceinline__ void load_tile(float *s, const TI *__restrict__ in, int H, int W,
-                                          int boundary, int gx0, int gy0, int pitch, int rows) {
-    const int plane = rows * pitch;
-    const int rowlen = pitch * C;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const bool clamp = boundary == SKC_CLAMP;
-    if constexpr (sizeof(TI) == 4) {
-        for (int r = warp; r < rows; r += nw) {
-            int gy = gy0 + r;
-            bool rowin = gy >= 0 && gy < H;
-            if (clamp) { gy = min(max(gy, 0), H - 1); rowin = true; }
-            gy = min(max(gy, 0), H - 1);  // keep the (unused) source address in bounds
-            const float *src = reinterpret_cast<const float *>(in) + (long long)gy * W * C;
-            float *dst = s + r * pitch;
-#pragma unroll 4
-            for (int e = lane; e < rowlen; e += 32) {
-                const int col = e / C;
-                const int c = e - col * C;
-                const int gx = gx0 + col;
-                const bool ok = clamp || (rowin && gx >= 0 && gx < W);
-                const int gxc = min(max(gx, 0), W - 1);
-                cp_async4(dst + c * plane + col, src + (long long)gxc * C + c, ok);
-            }
-        }
-        cp_async_wait_all();
-    } else {
-        constexpr int U = 8;
-        for (int r = warp; r < rows; r += nw) {
-            int gy = gy0 + r;
-            bool rowin = gy >= 0 && gy < H;
-            if (clamp) { gy = min(max(gy, 0), H - 1); rowin = true; }
-            gy = min(max(gy, 0), H - 1);
-            const TI *src = in + (long long)gy * W * C;
-            float *dst = s + r * pitch;
-            for (int e0 = lane; e0 < rowlen; e0 += 32 * U) {
-                float v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + 32 * u;
-                    const int col = e / C;
-                    const int c = e - col * C;
-                    const int gx = gx0 + col;
-                    const bool ok = e < rowlen && (clamp || (rowin && gx >= 0 && gx < W));
-                    const int gxc = min(max(gx, 0), W - 1);
-                    v[u] = ok ? IO<TI>::ld(src + (long long)gxc * C + c) : 0.f;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + 32 * u;
-                    if (e < rowlen) {
-                        const int col = e / C;
-                        dst[(e - col * C) * plane + col] = v[u];
-                    }
-                }
-            }
-        }
-    }
-}
-
-template <typename TO>
-__device__ __forceinline__ void store_px(TO *p, float v, int accumulate) {
-    IO<TO>::st(p, v);
-}
-template <>
-__device__ __forceinline__ void store_px<float>(float *p, float v, int accumulate) {
-    *p = accumulate ? (*p + v) : v;
-}
 
 // ----------------------------------------------------- uniform layer kernel ---
 template <int C, int KR, int MC, int WX, int WY, typename TI, typename TO>
@@ -389,9 +297,44 @@ static int convert(const void *in, int idt, void *out, int odt, long long n, cud
 // One full layer from `in` to `out` with tap chunking.  Chunks after the first
 // accumulate into an fp32 destination; an fp16 destination with more than
 // kMaxTaps taps goes through an fp32 temporary.
+// Dense-stencil eligibility: merged corner footprint D x D (D <= 9) with
+// D*D < 4*S FMAs per pixel.  SKC_DENSE=0 in the environment disables it.
+static bool dense_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SKC_DENSE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+static bool try_dense(const double *taps, int S, const LayerPlan &lp, DenseTable &dt) {
+    if (!dense_enabled()) return false;
+    const int sx = lp.dx_max - lp.dx_min + 1, sy = lp.dy_max - lp.dy_min + 1;
+    const int D = dense_size_for(std::max(sx, sy));
+    if (D == 0 || D * D >= 4 * S) return false;
+    double k[kMaxDense * kMaxDense] = {0.0};
+    for (int i = 0; i < S; ++i) {
+        const double ox = taps[3 * i], oy = taps[3 * i + 1], w = taps[3 * i + 2];
+        const double fx0 = std::floor(ox), fy0 = std::floor(oy);
+        const double fx = ox - fx0, fy = oy - fy0;
+        const double cw[4] = {w * (1.0 - fx) * (1.0 - fy), w * fx * (1.0 - fy), w * (1.0 - fx) * fy,
+                              w * fx * fy};
+        for (int c = 0; c < 4; ++c) {
+            const int a = (int)fy0 + (c >> 1) - lp.dy_min, b = (int)fx0 + (c & 1) - lp.dx_min;
+            k[a * D + b] += cw[c];
+        }
+    }
+    dt.D = D;
+    for (int e = 0; e < kMaxDense * kMaxDense; ++e) dt.k[e] = e < D * D ? (float)k[e] : 0.f;
+    return true;
+}
+
 static int run_layer(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
                      const double *taps, int S, int boundary, cudaStream_t s) {
     LayerPlan lp = make_plan(taps, S);
+    DenseTable dt;
+    if (try_dense(taps, S, lp, dt))
+        return launch_dense(in, idt, out, odt, B, H, W, C, dt, lp.dx_min, lp.dy_min, boundary, s);
     if (S <= kMaxTaps) return launch_layer(in, idt, out, odt, B, H, W, C, lp, 0, S, boundary, 0, s);
     void *dst = out;
     void *tmp = nullptr;

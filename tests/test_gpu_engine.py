@@ -197,3 +197,37 @@ def test_torch_in_torch_out_zero_copy(skc):
     assert isinstance(y, torch.Tensor) and y.is_cuda and y.shape == x.shape
     h = skc.apply_complex(x.half(), cpx)
     assert h.dtype == torch.float16
+
+
+def test_dense_and_tap_paths_agree(skc, orc):
+    """Layers whose merged corner footprint is small run as dense stencils
+    (D = 3/5/7/9); SKC_DENSE=0 forces the tap path: both match the oracle."""
+    import os
+    import subprocess
+    import sys
+    rng = np.random.default_rng(21)
+    img = rng.random((150, 170, 3)).astype(np.float32)
+    cases = []
+    for reach, n in ((0.9, 12), (1.9, 16), (2.9, 20), (3.9, 32)):   # D = 3, 5, 7, 9
+        off = rng.uniform(-reach, reach, (n, 2))
+        w = rng.random(n)
+        cases.append((off, w / w.sum()))
+    for off, w in cases:
+        ref = orc.apply_layer(img.astype(np.float64), off, w)
+        for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+            ref = orc.apply_layer(img.astype(np.float64), off, w, oid)
+            assert normwise(skc.apply_sparse_layer(img, skc.SparseLayer(off, w), mode), ref) < TOL32
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc;"
+            "d = np.load(sys.argv[1]); out = skc.apply_sparse_layer(d['img'], skc.SparseLayer(d['off'], d['w']));"
+            "np.save(sys.argv[2], out)")
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        for k, (off, w) in enumerate(cases):
+            np.savez(f"{td}/in{k}.npz", img=img, off=off, w=w)
+            env = dict(os.environ, SKC_DENSE="0")
+            subprocess.run([sys.executable, "-c", code, f"{td}/in{k}.npz", f"{td}/out{k}.npy"],
+                           check=True, env=env, cwd=str(__import__("pathlib").Path(__file__).parent.parent))
+            taps_out = np.load(f"{td}/out{k}.npy")
+            dense_out = skc.apply_sparse_layer(img, skc.SparseLayer(off, w))
+            assert normwise(dense_out, taps_out) < 2e-6
