@@ -1,17 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: BASELINE config 1 -- 4 layers x 32 taps on 2665x1264x3 fp32 frames.
+"""Benchmark of the Sparse Kernel Complex hot path on B200.
 
-One step = the hot path (the 4-layer chain) over one batch of 64 frames per
-GPU, resident in HBM (value), and the same through the public API from pinned
-HOST buffers with the copies inside the timed region (e2e).  N>1: one process
-per GPU (torchrun), each with its own 64 frames (weak scaling, no collective
-on the data path), timed with CUDA events and reported as the max over ranks.
+Default (the driver's headline): BASELINE config 1 -- a 4 layers x 32 taps
+disk complex over 64 frames of 2665x1264x3 fp32 per GPU.  One step = the
+whole chain over the batch, inputs resident in HBM (`value`); `e2e` is the
+same through the public API from pinned HOST buffers with both copies inside
+the timed region.  N>1: one process per GPU (torchrun), each with its own
+frames (weak scaling, no collective on the data path), CUDA-event timing,
+max over ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c0|c2|c3|c3big|c4]
 
-`--impl reference` times the reference's CPU algorithm (the float64 oracle
-port, oracle/skc_oracle.c -- the reference itself is Python and cannot travel
-to the GPU box) with all host threads on bounded samples of the same workload.
+The other configs are the remaining BASELINE workloads: c0 the
+512^2 clamp-to-edge case, c2 the spatially varying filter, c3 Kawase 6x4 fp16
+RGBA batch 32 (c3big: one 16384^2 image), c4 batched fitting (256 targets x
+3000 Adam steps, fit kernel-iterations/s).
+
+`--impl reference` times the reference's CPU algorithm -- the float64 C port
+(oracle/skc_oracle.c; the reference itself is Python and cannot travel to the
+GPU box) -- with all host threads on bounded samples of the same workload.
 """
 
 from __future__ import annotations
@@ -31,11 +39,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "filtered Mpix/s (1264x2665 RGB, 4 layers x 32 taps)"
-UNIT = "Mpix/s"
-H, W, C = 2665, 1264, 3
-LAYOUT = (32, 32, 32, 32)
-FRAMES_PER_GPU = 64
+DATA = "synthetic (seeded recipes of SURVEY 8d: value noise + rects, disk complexes, procedural targets)"
 
 
 def parse():
@@ -44,50 +48,46 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames", type=int, default=FRAMES_PER_GPU)
+    ap.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c3", "c3big", "c4"])
+    ap.add_argument("--frames", type=int, default=None, help="frames per GPU (c1/c3)")
+    ap.add_argument("--fit-steps", type=int, default=3000)
+    ap.add_argument("--fit-targets", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    p = ROOT / "profiles" / "ncu_layer_kernel.json"
+def ncu_traffic(config):
+    p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch_at_bench_batch")
+            return json.loads(p.read_text()).get(config)
         except Exception:
             return None
     return None
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
 
     QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
 
     def start(self):
         try:
@@ -95,8 +95,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -132,30 +131,261 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gpu_frames(n, seed0, device):
-    """Config-1 frames generated on the device from the seeded recipe."""
-    import torch
-    from paper_2512_04556_b200 import synth
-    out = torch.empty((n, H, W, C), dtype=torch.float32, device=device)
-    for i in range(n):
-        out[i].copy_(torch.from_numpy(synth.value_noise_frame(H, W, C, seed=seed0 + i)), non_blocking=False)
-    return out
+# ------------------------------------------------------------- workloads ---
 
+class Chain:
+    """Uniform chain workloads (c0, c1, c3, c3big): per-layer launches timed."""
 
-def cpu_oracle_rate(sample_rows: int, threads: int | None = None):
-    """Oracle (float64 C port of the reference apply_complex) on a bounded strip."""
-    from oracle import oracle as orc
-    from paper_2512_04556_b200 import synth
-    if threads:
+    def __init__(self, name, args, dev, rank):
+        import torch
+        from paper_2512_04556_b200 import synth
+        self.name = name
+        if name in ("c1", "c0"):
+            self.h, self.w, self.c = (2665, 1264, 3) if name == "c1" else (512, 512, 3)
+            self.cpx = synth.c1_complex() if name == "c1" else synth.c0_complex()
+            self.boundary = "zero" if name == "c1" else "clamp"
+            self.nf = args.frames or (64 if name == "c1" else 1)
+            self.storage = torch.float32
+        else:
+            self.h, self.w, self.c = synth.C3_SHAPE if name == "c3" else synth.C3_BIG
+            self.cpx = synth.kawase_complex()
+            self.boundary = "zero"
+            self.nf = args.frames or (32 if name == "c3" else 1)
+            self.storage = torch.float16
+        frames = torch.empty((self.nf, self.h, self.w, self.c), dtype=self.storage, device=dev)
+        for i in range(self.nf):
+            if name == "c0":
+                frames[i].copy_(torch.from_numpy(synth.c0_image()))
+            else:
+                frames[i].copy_(synth.value_noise_frame_device(self.h, self.w, self.c, rank * self.nf + i,
+                                                               dev, dtype=self.storage))
+        self.frames = frames
+        npx = self.nf * self.h * self.w * self.c
+        self.bufs = [torch.empty(npx, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.out = torch.empty_like(frames)
+        self.taps = [np.ascontiguousarray(l.taps()) for l in self.cpx.layers]
+        self.launches_per_step = len(self.taps)
+        self.units_per_step = self.nf * self.h * self.w
+        esz = 2 if self.storage == torch.float16 else 4
+        # algorithmic HBM bytes per launch: image in + out in their storage dtypes
+        self.alg_bytes = []
+        for l in range(len(self.taps)):
+            bi = esz if l == 0 else 4
+            bo = esz if l == len(self.taps) - 1 else 4
+            self.alg_bytes.append(self.nf * self.h * self.w * self.c * (bi + bo))
+        self.metric = {
+            "c1": "filtered Mpix/s (1264x2665 RGB, 4 layers x 32 taps)",
+            "c0": "filtered Mpix/s (512x512 RGB, 4 layers x 12 taps, clamp-to-edge)",
+            "c3": "filtered Mpix/s (3840x2160 RGBA fp16, Kawase 6 layers x 4 taps)",
+            "c3big": "filtered Mpix/s (16384x16384 RGBA fp16, Kawase 6 layers x 4 taps, 1 GPU)",
+        }[name]
+        self.dtype = "f32" if self.storage == torch.float32 else "f16 storage, f32 accumulate"
+        self.config = {"workload": f"{name}: {self.nf} frame(s)/GPU of {self.h}x{self.w}x{self.c} "
+                                   f"{'fp32' if esz == 4 else 'fp16'}, layout {self.cpx.layout}, {self.boundary} boundary",
+                       "frames_per_gpu": self.nf,
+                       "l2": "inputs larger than L2, no flush" if npx * esz > 126e6 else "L2 flushed between steps"}
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if npx * esz <= 126e6 else None
+        self.kernel = "layer kernels (dense + tap tile)"
+
+    def step(self, stream, events=None):
+        from paper_2512_04556_b200 import _native as nat
+        lib = nat.lib()
+        sp = nat.stream_ptr(stream)
+        dt_store = nat.SKC_F16 if self.out.dtype != self.bufs[0].dtype else nat.SKC_F32
+        src, sdt = self.frames, dt_store
+        L = len(self.taps)
+        for l, t in enumerate(self.taps):
+            last = l == L - 1
+            dst, ddt = (self.out, dt_store) if last else (self.bufs[l & 1], nat.SKC_F32)
+            if events is not None:
+                events[l][0].record(stream)
+            rc = lib.skc_layer_fwd(nat.ptr(src), sdt, nat.ptr(dst), ddt, self.nf, self.h, self.w, self.c,
+                                   nat.dbl(t), t.shape[0], 0 if self.boundary == "zero" else 1, sp)
+            if rc:
+                raise RuntimeError(nat.last_error())
+            if events is not None:
+                events[l][1].record(stream)
+            src, sdt = dst, ddt
+
+    def pre_step(self):
+        if self.flush is not None:
+            self.flush.zero_()
+
+    def e2e_setup(self):
+        self.host_in = self.frames.cpu().pin_memory()
+        self.host_out = torch_mod().empty_like(self.host_in).pin_memory()
+        n = self.host_in.numel() * self.host_in.element_size()
+        return n, n
+
+    def e2e_step(self):
+        import paper_2512_04556_b200 as skc
+        skc.apply_complex_batch(self.host_in, self.cpx, boundary=self.boundary, out=self.host_out)
+
+    def cpu_sample(self, threads):
+        from oracle import oracle as orc
+        from paper_2512_04556_b200 import synth
         orc.set_threads(threads)
-    cpx = synth.c1_complex()
-    layers = [(l.offsets, l.weights) for l in cpx.layers]
-    frame = synth.c1_frame(0)[:sample_rows].astype(np.float64)
-    t0 = time.perf_counter()
-    orc.apply_complex(frame, layers)
-    dt = time.perf_counter() - t0
-    return sample_rows * W / dt / 1e6, orc.num_threads(), dt
+        rows = {"c1": 768, "c0": 512, "c3": 256, "c3big": 128}[self.name]
+        if self.name == "c0":
+            img = synth.c0_image().astype(np.float64)
+        elif self.name == "c1":
+            img = synth.c1_frame(0)[:rows].astype(np.float64)
+        else:
+            img = synth.value_noise_frame(rows, self.w, self.c, seed=0, rects=20, dtype=np.float16).astype(np.float64)
+        layers = [(l.offsets, l.weights) for l in self.cpx.layers]
+        t0 = time.perf_counter()
+        orc.apply_complex(img, layers, orc.CLAMP if self.boundary == "clamp" else orc.ZERO)
+        dt = time.perf_counter() - t0
+        return (img.shape[0] * img.shape[1] / dt / 1e6, orc.num_threads(),
+                f"{img.shape[0]} rows x {img.shape[1]} px x {self.c} ch (float64 oracle port of "
+                f"engine.apply_complex), {dt:.2f}s")
 
+
+class SV:
+    """c2: spatially varying filter, one 2665x1264x3 frame, 3 bases x 4x24."""
+
+    def __init__(self, args, dev, rank):
+        import torch
+        from paper_2512_04556_b200 import synth
+        from paper_2512_04556_b200.svfilter import stacked_params
+        self.h, self.w, self.c = synth.C1_SHAPE
+        self.basis = synth.c2_basis()
+        self.frame = synth.value_noise_frame_device(self.h, self.w, self.c, rank, dev)
+        self.pmap = torch.from_numpy(synth.c2_pmap()).to(dev)
+        self.stack = np.ascontiguousarray(stacked_params(self.basis))
+        self.ps = np.ascontiguousarray(self.basis.params)
+        self.bufs = [torch.empty_like(self.frame) for _ in range(2)]
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        L = len(self.basis.layout)
+        self.launches_per_step = L
+        self.units_per_step = self.h * self.w
+        self.alg_bytes = [self.h * self.w * (self.c * 8 + 4)] * L
+        self.metric = "SV-filtered Mpix/s (1264x2665 RGB, 3 bases x 4 layers x 24 taps)"
+        self.dtype = "f32"
+        self.config = {"workload": "c2: 1 frame 2665x1264x3 fp32, pmap radial + 20 blobs, bases 4x24 at p=0/0.5/1 (radius x0.5/1/2)",
+                       "l2": "L2 flushed (256 MB write) before each step"}
+        self.kernel = "sv_tile_kernel"
+
+    def step(self, stream, events=None):
+        from paper_2512_04556_b200 import _native as nat
+        lib = nat.lib()
+        sp = nat.stream_ptr(stream)
+        src = self.frame
+        layout = self.basis.layout
+        for l, n in enumerate(layout):
+            dst = self.bufs[l & 1]
+            sub = np.ascontiguousarray(self.stack[:, l:l + 1, :n])
+            lay = np.array([n], dtype=np.int32)
+            if events is not None:
+                events[l][0].record(stream)
+            rc = lib.skc_sv_fwd(nat.ptr(src), 0, nat.ptr(dst), 0, self.h, self.w, self.c, nat.ptr(self.pmap),
+                                nat.dbl(self.ps), self.ps.size, nat.dbl(sub), n, nat.ints(lay), 1, 0, sp)
+            if rc:
+                raise RuntimeError(nat.last_error())
+            if events is not None:
+                events[l][1].record(stream)
+            src = dst
+
+    def pre_step(self):
+        self.flush.zero_()
+
+    def e2e_setup(self):
+        self.host_in = self.frame.cpu().numpy()
+        self.host_pmap = self.pmap.cpu().numpy()
+        n = self.host_in.nbytes + self.host_pmap.nbytes
+        return n, self.host_in.nbytes
+
+    def e2e_step(self):
+        import paper_2512_04556_b200 as skc
+        skc.sv_filter(self.host_in, self.basis, self.host_pmap)
+
+    def cpu_sample(self, threads):
+        from oracle import oracle as orc
+        from paper_2512_04556_b200 import synth
+        orc.set_threads(threads)
+        rows = 384
+        img = synth.c1_frame(0)[:rows].astype(np.float64)
+        pm = synth.c2_pmap()[:rows]
+        t0 = time.perf_counter()
+        orc.sv_filter(img, pm, self.ps, self.stack, self.basis.layout)
+        dt = time.perf_counter() - t0
+        return (rows * self.w / dt / 1e6, orc.num_threads(),
+                f"{rows} rows x {self.w} px x 3 ch (float64 oracle port of sv_filter/_sv_pass_loop), {dt:.2f}s")
+
+
+class Fit:
+    """c4: 256 targets of 129^2, 4x32 complex, L1, SUM, default schedule."""
+
+    def __init__(self, args, dev, rank, world):
+        import paper_2512_04556_b200 as skc
+        from paper_2512_04556_b200 import synth
+        from paper_2512_04556_b200.dist import shard
+        n = args.fit_targets
+        idx = list(range(n))[shard(n, rank, world)] if world > 1 else list(range(n))
+        self.targets = [synth.c4_target(i) for i in idx]
+        self.inits = [synth.c4_init(i) for i in idx]
+        self.cfg = skc.TrainConfig(steps=args.fit_steps)
+        self.con = skc.ConstraintConfig("sum")
+        self.kind = skc.LossKind("l1")
+        self.launches_per_step = 1
+        self.units_per_step = len(idx) * args.fit_steps
+        self.alg_bytes = [len(idx) * (129 * 129 * 4 + 6 * 128 * 3 * 4)]
+        self.metric = "fit kernel-iterations/s (256 targets 129^2, 4x32, L1, Adam 1e-3->1e-4)"
+        self.unit = "kernel-it/s"
+        self.dtype = "f32 (f64 reductions)"
+        self.config = {"workload": f"c4: {n} targets (disk/square/hexagon/ring/star4, R~U[20,60]), "
+                                   f"{args.fit_steps} steps each, explicit disk-complex inits",
+                       "targets_per_gpu": len(idx), "note": "lr 1e-3->1e-4 reference default (BASELINE lr 1e-2 diverges in the reference, SURVEY D4)"}
+        self.kernel = "fit_kernel"
+        self.result = None
+
+    def step(self, stream, events=None):
+        import paper_2512_04556_b200 as skc
+        if events is not None:
+            events[0][0].record(stream)
+        self.result = skc.fit_batch(self.targets, (32,) * 4, self.inits, self.cfg, self.con, self.kind,
+                                    return_device=True)
+        if events is not None:
+            events[0][1].record(stream)
+
+    def pre_step(self):
+        pass
+
+    def e2e_setup(self):
+        return len(self.targets) * 129 * 129 * 4, len(self.targets) * (self.cfg.steps + 1 + 4 * 32 * 3) * 4
+
+    def e2e_step(self):
+        import paper_2512_04556_b200 as skc
+        skc.fit_batch(self.targets, (32,) * 4, self.inits, self.cfg, self.con, self.kind)
+
+    def cpu_sample(self, threads):
+        from oracle import oracle as orc
+        orc.set_threads(threads)
+        nk, steps = min(len(self.targets), 2 * threads), 20
+        tg = np.stack([t.weights for t in self.targets[:nk]])
+        off = np.stack([np.concatenate([l.offsets for l in c.layers]) for c in self.inits[:nk]])
+        w = np.stack([np.concatenate([l.weights for l in c.layers]) for c in self.inits[:nk]])
+        t0 = time.perf_counter()
+        orc.fit_batch(tg, off, w, [32] * 4, steps=steps, weight_norm="sum", loss_kind="l1")
+        dt = time.perf_counter() - t0
+        return (nk * steps / dt, orc.num_threads(),
+                f"{nk} targets x {steps} fit steps (float64 oracle port of optim.fit), {dt:.2f}s")
+
+
+def torch_mod():
+    import torch
+    return torch
+
+
+def make_workload(args, dev, rank, world):
+    if args.config in ("c0", "c1", "c3", "c3big"):
+        return Chain(args.config, args, dev, rank)
+    if args.config == "c2":
+        return SV(args, dev, rank)
+    return Fit(args, dev, rank, world)
+
+
+# ------------------------------------------------------------------ arms ---
 
 def run_reference(args):
     rank, world, local = dist_env()
@@ -163,158 +393,177 @@ def run_reference(args):
         return
     from oracle import oracle as orc
     orc.build()
-    nthreads = os.cpu_count() or 1
-    orc.set_threads(nthreads)
-    rows = 512
-    for _ in range(max(0, args.warmup)):
-        cpu_oracle_rate(64, nthreads)
-    times = []
+    threads = os.cpu_count() or 1
+
+    class _Args:
+        frames = 1
+        fit_steps = args.fit_steps
+        fit_targets = min(args.fit_targets, 2 * threads)
+
+    wl = _cpu_only_workload(args.config, _Args)
+    for _ in range(args.warmup):
+        wl.cpu_sample(threads)
+    vals, secs, sample = [], 0.0, ""
     for _ in range(args.steps):
-        rate, cores, dt = cpu_oracle_rate(rows, nthreads)
-        times.append(dt)
-    tot = sum(times)
-    value = args.steps * rows * W / tot / 1e6
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded value noise + 200 rects, SURVEY 8d)",
-        "config": {"workload": "C1: 4x32 disk complex on 2665x1264x3; each step a 512-row strip of frame 0",
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
-                         "sample": f"{rows} rows x {W} px x 3 ch per step, float64 oracle port of engine.apply_complex"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+        t0 = time.perf_counter()
+        v, cores, sample = wl.cpu_sample(threads)
+        secs += time.perf_counter() - t0
+        vals.append(v)
+    value = statistics.median(vals)
+    unit = getattr(wl, "unit", "Mpix/s")
+    print(json.dumps({
+        "impl": "reference", "metric": wl.metric, "value": value, "unit": unit, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": dict(wl.config, parallelism="host threads"),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _cpu_only_workload(config, a):
+    """Workload metadata + cpu_sample without touching a GPU."""
+    from paper_2512_04556_b200 import synth
+    from paper_2512_04556_b200.svfilter import stacked_params
+    if config in ("c0", "c1", "c3", "c3big"):
+        wl = Chain.__new__(Chain)
+        wl.name = config
+        if config in ("c1", "c0"):
+            wl.h, wl.w, wl.c = (2665, 1264, 3) if config == "c1" else (512, 512, 3)
+            wl.cpx = synth.c1_complex() if config == "c1" else synth.c0_complex()
+            wl.boundary = "zero" if config == "c1" else "clamp"
+        else:
+            wl.h, wl.w, wl.c = synth.C3_SHAPE if config == "c3" else synth.C3_BIG
+            wl.cpx = synth.kawase_complex()
+            wl.boundary = "zero"
+        wl.metric = {"c1": "filtered Mpix/s (1264x2665 RGB, 4 layers x 32 taps)",
+                     "c0": "filtered Mpix/s (512x512 RGB, 4 layers x 12 taps, clamp-to-edge)",
+                     "c3": "filtered Mpix/s (3840x2160 RGBA fp16, Kawase 6 layers x 4 taps)",
+                     "c3big": "filtered Mpix/s (16384x16384 RGBA fp16, Kawase 6 layers x 4 taps, 1 GPU)"}[config]
+        wl.config = {"workload": f"{config}: bounded strips of the same frames on the host"}
+        return wl
+    if config == "c2":
+        wl = SV.__new__(SV)
+        wl.h, wl.w, wl.c = synth.C1_SHAPE
+        wl.basis = synth.c2_basis()
+        wl.stack = np.ascontiguousarray(stacked_params(wl.basis))
+        wl.ps = np.ascontiguousarray(wl.basis.params)
+        wl.metric = "SV-filtered Mpix/s (1264x2665 RGB, 3 bases x 4 layers x 24 taps)"
+        wl.config = {"workload": "c2: bounded strips of the frame on the host"}
+        return wl
+    wl = Fit.__new__(Fit)
+    n = a.fit_targets
+    wl.targets = [synth.c4_target(i) for i in range(n)]
+    wl.inits = [synth.c4_init(i) for i in range(n)]
+    wl.metric = "fit kernel-iterations/s (256 targets 129^2, 4x32, L1, Adam 1e-3->1e-4)"
+    wl.unit = "kernel-it/s"
+    wl.config = {"workload": f"c4: {n} targets x 20 steps per sample on the host"}
+    return wl
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2512_04556_b200 as skc
-    from paper_2512_04556_b200 import _native as nat
-    from paper_2512_04556_b200 import synth
-
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    lib = nat.lib()
-    cpx = synth.c1_complex()
-    nf = args.frames
-    frames = gpu_frames(nf, rank * nf, dev)
-    bufs = [torch.empty_like(frames) for _ in range(2)]
+    from paper_2512_04556_b200 import _native as nat
+    nat.lib()
+    wl = make_workload(args, dev, rank, world)
     stream = torch.cuda.current_stream()
-    sp = nat.stream_ptr(stream)
-    taps = [np.ascontiguousarray(l.taps()) for l in cpx.layers]
-
-    def step(events=None):
-        src = frames
-        for l, t in enumerate(taps):
-            dst = bufs[l & 1]
-            if events is not None:
-                events[l][0].record(stream)
-            rc = lib.skc_layer_fwd(nat.ptr(src), nat.SKC_F32, nat.ptr(dst), nat.SKC_F32, nf, H, W, C,
-                                   nat.dbl(t), t.shape[0], nat.SKC_ZERO, sp)
-            if rc:
-                raise RuntimeError(nat.last_error())
-            if events is not None:
-                events[l][1].record(stream)
-            src = dst
-        return src
-
     for _ in range(args.warmup):
-        step()
+        wl.pre_step()
+        wl.step(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
         clocks.start()
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in taps] for _ in range(args.steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    nl = wl.launches_per_step
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
+          for _ in range(args.steps)]
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     torch.cuda.synchronize()
-    t0.record(stream)
     for k in range(args.steps):
-        step(ev[k])
-    t1.record(stream)
+        wl.pre_step()                  # L2 flush (if inputs fit L2) outside the timed step
+        sev[k][0].record(stream)
+        wl.step(stream, ev[k])
+        sev[k][1].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
-    ms = t0.elapsed_time(t1)
-    launch_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(len(taps))]
+    ms = sum(a.elapsed_time(b) for a, b in sev)
+    launch_ms = [[ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps)] for l in range(nl)]
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    px_total = world * nf * H * W * args.steps
-    value = px_total / (ms_max / 1e3) / 1e6
+    scale = 1e6 if getattr(wl, "unit", "Mpix/s") == "Mpix/s" else 1.0
+    value = world * wl.units_per_step * args.steps / (ms_max / 1e3) / scale
 
-    # end-to-end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host_in = frames.cpu().pin_memory()
-        host_out = torch.empty_like(host_in).pin_memory()
-        for _ in range(1):
-            skc.apply_complex_batch(host_in, cpx, out=host_out)
+        bi, bo = wl.e2e_setup()
+        wl.e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ke = max(1, min(args.steps, 3))
         e0.record(stream)
         for _ in range(ke):
-            skc.apply_complex_batch(host_in, cpx, out=host_out)
+            wl.e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
         ems = torch.tensor([e0.elapsed_time(e1) / ke], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        nbytes = host_in.numel() * host_in.element_size()
-        e2e = {"value": world * nf * H * W / (float(ems.item()) / 1e3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": int(nbytes),
-               "ms_per_step": float(ems.item()), "steps": ke}
+        e2e = {"value": world * wl.units_per_step / (float(ems.item()) / 1e3) / scale,
+               "unit": getattr(wl, "unit", "Mpix/s"), "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo), "ms_per_step": float(ems.item()), "steps": ke}
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
-        avg_launch_ms = sum(launch_ms) / len(launch_ms)
-        alg_bytes = nf * H * W * C * 4 * 2            # compulsory image in + out per launch
-        achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
-        nominal_smem = 148 * 128 * 1.965e9 / 1e9     # GB/s, nominal
-        smem_bytes = nf * H * W * 4 * 32 * C * 4      # taps x 4 fetches x 12 B per px per launch
-        fma = nf * H * W * C * 32 * 4                 # FMAs per launch (4 per tap per channel)
-        per_layer = [sum(launch_ms[l::len(taps)]) / args.steps for l in range(len(taps))]
+        per_launch = [sum(v) / len(v) for v in launch_ms]
+        dom = int(np.argmax(per_launch))
+        achieved = wl.alg_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
+        total_launch_ms = sum(per_launch)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded value noise + 200 rects per frame, SURVEY 8d); inputs > L2 (2.6 GB/GPU)",
-            "config": {"workload": "C1 batch: 64 frames/GPU of 2665x1264x3 fp32 through a 4x32 disk complex (zero pad)",
-                       "frames_per_gpu": nf, "layout": "4x32", "l2": "inputs larger than L2, no flush needed",
-                       "parallelism": f"dp{world} (frames sharded, no collective)"},
+            "metric": wl.metric, "value": value, "unit": getattr(wl, "unit", "Mpix/s"), "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
+            "data": DATA,
+            "config": dict(wl.config, parallelism=f"dp{world} (independent units sharded, no collective)"),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-                         "kernel": "layer_tile_kernel", "avg_launch_ms": avg_launch_ms,
-                         "per_layer_ms": per_layer,
-                         "alg_bytes_per_launch": alg_bytes,
-                         "smem_bound": {"alg_bytes_per_launch": smem_bytes,
-                                        "achieved_GBps": smem_bytes / (avg_launch_ms / 1e3) / 1e9,
-                                        "nominal_peak_GBps": nominal_smem,
-                                        "frac_of_nominal": smem_bytes / (avg_launch_ms / 1e3) / 1e9 / nominal_smem},
-                         "fp32_fma": {"tflops": 2 * fma / (avg_launch_ms / 1e3) / 1e12,
-                                      "nominal_peak_tflops": 2 * 148 * 128 * 1.965e9 / 1e12}},
-            "gpu_launches": args.steps * len(taps),
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
+                         "kernel": wl.kernel, "launch_index": dom, "launch_ms": per_launch[dom],
+                         "alg_bytes_per_launch": wl.alg_bytes[dom],
+                         "per_launch_ms": per_launch,
+                         "share_of_step": per_launch[dom] / (ms_max / args.steps),
+                         "step_hbm_frac": sum(wl.alg_bytes) / (total_launch_ms / 1e3) / 1e9 / peak},
+            "gpu_launches": args.steps * nl,
             "clocks": clk,
         }
+        if isinstance(wl, Chain):
+            fma = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * wl.units_per_step
+            line["roofline"]["fp32_fma"] = {
+                "alg_tflops_4_per_tap": 2 * fma / (total_launch_ms / 1e3) / 1e12,
+                "nominal_peak_tflops": 2 * 148 * 128 * 1.965e9 / 1e12}
+            smem = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * 4 * wl.units_per_step
+            line["roofline"]["smem_bound_baseline_def"] = {
+                "achieved_GBps": smem / (total_launch_ms / 1e3) / 1e9, "nominal_peak_GBps": 148 * 128 * 1.965,
+                "note": "taps x 4 fetches x C x 4 B per px (BASELINE definition); register blocking and "
+                        "dense-stencil merging move fewer bytes, so this can exceed 1"}
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu and world == 1:
-            rate, cores, dt = cpu_oracle_rate(384, os.cpu_count())
-            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                    "sample": f"384 rows x {W} px x 3 ch of frame 0 (float64 oracle port), {dt:.1f}s"}
+            v, cores, sample = wl.cpu_sample(os.cpu_count())
+            line["cpu_baseline"] = {"value": v, "unit": getattr(wl, "unit", "Mpix/s"), "cores": cores,
+                                    "kind": "port", "sample": sample}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -87,6 +87,39 @@ def value_noise_frame(h: int, w: int, c: int, seed: int, rects: int = 200,
     return acc.astype(dtype)
 
 
+def value_noise_frame_device(h: int, w: int, c: int, seed: int, device, rects: int = 200,
+                             dtype=None):
+    """value_noise_frame with the upsampling done on the device (same draws,
+    float64 arithmetic; used to build large benchmark batches quickly)."""
+    import torch
+    rng = np.random.default_rng(seed)
+    acc = torch.zeros((h, w, c), dtype=torch.float64, device=device)
+    amps = (1.0, 0.5, 0.25, 0.125)
+
+    def up(lat, n, cell, axis):
+        pos = torch.arange(n, dtype=torch.float64, device=device) / cell
+        i = torch.floor(pos).long()
+        t = pos - i
+        s = t * t * (3.0 - 2.0 * t)
+        a = lat.index_select(axis, i)
+        b = lat.index_select(axis, i + 1)
+        shape = [1] * lat.dim()
+        shape[axis] = n
+        return a + (b - a) * s.view(shape)
+
+    for cell, amp in zip((128, 64, 32, 16), amps):
+        lat = torch.from_numpy(rng.random((h // cell + 2, w // cell + 2, c))).to(device)
+        acc += amp * up(up(lat, h, cell, 0), w, cell, 1)
+    acc /= sum(amps)
+    for _ in range(rects):
+        rh = int(rng.integers(8, 129))
+        rw = int(rng.integers(8, 129))
+        y0 = int(rng.integers(0, max(1, h - rh + 1)))
+        x0 = int(rng.integers(0, max(1, w - rw + 1)))
+        acc[y0:y0 + rh, x0:x0 + rw, :] = 1.0
+    return acc.to(torch.float32 if dtype is None else dtype)
+
+
 def c0_image() -> np.ndarray:
     """Config 0: 512x512x3, iid U[0,1) from seed 0, fp32."""
     return np.random.default_rng(0).random((512, 512, 3)).astype(np.float32)
