@@ -1,0 +1,626 @@
+// skc_layer.cu -- uniform sparse-layer kernels (sm_100a), v3.
+//
+// Reference: engine.apply_sparse_layer (engine.py:160-170) -> sample_shifted
+// (118-130) -> _accum_shift (106-115); engine.apply_complex (173-178).
+//
+// Work decomposition: one CTA = one (output tile, channel) pair.  The chain's
+// intermediates are fp32 *planar* (B, C, H, W): only the first layer reads the
+// caller's HWC image and only the last writes HWC, so every inner layer loads
+// its halo tile as contiguous rows with 8-byte cp.async (LDGSTS, zero-fill at
+// the image edge) and stores 8-pixel row segments with 16-byte stores.
+//
+// Tap path (layer_tap_kernel): a uniform tap is 4 integer shifts with constant
+// weights; the host folds each tap into (shared-memory offset of corner 00,
+// 4 weights) and sorts taps by offset parity.  Each thread owns a KR x 8
+// output block (KR odd); per tap it reads a (KR+1) x 9 window -- 4 LDS.64 +
+// 1 LDS.32 per row, bank-conflict free for LDS.64 because the row pitch is
+// 2 mod 4 and KR is odd -- and issues 32*KR FFMAs with uniform-register
+// weights.  Dense path (layer_dense_kernel): when the merged corner footprint
+// fits D x D (D <= 9) with D^2 < 4S the host merges coincident corners into a
+// stencil whose weights are compile-time constant-bank operands.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
+
+#include "skc_tile.cuh"
+
+namespace skc {
+
+constexpr int kLMaxTaps = 256;
+
+struct TapList {
+    float4 cw[kLMaxTaps];  // corner weights (00, 10, 01, 11)
+    int off[kLMaxTaps];    // smem offset of corner 00 relative to the thread's block origin
+    int ix[kLMaxTaps];     // integer parts (direct kernel)
+    int iy[kLMaxTaps];
+    int n_even;            // taps [0, n_even) have even offsets, [n_even, n) odd
+    int n;
+};
+
+struct DenseList {
+    float k[kMaxDense * kMaxDense];  // K[a][b] multiplies in[y + dy0 + a][x + dx0' + b]
+    int D;
+    int col_shift;                   // stencil column 0 relative to the smem tile column of x
+};
+
+struct LGeom {
+    int H, W, C;
+    int dx0, dy0;      // smem (0,0) <-> global (tx0 + dx0, ty0 + dy0); dx0 even
+    int pitch, rows;   // pitch = 2 mod 4
+    int boundary;
+    int accumulate;
+};
+
+// ---------------------------------------------------------------- loaders ---
+__device__ __forceinline__ void cp_async8(float *dst, const float *src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(valid ? 8 : 0));
+}
+
+// One channel plane of the halo tile into s[rows][pitch].  `frame` points at
+// the (H, W, C) HWC frame or the (C, H, W) planar frame.
+template <typename TI, bool PLANAR>
+__device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ frame, const LGeom &g,
+                                           int c, int gx0, int gy0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool clamp = g.boundary == SKC_CLAMP;
+    const int H = g.H, W = g.W, C = g.C;
+    if constexpr (PLANAR) {
+        static_assert(sizeof(TI) == 4, "planar intermediates are fp32");
+        const float *plane = reinterpret_cast<const float *>(frame) + (long long)c * H * W;
+        const bool pairs_ok = (W & 1) == 0;  // 8-byte alignment of row starts
+        for (int r = warp; r < g.rows; r += nw) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const float *src = plane + (long long)gy * W;
+            float *dst = s + r * g.pitch;
+            for (int p = lane; 2 * p < g.pitch; p += 32) {
+                const int col = 2 * p;
+                const int gx = gx0 + col;
+                if (pairs_ok && gx >= 0 && gx + 1 < W) {
+                    cp_async8(dst + col, src + gx, rowin);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int x = gx + u;
+                        const bool ok = clamp || (rowin && x >= 0 && x < W);
+                        cp_async4(dst + col + u, src + min(max(x, 0), W - 1), ok);
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();
+    } else if constexpr (sizeof(TI) == 4) {
+        const float *img = reinterpret_cast<const float *>(frame);
+        for (int r = warp; r < g.rows; r += nw) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const float *src = img + (long long)gy * W * C + c;
+            float *dst = s + r * g.pitch;
+#pragma unroll 4
+            for (int col = lane; col < g.pitch; col += 32) {
+                const int gx = gx0 + col;
+                const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                cp_async4(dst + col, src + (long long)min(max(gx, 0), W - 1) * C, ok);
+            }
+        }
+        cp_async_wait_all();
+    } else {
+        constexpr int U = 8;
+        for (int r = warp; r < g.rows; r += nw) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const TI *src = frame + (long long)gy * W * C + c;
+            float *dst = s + r * g.pitch;
+            for (int c0 = lane; c0 < g.pitch; c0 += 32 * U) {
+                float v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int col = c0 + 32 * u;
+                    const int gx = gx0 + col;
+                    const bool ok = col < g.pitch && (clamp || (rowin && gx >= 0 && gx < W));
+                    v[u] = ok ? IO<TI>::ld(src + (long long)min(max(gx, 0), W - 1) * C) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (c0 + 32 * u < g.pitch) dst[c0 + 32 * u] = v[u];
+            }
+        }
+    }
+}
+
+// Store a KR x 8 block of one channel.
+template <int KR, typename TO, bool PLANAR>
+__device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom &g, int c, int gy0,
+                                            int gx0, const float (&acc)[KR][8]) {
+    const int H = g.H, W = g.W, C = g.C;
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+        const int gy = gy0 + r;
+        if (gy >= H) continue;
+        if constexpr (PLANAR) {
+            float *row = reinterpret_cast<float *>(frame) + ((long long)c * H + gy) * W;
+            float *p = row + gx0;
+            if (gx0 + 7 < W && ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && !g.accumulate) {
+                reinterpret_cast<float4 *>(p)[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+                reinterpret_cast<float4 *>(p)[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (gx0 + j < W) p[j] = g.accumulate ? p[j] + acc[r][j] : acc[r][j];
+            }
+        } else {
+            TO *row = frame + (long long)gy * W * C + c;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (gx0 + j < W) store_px<TO>(row + (long long)(gx0 + j) * C, acc[r][j], g.accumulate);
+        }
+    }
+}
+
+// --------------------------------------------------------------- tap path ---
+constexpr int kTKR = 5, kTWX = 4, kTWY = 2;       // 256 threads, tile 128 x 80
+constexpr int kTTW = kTWX * 32, kTTH = kTWY * 8 * kTKR;
+
+template <int KR>
+__device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, int pitch, float4 w,
+                                         bool odd) {
+    float a[9], b[9];
+    auto load_row = [&](const float *q, float (&v)[9]) {
+        if (!odd) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 t = reinterpret_cast<const float2 *>(q)[k];
+                v[2 * k] = t.x;
+                v[2 * k + 1] = t.y;
+            }
+            v[8] = q[8];
+        } else {
+            v[0] = q[0];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 t = reinterpret_cast<const float2 *>(q + 1)[k];
+                v[2 * k + 1] = t.x;
+                v[2 * k + 2] = t.y;
+            }
+        }
+    };
+    load_row(p, a);
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+        load_row(p + (r + 1) * pitch, b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float v = acc[r][j];
+            v = fmaf(w.x, a[j], v);
+            v = fmaf(w.y, a[j + 1], v);
+            v = fmaf(w.z, b[j], v);
+            v = fmaf(w.w, b[j + 1], v);
+            acc[r][j] = v;
+        }
+#pragma unroll
+        for (int j = 0; j < 9; ++j) a[j] = b[j];
+    }
+}
+
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+__global__ void __launch_bounds__(kTWX *kTWY * 32)
+    layer_tap_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                     const __grid_constant__ TapList tl) {
+    extern __shared__ __align__(16) float smem[];
+    const int C = g.C;
+    const int b = blockIdx.z / C, c = blockIdx.z - (blockIdx.z / C) * C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = blockIdx.x * kTTW, ty0 = blockIdx.y * kTTH;
+    load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * kTKR + ly * kTKR;
+    const float *base = smem + row0 * g.pitch + col0;
+
+    float acc[kTKR][8];
+#pragma unroll
+    for (int r = 0; r < kTKR; ++r)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+#pragma unroll 1
+    for (int i = 0; i < tl.n_even; ++i) tap_rows<kTKR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+#pragma unroll 1
+    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<kTKR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+
+    store_block<kTKR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
+// ------------------------------------------------------------- dense path ---
+constexpr int kDenKR = 5, kDenWX = 4, kDenWY = 2;  // 256 threads, tile 128 x 80
+constexpr int kDenTW = kDenWX * 32, kDenTH = kDenWY * 8 * kDenKR;
+
+template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+__global__ void __launch_bounds__(kDenWX *kDenWY * 32)
+    layer_stencil_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                         const __grid_constant__ DenseList dl) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kDenKR;
+    const int C = g.C;
+    const int b = blockIdx.z / C, c = blockIdx.z - (blockIdx.z / C) * C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = blockIdx.x * kDenTW, ty0 = blockIdx.y * kDenTH;
+    load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kDenWX, wy = warp / kDenWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * KR + ly * KR;
+    const float *pc = smem + row0 * g.pitch + col0 + dl.col_shift;
+    const int pitch = g.pitch;
+
+    float acc[KR][8];
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int r = 0; r < KR + D - 1; ++r) {
+        float w[8 + D - 1];
+#pragma unroll
+        for (int j = 0; j < 8 + D - 1; ++j) w[j] = pc[r * pitch + j];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int i = r - a;
+            if (i < 0 || i >= KR) continue;
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                const float k = dl.k[a * D + bb];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
+            }
+        }
+    }
+    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
+// ------------------------------------------------ direct (huge halo) path ---
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+__global__ void __launch_bounds__(256)
+    layer_gather_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                        const __grid_constant__ TapList tl) {
+    const int C = g.C;
+    const int b = blockIdx.y / C, c = blockIdx.y - (blockIdx.y / C) * C;
+    const long long hw = (long long)g.H * g.W, fs = hw * C;
+    in += b * fs;
+    out += b * fs;
+    const long long ps = IN_PL ? 1 : C, cs = IN_PL ? hw : 1;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < hw;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(p / g.W), x = (int)(p - (long long)y * g.W);
+        float acc = 0.f;
+        for (int i = 0; i < tl.n; ++i) {
+            const float4 w = tl.cw[i];
+            const float cw[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int yy = y + tl.iy[i] + (k >> 1), xx = x + tl.ix[i] + (k & 1);
+                if (g.boundary == SKC_CLAMP) {
+                    yy = min(max(yy, 0), g.H - 1);
+                    xx = min(max(xx, 0), g.W - 1);
+                } else if (yy < 0 || yy >= g.H || xx < 0 || xx >= g.W) {
+                    continue;
+                }
+                acc = fmaf(cw[k], IO<TI>::ld(in + ((long long)yy * g.W + xx) * ps + c * cs), acc);
+            }
+        }
+        TO *o = OUT_PL ? out + c * hw + p : out + p * C + c;
+        store_px<TO>(o, acc, g.accumulate);
+    }
+}
+
+// ------------------------------------------------------------------ host ---
+struct Plan {
+    std::vector<int> ix, iy;
+    std::vector<double> cw;  // 4 per tap, float64 (sample_shifted order)
+    int dx_min = 0, dx_max = 0, dy_min = 0, dy_max = 0;  // corner footprint (inclusive)
+};
+
+// sample_shifted (engine.py:118-130): ix = floor(ox), fx = ox - ix, corners 00, 10, 01, 11.
+static Plan plan_taps(const double *taps, int S) {
+    Plan p;
+    p.ix.resize(S);
+    p.iy.resize(S);
+    p.cw.resize(4 * (size_t)S);
+    for (int i = 0; i < S; ++i) {
+        const double ox = taps[3 * i], oy = taps[3 * i + 1], w = taps[3 * i + 2];
+        const double fx0 = std::floor(ox), fy0 = std::floor(oy);
+        const double fx = ox - fx0, fy = oy - fy0;
+        p.ix[i] = (int)fx0;
+        p.iy[i] = (int)fy0;
+        p.cw[4 * i + 0] = w * (1.0 - fx) * (1.0 - fy);
+        p.cw[4 * i + 1] = w * fx * (1.0 - fy);
+        p.cw[4 * i + 2] = w * (1.0 - fx) * fy;
+        p.cw[4 * i + 3] = w * fx * fy;
+        if (i == 0 || p.ix[i] < p.dx_min) p.dx_min = p.ix[i];
+        if (i == 0 || p.ix[i] + 1 > p.dx_max) p.dx_max = p.ix[i] + 1;
+        if (i == 0 || p.iy[i] < p.dy_min) p.dy_min = p.iy[i];
+        if (i == 0 || p.iy[i] + 1 > p.dy_max) p.dy_max = p.iy[i] + 1;
+    }
+    return p;
+}
+
+static bool dense_allowed() {
+    static const bool on = [] {
+        const char *e = std::getenv("SKC_DENSE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+static int floor_even(int v) { return v & ~1; }
+
+static LGeom make_geom(int H, int W, int C, int boundary, int accumulate, int tw, int th, int dx_min,
+                       int dx_max, int dy_min, int dy_max) {
+    LGeom g;
+    g.H = H;
+    g.W = W;
+    g.C = C;
+    g.boundary = boundary;
+    g.accumulate = accumulate;
+    g.dx0 = floor_even(dx_min);
+    g.dy0 = dy_min;
+    int pitch = tw + (dx_max - g.dx0) + 1;  // +1: the odd-tap window reads one column past
+    pitch = (pitch + 3) & ~3;
+    pitch += 2;                              // pitch = 2 mod 4
+    g.pitch = pitch;
+    g.rows = th + (dy_max - dy_min);
+    return g;
+}
+
+template <typename K>
+static int set_smem_attr(K kern) {
+    SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    return SKC_OK;
+}
+
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+static int launch_taps(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int t0,
+                       int t1, int boundary, int accumulate, cudaStream_t s) {
+    int dx_min = 1 << 30, dx_max = -(1 << 30), dy_min = 1 << 30, dy_max = -(1 << 30);
+    for (int i = t0; i < t1; ++i) {
+        dx_min = std::min(dx_min, pl.ix[i]);
+        dx_max = std::max(dx_max, pl.ix[i] + 1);
+        dy_min = std::min(dy_min, pl.iy[i]);
+        dy_max = std::max(dy_max, pl.iy[i] + 1);
+    }
+    LGeom g = make_geom(H, W, C, boundary, accumulate, kTTW, kTTH, dx_min, dx_max, dy_min, dy_max);
+    TapList tl;
+    tl.n = t1 - t0;
+    int k = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) tl.n_even = k;
+        for (int i = t0; i < t1; ++i) {
+            const int off = (pl.iy[i] - g.dy0) * g.pitch + (pl.ix[i] - g.dx0);
+            if ((off & 1) != pass) continue;
+            tl.off[k] = off;
+            tl.ix[k] = pl.ix[i];
+            tl.iy[k] = pl.iy[i];
+            tl.cw[k] = make_float4((float)pl.cw[4 * i], (float)pl.cw[4 * i + 1], (float)pl.cw[4 * i + 2],
+                                   (float)pl.cw[4 * i + 3]);
+            ++k;
+        }
+    }
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    const TI *pin = static_cast<const TI *>(in);
+    TO *pout = static_cast<TO *>(out);
+    if (smem <= (size_t)kMaxSmem) {
+        auto kern = layer_tap_kernel<TI, TO, IN_PL, OUT_PL>;
+        static int attr = set_smem_attr(kern);
+        if (attr) return attr;
+        dim3 grid(ceil_div(W, kTTW), ceil_div(H, kTTH), B * C);
+        kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
+        SKC_LAUNCH_CHECK("layer_tap_kernel");
+    } else {
+        const long long hw = (long long)H * W;
+        dim3 grid((unsigned)std::min<long long>((hw + 255) / 256, 148 * 8), B * C);
+        layer_gather_kernel<TI, TO, IN_PL, OUT_PL><<<grid, 256, 0, s>>>(pin, pout, g, tl);
+        SKC_LAUNCH_CHECK("layer_gather_kernel");
+    }
+    return SKC_OK;
+}
+
+template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int C, const DenseList &dl,
+                            const LGeom &g, cudaStream_t s) {
+    auto kern = layer_stencil_kernel<D, TI, TO, IN_PL, OUT_PL>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    dim3 grid(ceil_div(W, kDenTW), ceil_div(H, kDenTH), B * C);
+    kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);
+    SKC_LAUNCH_CHECK("layer_stencil_kernel");
+    return SKC_OK;
+}
+
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int S,
+                        int boundary, cudaStream_t s, int *rc) {
+    if (!dense_allowed()) return false;
+    const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
+    const int D = dense_size_for(std::max(sx, sy));
+    if (D == 0 || D * D >= 4 * S) return false;
+    DenseList dl;
+    double k[kMaxDense * kMaxDense] = {0.0};
+    for (int i = 0; i < S; ++i)
+        for (int q = 0; q < 4; ++q) {
+            const int a = pl.iy[i] + (q >> 1) - pl.dy_min, bb = pl.ix[i] + (q & 1) - pl.dx_min;
+            k[a * D + bb] += pl.cw[4 * i + q];
+        }
+    dl.D = D;
+    for (int e = 0; e < kMaxDense * kMaxDense; ++e) dl.k[e] = e < D * D ? (float)k[e] : 0.f;
+    LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenTH, pl.dx_min, pl.dx_min + D - 1,
+                        pl.dy_min, pl.dy_min + D - 1);
+    dl.col_shift = pl.dx_min - g.dx0;
+    switch (D) {
+        case 3: *rc = launch_stencil_d<3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        case 5: *rc = launch_stencil_d<5, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        case 7: *rc = launch_stencil_d<7, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        default: *rc = launch_stencil_d<9, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+    }
+    return true;
+}
+
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+static int layer_t(const void *in, void *out, int B, int H, int W, int C, const double *taps, int S,
+                   int boundary, cudaStream_t s) {
+    const Plan pl = plan_taps(taps, S);
+    int rc = SKC_OK;
+    if (try_stencil<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, S, boundary, s, &rc)) return rc;
+    if (S <= kLMaxTaps)
+        return launch_taps<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, 0, S, boundary, 0, s);
+    // long layers: accumulate chunks into an fp32 destination
+    if constexpr (std::is_same<TO, float>::value) {
+        for (int t0 = 0; t0 < S && rc == SKC_OK; t0 += kLMaxTaps)
+            rc = launch_taps<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, t0, std::min(S, t0 + kLMaxTaps),
+                                                    boundary, t0 > 0, s);
+        return rc;
+    } else {
+        return -1;  // caller routes fp16 outputs of long layers through fp32
+    }
+}
+
+// Dispatch on (input dtype, output dtype, input planar, output planar).
+int layer_dispatch(const void *in, int idt, bool in_pl, void *out, int odt, bool out_pl, int B, int H,
+                   int W, int C, const double *taps, int S, int boundary, cudaStream_t s) {
+    if (in_pl && idt != SKC_F32) return fail(SKC_EBADARG, "planar intermediates are fp32");
+    if (out_pl && odt != SKC_F32) return fail(SKC_EBADARG, "planar intermediates are fp32");
+    if (in_pl && out_pl) return layer_t<float, float, true, true>(in, out, B, H, W, C, taps, S, boundary, s);
+    if (in_pl) {
+        if (odt == SKC_F32) return layer_t<float, float, true, false>(in, out, B, H, W, C, taps, S, boundary, s);
+        return layer_t<float, __half, true, false>(in, out, B, H, W, C, taps, S, boundary, s);
+    }
+    if (out_pl) {
+        if (idt == SKC_F32) return layer_t<float, float, false, true>(in, out, B, H, W, C, taps, S, boundary, s);
+        return layer_t<__half, float, false, true>(in, out, B, H, W, C, taps, S, boundary, s);
+    }
+    if (idt == SKC_F32 && odt == SKC_F32) return layer_t<float, float, false, false>(in, out, B, H, W, C, taps, S, boundary, s);
+    if (idt == SKC_F16 && odt == SKC_F32) return layer_t<__half, float, false, false>(in, out, B, H, W, C, taps, S, boundary, s);
+    if (idt == SKC_F32 && odt == SKC_F16) return layer_t<float, __half, false, false>(in, out, B, H, W, C, taps, S, boundary, s);
+    return layer_t<__half, __half, false, false>(in, out, B, H, W, C, taps, S, boundary, s);
+}
+
+int dense_size_for(int span) {
+    if (span <= 3) return 3;
+    if (span <= 5) return 5;
+    if (span <= 7) return 7;
+    if (span <= 9) return 9;
+    return 0;
+}
+
+bool finite_taps(const double *taps, int n) {
+    for (int i = 0; i < 3 * n; ++i)
+        if (!std::isfinite(taps[i])) return false;
+    return true;
+}
+
+int check_image_args(const void *in, int idt, const void *out, int odt, int B, int H, int W, int C,
+                     int boundary) {
+    if (!in || !out) return fail(SKC_EBADARG, "null image pointer");
+    if (B < 1 || H < 1 || W < 1) return fail(SKC_EBADARG, "image dimensions must be positive");
+    if (C < 1 || C > 4) return fail(SKC_EBADARG, "channels must be 1..4");
+    if ((idt != SKC_F32 && idt != SKC_F16) || (odt != SKC_F32 && odt != SKC_F16))
+        return fail(SKC_EBADARG, "dtype must be SKC_F32 or SKC_F16");
+    if (boundary != SKC_ZERO && boundary != SKC_CLAMP)
+        return fail(SKC_EBADARG, "boundary must be SKC_ZERO or SKC_CLAMP");
+    if ((long long)H * W >= (1LL << 31)) return fail(SKC_EBADARG, "image too large (H*W >= 2^31)");
+    if ((long long)B * C > 65535) return fail(SKC_EBADARG, "batch*channels must be <= 65535 per call");
+    return SKC_OK;
+}
+
+template <typename TI, typename TO>
+__global__ void convert_kernel(const TI *__restrict__ in, TO *__restrict__ out, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        IO<TO>::st(out + i, IO<TI>::ld(in + i));
+}
+
+// HWC output layer with the long-layer fp16 fallback (fp32 temporary + convert).
+static int last_layer(const void *in, int idt, bool in_pl, void *out, int odt, int B, int H, int W,
+                      int C, const double *taps, int S, int boundary, cudaStream_t s) {
+    int rc = layer_dispatch(in, idt, in_pl, out, odt, false, B, H, W, C, taps, S, boundary, s);
+    if (rc != -1) return rc;
+    const long long n = (long long)B * H * W * C;
+    void *tmp = nullptr;
+    if ((rc = pool_alloc(&tmp, (size_t)n * sizeof(float), s))) return rc;
+    rc = layer_dispatch(in, idt, in_pl, tmp, SKC_F32, false, B, H, W, C, taps, S, boundary, s);
+    if (rc == SKC_OK) {
+        const unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 32);
+        convert_kernel<float, __half><<<grid, 256, 0, s>>>((const float *)tmp, (__half *)out, n);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "convert_kernel");
+    }
+    pool_free(tmp, s);
+    return rc;
+}
+
+}  // namespace skc
+
+using namespace skc;
+
+extern "C" {
+
+int skc_max_taps(void) { return kLMaxTaps; }
+
+int skc_layer_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
+                  int C, const double *taps, int S, int boundary, void *stream) {
+    int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
+    if (rc) return rc;
+    if (S < 1 || !taps) return fail(SKC_EBADARG, "sparse layer needs at least one sample");
+    if (!finite_taps(taps, S)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
+    return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, S, boundary,
+                      (cudaStream_t)stream);
+}
+
+int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
+                  int C, const double *taps, const int *layout, int L, int boundary, void *stream) {
+    int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
+    if (rc) return rc;
+    if (L < 1 || !layout || !taps) return fail(SKC_EBADARG, "kernel complex needs at least one layer");
+    long long total = 0;
+    for (int l = 0; l < L; ++l) {
+        if (layout[l] < 1) return fail(SKC_EBADARG, "sparse layer needs at least one sample");
+        total += layout[l];
+    }
+    if (!finite_taps(taps, (int)total)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (L == 1) return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, layout[0], boundary, s);
+    // intermediates: fp32 planar (B, C, H, W), ping-pong
+    const size_t n = (size_t)B * H * W * C;
+    void *buf[2] = {nullptr, nullptr};
+    const int nbuf = L > 2 ? 2 : 1;
+    for (int i = 0; i < nbuf; ++i) {
+        rc = pool_alloc(&buf[i], n * sizeof(float), s);
+        if (rc) { for (int j = 0; j < i; ++j) pool_free(buf[j], s); return rc; }
+    }
+    const double *tp = taps;
+    for (int l = 0; l < L && rc == SKC_OK; ++l) {
+        const bool first = l == 0, last = l == L - 1;
+        const void *src = first ? in : buf[(l - 1) & 1];
+        if (last)
+            rc = last_layer(src, SKC_F32, true, out, out_dtype, B, H, W, C, tp, layout[l], boundary, s);
+        else
+            rc = layer_dispatch(src, first ? in_dtype : SKC_F32, !first, buf[l & 1], SKC_F32, true, B, H,
+                                W, C, tp, layout[l], boundary, s);
+        tp += 3 * layout[l];
+    }
+    for (int i = 0; i < nbuf; ++i) pool_free(buf[i], s);
+    return rc;
+}
+
+}  // extern "C"

@@ -103,12 +103,11 @@ __device__ __forceinline__ void store_px<float>(float *p, float v, int accumulat
 // Dense-stencil path (skc_dense.cu): a layer whose merged corner footprint
 // fits a D x D window (D <= 9) and costs fewer FMAs than 4 per tap.
 constexpr int kMaxDense = 9;
-struct DenseTable {
-    float k[kMaxDense * kMaxDense];  // K[a][b] multiplies in[y + dy0 + a][x + dx0 + b]
-    int D;
-};
-int launch_dense(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
-                 const DenseTable &dt, int dx0, int dy0, int boundary, cudaStream_t s);
 int dense_size_for(int span);  // smallest compiled D >= span, or 0
+
+// Argument checks shared by the image entry points (skc_layer.cu).
+int check_image_args(const void *in, int idt, const void *out, int odt, int B, int H, int W, int C,
+                     int boundary);
+bool finite_taps(const double *taps, int n);
 
 }  // namespace skc
