@@ -194,18 +194,23 @@ class Chain:
         dt_store = nat.SKC_F16 if self.out.dtype != self.bufs[0].dtype else nat.SKC_F32
         src, sdt = self.frames, dt_store
         L = len(self.taps)
+        # the layer sequence skc_chain_fwd runs: HWC -> planar fp32 -> ... -> HWC,
+        # issued one layer at a time so each launch can be timed
+        lay_in = nat.SKC_HWC
         for l, t in enumerate(self.taps):
             last = l == L - 1
             dst, ddt = (self.out, dt_store) if last else (self.bufs[l & 1], nat.SKC_F32)
+            lay_out = nat.SKC_HWC if last else nat.SKC_CHW
             if events is not None:
                 events[l][0].record(stream)
-            rc = lib.skc_layer_fwd(nat.ptr(src), sdt, nat.ptr(dst), ddt, self.nf, self.h, self.w, self.c,
-                                   nat.dbl(t), t.shape[0], 0 if self.boundary == "zero" else 1, sp)
+            rc = lib.skc_layer_fwd_ex(nat.ptr(src), sdt, lay_in, nat.ptr(dst), ddt, lay_out, self.nf, self.h,
+                                      self.w, self.c, nat.dbl(t), t.shape[0],
+                                      0 if self.boundary == "zero" else 1, sp)
             if rc:
                 raise RuntimeError(nat.last_error())
             if events is not None:
                 events[l][1].record(stream)
-            src, sdt = dst, ddt
+            src, sdt, lay_in = dst, ddt, lay_out
 
     def pre_step(self):
         if self.flush is not None:

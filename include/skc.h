@@ -72,6 +72,21 @@ int skc_layer_fwd(const void *in, int in_dtype, void *out, int out_dtype,
                   int B, int H, int W, int C,
                   const double *taps, int S, int boundary, void *stream);
 
+/* memory layouts for skc_layer_fwd_ex: HWC interleaved (the reference's) or
+ * planar CHW (the chain's internal fp32 intermediate layout) */
+#define SKC_HWC 0
+#define SKC_CHW 1
+
+/*
+ * skc_layer_fwd with explicit layouts: in/out each (B, H, W, C) HWC or
+ * (B, C, H, W) planar.  Planar tensors must be fp32.  This is the per-layer
+ * step skc_chain_fwd runs (first layer HWC -> CHW, inner CHW -> CHW, last
+ * CHW -> HWC), exposed so callers can drive/time layers individually.
+ */
+int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
+                     int out_layout, int B, int H, int W, int C,
+                     const double *taps, int S, int boundary, void *stream);
+
 /*
  * A chain of L layers (engine.apply_complex, engine.py:173-178).  Intermediate
  * images stay fp32 in pool scratch; only `in` and `out` use the given dtypes.

@@ -21,13 +21,14 @@ LIB_PATH = PKG / "libskc.so"
 SKC_OK, SKC_EBADARG, SKC_ENONFINITE, SKC_ETRUNC, SKC_ECUDA, SKC_EDEGENERATE = 0, 1, 2, 3, 4, 5
 SKC_F32, SKC_F16 = 0, 1
 SKC_ZERO, SKC_CLAMP = 0, 1
+SKC_HWC, SKC_CHW = 0, 1
 LOSS_IDS = {"charbonnier": 0, "l1": 1, "l2": 2}
 WN_IDS = {"none": 0, "sum": 1, "sofm": 2}
 FIT_HDR = 8
 
 # Symbols declared in include/skc.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_chain_fwd",
+    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_chain_fwd",
     "skc_sv_fwd", "skc_ir_batch", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step",
 )
@@ -72,6 +73,7 @@ def _declare(lib):
     lib.skc_last_error.restype = ctypes.c_char_p
     lib.skc_max_taps.restype = _i
     lib.skc_layer_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _i, _i, _vp]
+    lib.skc_layer_fwd_ex.argtypes = [_vp, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _dp, _i, _i, _vp]
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,
                                _vp]

@@ -215,9 +215,9 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
                      const __grid_constant__ TapList tl) {
     extern __shared__ __align__(16) float smem[];
     const int C = g.C;
-    const int b = blockIdx.z / C, c = blockIdx.z - (blockIdx.z / C) * C;
+    const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = blockIdx.x * kTTW, ty0 = blockIdx.y * kTTH;
+    const int tx0 = (blockIdx.x / C) * kTTW, ty0 = blockIdx.y * kTTH;
     load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
@@ -251,9 +251,9 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     extern __shared__ __align__(16) float smem[];
     constexpr int KR = kDenKR;
     const int C = g.C;
-    const int b = blockIdx.z / C, c = blockIdx.z - (blockIdx.z / C) * C;
+    const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = blockIdx.x * kDenTW, ty0 = blockIdx.y * kDenTH;
+    const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * kDenTH;
     load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
@@ -423,7 +423,7 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
         auto kern = layer_tap_kernel<TI, TO, IN_PL, OUT_PL>;
         static int attr = set_smem_attr(kern);
         if (attr) return attr;
-        dim3 grid(ceil_div(W, kTTW), ceil_div(H, kTTH), B * C);
+        dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, kTTH), B);
         kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
         SKC_LAUNCH_CHECK("layer_tap_kernel");
     } else {
@@ -442,7 +442,7 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
-    dim3 grid(ceil_div(W, kDenTW), ceil_div(H, kDenTH), B * C);
+    dim3 grid(ceil_div(W, kDenTW) * C, ceil_div(H, kDenTH), B);
     kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);
     SKC_LAUNCH_CHECK("layer_stencil_kernel");
     return SKC_OK;
@@ -539,7 +539,7 @@ int check_image_args(const void *in, int idt, const void *out, int odt, int B, i
     if (boundary != SKC_ZERO && boundary != SKC_CLAMP)
         return fail(SKC_EBADARG, "boundary must be SKC_ZERO or SKC_CLAMP");
     if ((long long)H * W >= (1LL << 31)) return fail(SKC_EBADARG, "image too large (H*W >= 2^31)");
-    if ((long long)B * C > 65535) return fail(SKC_EBADARG, "batch*channels must be <= 65535 per call");
+    if (B > 65535) return fail(SKC_EBADARG, "batch must be <= 65535 frames per call");
     return SKC_OK;
 }
 
@@ -585,6 +585,23 @@ int skc_layer_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     if (!finite_taps(taps, S)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
     return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, S, boundary,
                       (cudaStream_t)stream);
+}
+
+int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
+                     int out_layout, int B, int H, int W, int C, const double *taps, int S,
+                     int boundary, void *stream) {
+    int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
+    if (rc) return rc;
+    if (S < 1 || !taps) return fail(SKC_EBADARG, "sparse layer needs at least one sample");
+    if (!finite_taps(taps, S)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
+    if ((in_layout != SKC_HWC && in_layout != SKC_CHW) || (out_layout != SKC_HWC && out_layout != SKC_CHW))
+        return fail(SKC_EBADARG, "layout must be SKC_HWC or SKC_CHW");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (out_layout == SKC_HWC)
+        return last_layer(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, B, H, W, C, taps, S, boundary, s);
+    rc = layer_dispatch(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, true, B, H, W, C, taps, S,
+                        boundary, s);
+    return rc == -1 ? fail(SKC_EBADARG, "planar output must be fp32") : rc;
 }
 
 int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
