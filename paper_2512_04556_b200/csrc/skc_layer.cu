@@ -165,8 +165,8 @@ __device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom 
 }
 
 // --------------------------------------------------------------- tap path ---
-constexpr int kTKR = 5, kTWX = 4, kTWY = 2;       // 256 threads, tile 128 x 80
-constexpr int kTTW = kTWX * 32, kTTH = kTWY * 8 * kTKR;
+constexpr int kTWX = 4, kTWY = 2;                 // 256 threads, tile 128 x (16 * KR)
+constexpr int kTTW = kTWX * 32;
 
 template <int KR>
 __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, int pitch, float4 w,
@@ -209,7 +209,7 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
     }
 }
 
-template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+template <int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(kTWX *kTWY * 32)
     layer_tap_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
                      const __grid_constant__ TapList tl) {
@@ -217,27 +217,28 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
     const int C = g.C;
     const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = (blockIdx.x / C) * kTTW, ty0 = blockIdx.y * kTTH;
+    constexpr int TH = kTWY * 8 * KR;
+    const int tx0 = (blockIdx.x / C) * kTTW, ty0 = blockIdx.y * TH;
     load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
     const int col0 = wx * 32 + lx * 8;
-    const int row0 = wy * 8 * kTKR + ly * kTKR;
+    const int row0 = wy * 8 * KR + ly * KR;
     const float *base = smem + row0 * g.pitch + col0;
 
-    float acc[kTKR][8];
+    float acc[KR][8];
 #pragma unroll
-    for (int r = 0; r < kTKR; ++r)
+    for (int r = 0; r < KR; ++r)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
 #pragma unroll 1
-    for (int i = 0; i < tl.n_even; ++i) tap_rows<kTKR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
 #pragma unroll 1
-    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<kTKR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
 
-    store_block<kTKR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
 // ------------------------------------------------------------- dense path ---
@@ -389,6 +390,16 @@ static int set_smem_attr(K kern) {
     return SKC_OK;
 }
 
+// Rows per thread of the tap kernel: SKC_TAP_KR (5 or 7) overrides; default 7
+// when the halo tile of a 7-row block still leaves two CTAs per SM, else 5.
+static int tap_kr_override() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_TAP_KR");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_taps(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int t0,
                        int t1, int boundary, int accumulate, cudaStream_t s) {
@@ -399,7 +410,13 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
         dy_min = std::min(dy_min, pl.iy[i]);
         dy_max = std::max(dy_max, pl.iy[i] + 1);
     }
-    LGeom g = make_geom(H, W, C, boundary, accumulate, kTTW, kTTH, dx_min, dx_max, dy_min, dy_max);
+    int KR = tap_kr_override();
+    if (KR != 5 && KR != 7) {
+        const LGeom g7 = make_geom(H, W, C, boundary, accumulate, kTTW, kTWY * 8 * 7, dx_min, dx_max, dy_min, dy_max);
+        KR = ((size_t)g7.rows * g7.pitch * sizeof(float) * 2 <= (size_t)kMaxSmem) ? 7 : 5;
+    }
+    const int TH = kTWY * 8 * KR;
+    LGeom g = make_geom(H, W, C, boundary, accumulate, kTTW, TH, dx_min, dx_max, dy_min, dy_max);
     TapList tl;
     tl.n = t1 - t0;
     int k = 0;
@@ -420,10 +437,11 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
     if (smem <= (size_t)kMaxSmem) {
-        auto kern = layer_tap_kernel<TI, TO, IN_PL, OUT_PL>;
-        static int attr = set_smem_attr(kern);
-        if (attr) return attr;
-        dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, kTTH), B);
+        auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>;
+        static int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
+        static int attr7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>);
+        if (attr5 || attr7) return attr5 ? attr5 : attr7;
+        dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
         kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
         SKC_LAUNCH_CHECK("layer_tap_kernel");
     } else {
