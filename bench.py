@@ -164,15 +164,17 @@ class Chain:
         self.bufs = [torch.empty(npx, dtype=torch.float32, device=dev) for _ in range(2)]
         self.out = torch.empty_like(frames)
         self.taps = [np.ascontiguousarray(l.taps()) for l in self.cpx.layers]
-        self.launches_per_step = len(self.taps)
+        pol = int(os.environ.get("SKC_CHAIN_IO", "2"))
+        self.launches_per_step = len(self.taps) + (2 if pol == 1 else 1 if pol == 2 else 0)
         self.units_per_step = self.nf * self.h * self.w
         esz = 2 if self.storage == torch.float16 else 4
         # algorithmic HBM bytes per launch: image in + out in their storage dtypes
+        px = self.nf * self.h * self.w * self.c
         self.alg_bytes = []
-        for l in range(len(self.taps)):
-            bi = esz if l == 0 else 4
-            bo = esz if l == len(self.taps) - 1 else 4
-            self.alg_bytes.append(self.nf * self.h * self.w * self.c * (bi + bo))
+        for k in range(self.launches_per_step):
+            bi = esz if k == 0 else 4
+            bo = esz if k == self.launches_per_step - 1 else 4
+            self.alg_bytes.append(px * (bi + bo))
         self.metric = {
             "c1": "filtered Mpix/s (1264x2665 RGB, 4 layers x 32 taps)",
             "c0": "filtered Mpix/s (512x512 RGB, 4 layers x 12 taps, clamp-to-edge)",
@@ -194,22 +196,35 @@ class Chain:
         dt_store = nat.SKC_F16 if self.out.dtype != self.bufs[0].dtype else nat.SKC_F32
         src, sdt = self.frames, dt_store
         L = len(self.taps)
-        # the layer sequence skc_chain_fwd runs: HWC -> planar fp32 -> ... -> HWC,
-        # issued one layer at a time so each launch can be timed
+        # the launch sequence skc_chain_fwd runs (SKC_CHAIN_IO policy: HWC in ->
+        # planar fp32 layers -> relayout to HWC out), issued one launch at a
+        # time so each can be timed
+        pol = int(os.environ.get("SKC_CHAIN_IO", "2"))
+        seq = []
+        if pol == 1:
+            seq.append(("relayout", None))
+        seq += [("layer", t) for t in self.taps]
+        if pol in (1, 2):
+            seq.append(("relayout", None))
+        bnd = 0 if self.boundary == "zero" else 1
         lay_in = nat.SKC_HWC
-        for l, t in enumerate(self.taps):
-            last = l == L - 1
-            dst, ddt = (self.out, dt_store) if last else (self.bufs[l & 1], nat.SKC_F32)
+        for k, (kind, t) in enumerate(seq):
+            last = k == len(seq) - 1
+            dst = self.out if last else self.bufs[k & 1]
+            ddt = dt_store if last else nat.SKC_F32
             lay_out = nat.SKC_HWC if last else nat.SKC_CHW
             if events is not None:
-                events[l][0].record(stream)
-            rc = lib.skc_layer_fwd_ex(nat.ptr(src), sdt, lay_in, nat.ptr(dst), ddt, lay_out, self.nf, self.h,
-                                      self.w, self.c, nat.dbl(t), t.shape[0],
-                                      0 if self.boundary == "zero" else 1, sp)
+                events[k][0].record(stream)
+            if kind == "relayout":
+                rc = lib.skc_relayout(nat.ptr(src), sdt, lay_in, nat.ptr(dst), ddt, lay_out, self.nf, self.h,
+                                      self.w, self.c, sp)
+            else:
+                rc = lib.skc_layer_fwd_ex(nat.ptr(src), sdt, lay_in, nat.ptr(dst), ddt, lay_out, self.nf,
+                                          self.h, self.w, self.c, nat.dbl(t), t.shape[0], bnd, sp)
             if rc:
                 raise RuntimeError(nat.last_error())
             if events is not None:
-                events[l][1].record(stream)
+                events[k][1].record(stream)
             src, sdt, lay_in = dst, ddt, lay_out
 
     def pre_step(self):

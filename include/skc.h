@@ -87,6 +87,10 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
                      int out_layout, int B, int H, int W, int C,
                      const double *taps, int S, int boundary, void *stream);
 
+/* Layout/dtype conversion HWC <-> planar fp32 (the chain's bracketing passes). */
+int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
+                 int out_layout, int B, int H, int W, int C, void *stream);
+
 /*
  * A chain of L layers (engine.apply_complex, engine.py:173-178).  Intermediate
  * images stay fp32 in pool scratch; only `in` and `out` use the given dtypes.

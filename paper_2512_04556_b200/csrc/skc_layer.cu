@@ -568,6 +568,51 @@ __global__ void convert_kernel(const TI *__restrict__ in, TO *__restrict__ out, 
         IO<TO>::st(out + i, IO<TI>::ld(in + i));
 }
 
+// Layout/dtype conversion between HWC and planar CHW, one thread per pixel:
+// C contiguous elements on the HWC side, C coalesced plane rows on the CHW side.
+template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+__global__ void relayout_kernel(const TI *__restrict__ in, TO *__restrict__ out, int B, long long hw, int C) {
+    const long long n = (long long)B * hw;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long b = q / hw, p = q - b * hw;
+        const long long fb = b * hw * C;
+#pragma unroll 4
+        for (int c = 0; c < C; ++c) {
+            const float v = IO<TI>::ld(in + fb + (IN_PL ? c * hw + p : p * C + c));
+            IO<TO>::st(out + fb + (OUT_PL ? c * hw + p : p * C + c), v);
+        }
+    }
+}
+
+int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_pl, int B, int H, int W,
+             int C, cudaStream_t s) {
+    const long long hw = (long long)H * W;
+    const unsigned grid = (unsigned)std::min<long long>((B * hw + 255) / 256, 148 * 32);
+#define SKC_RL(TI, TO, IP, OP) relayout_kernel<TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, C)
+    if (!in_pl && out_pl) {
+        if (idt == SKC_F32) SKC_RL(float, float, false, true); else SKC_RL(__half, float, false, true);
+    } else if (in_pl && !out_pl) {
+        if (odt == SKC_F32) SKC_RL(float, float, true, false); else SKC_RL(float, __half, true, false);
+    } else {
+        return fail(SKC_EBADARG, "relayout converts between HWC and planar fp32");
+    }
+#undef SKC_RL
+    SKC_LAUNCH_CHECK("relayout_kernel");
+    return SKC_OK;
+}
+
+// Chain I/O policy: 0 = the first layer reads HWC and the last writes HWC
+// directly; 1 = planar everywhere with relayout passes at both ends; 2 = only
+// the output side goes through a relayout pass (default).
+static int chain_policy() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_CHAIN_IO");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
 // HWC output layer with the long-layer fp16 fallback (fp32 temporary + convert).
 static int last_layer(const void *in, int idt, bool in_pl, void *out, int odt, int B, int H, int W,
                       int C, const double *taps, int S, int boundary, cudaStream_t s) {
@@ -622,6 +667,17 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
     return rc == -1 ? fail(SKC_EBADARG, "planar output must be fp32") : rc;
 }
 
+int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype, int out_layout,
+                 int B, int H, int W, int C, void *stream) {
+    int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, SKC_ZERO);
+    if (rc) return rc;
+    if (in_layout == out_layout) return fail(SKC_EBADARG, "relayout needs different layouts");
+    if ((in_layout == SKC_CHW && in_dtype != SKC_F32) || (out_layout == SKC_CHW && out_dtype != SKC_F32))
+        return fail(SKC_EBADARG, "planar tensors are fp32");
+    return relayout(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, out_layout == SKC_CHW, B, H, W, C,
+                    (cudaStream_t)stream);
+}
+
 int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
                   int C, const double *taps, const int *layout, int L, int boundary, void *stream) {
     int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
@@ -635,25 +691,42 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     if (!finite_taps(taps, (int)total)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
     cudaStream_t s = (cudaStream_t)stream;
     if (L == 1) return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, layout[0], boundary, s);
-    // intermediates: fp32 planar (B, C, H, W), ping-pong
+    // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
+    const int pol = chain_policy();
+    const bool pre = pol == 1, post = pol == 1 || pol == 2;
     const size_t n = (size_t)B * H * W * C;
     void *buf[2] = {nullptr, nullptr};
-    const int nbuf = L > 2 ? 2 : 1;
+    const int nbuf = (L > 2 || post || pre) ? 2 : 1;
     for (int i = 0; i < nbuf; ++i) {
         rc = pool_alloc(&buf[i], n * sizeof(float), s);
         if (rc) { for (int j = 0; j < i; ++j) pool_free(buf[j], s); return rc; }
     }
+    const void *src = in;
+    int sdt = in_dtype;
+    bool spl = false;
+    int k = 0;  // next scratch buffer
+    if (pre) {
+        rc = relayout(in, in_dtype, false, buf[0], SKC_F32, true, B, H, W, C, s);
+        src = buf[0];
+        sdt = SKC_F32;
+        spl = true;
+        k = 1;
+    }
     const double *tp = taps;
     for (int l = 0; l < L && rc == SKC_OK; ++l) {
-        const bool first = l == 0, last = l == L - 1;
-        const void *src = first ? in : buf[(l - 1) & 1];
-        if (last)
-            rc = last_layer(src, SKC_F32, true, out, out_dtype, B, H, W, C, tp, layout[l], boundary, s);
-        else
-            rc = layer_dispatch(src, first ? in_dtype : SKC_F32, !first, buf[l & 1], SKC_F32, true, B, H,
-                                W, C, tp, layout[l], boundary, s);
+        const bool last = l == L - 1;
+        if (last && !post) {
+            rc = last_layer(src, sdt, spl, out, out_dtype, B, H, W, C, tp, layout[l], boundary, s);
+        } else {
+            rc = layer_dispatch(src, sdt, spl, buf[k], SKC_F32, true, B, H, W, C, tp, layout[l], boundary, s);
+            src = buf[k];
+            sdt = SKC_F32;
+            spl = true;
+            k ^= 1;
+        }
         tp += 3 * layout[l];
     }
+    if (rc == SKC_OK && post) rc = relayout(src, SKC_F32, true, out, out_dtype, false, B, H, W, C, s);
     for (int i = 0; i < nbuf; ++i) pool_free(buf[i], s);
     return rc;
 }
