@@ -164,7 +164,10 @@ class Chain:
         self.bufs = [torch.empty(npx, dtype=torch.float32, device=dev) for _ in range(2)]
         self.out = torch.empty_like(frames)
         self.taps = [np.ascontiguousarray(l.taps()) for l in self.cpx.layers]
-        pol = int(os.environ.get("SKC_CHAIN_IO", "2"))
+        pol = int(os.environ.get("SKC_CHAIN_IO", "-1"))
+        if pol < 0:   # the library default (skc_layer.cu chain_policy)
+            pol = 1 if self.storage == torch.float16 else 2
+        self.policy = pol
         self.launches_per_step = len(self.taps) + (2 if pol == 1 else 1 if pol == 2 else 0)
         self.units_per_step = self.nf * self.h * self.w
         esz = 2 if self.storage == torch.float16 else 4
@@ -199,7 +202,7 @@ class Chain:
         # the launch sequence skc_chain_fwd runs (SKC_CHAIN_IO policy: HWC in ->
         # planar fp32 layers -> relayout to HWC out), issued one launch at a
         # time so each can be timed
-        pol = int(os.environ.get("SKC_CHAIN_IO", "2"))
+        pol = self.policy
         seq = []
         if pol == 1:
             seq.append(("relayout", None))

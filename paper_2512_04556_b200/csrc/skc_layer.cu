@@ -568,19 +568,92 @@ __global__ void convert_kernel(const TI *__restrict__ in, TO *__restrict__ out, 
         IO<TO>::st(out + i, IO<TI>::ld(in + i));
 }
 
-// Layout/dtype conversion between HWC and planar CHW, one thread per pixel:
-// C contiguous elements on the HWC side, C coalesced plane rows on the CHW side.
+// Layout/dtype conversion between HWC and planar CHW.  Each thread moves 4
+// consecutive pixels: on the HWC side that is 4*C contiguous elements
+// (vectorised 16-byte accesses when aligned), on the planar side 4 contiguous
+// elements of each of the C planes.
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+    static __device__ __forceinline__ void ld(const float *p, float *v) {
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+    static __device__ __forceinline__ void st(float *p, const float *v) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <> struct Vec4<__half> {
+    static __device__ __forceinline__ void ld(const __half *p, float *v) {
+        const uint2 t = *reinterpret_cast<const uint2 *>(p);
+        const __half2 a = *reinterpret_cast<const __half2 *>(&t.x), b = *reinterpret_cast<const __half2 *>(&t.y);
+        const float2 fa = __half22float2(a), fb = __half22float2(b);
+        v[0] = fa.x; v[1] = fa.y; v[2] = fb.x; v[3] = fb.y;
+    }
+    static __device__ __forceinline__ void st(__half *p, const float *v) {
+        const __half2 a = __floats2half2_rn(v[0], v[1]), b = __floats2half2_rn(v[2], v[3]);
+        uint2 t;
+        t.x = *reinterpret_cast<const unsigned *>(&a);
+        t.y = *reinterpret_cast<const unsigned *>(&b);
+        *reinterpret_cast<uint2 *>(p) = t;
+    }
+};
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
-__global__ void relayout_kernel(const TI *__restrict__ in, TO *__restrict__ out, int B, long long hw, int C) {
-    const long long n = (long long)B * hw;
-    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+__global__ void __launch_bounds__(256) relayout_kernel(const TI *__restrict__ in, TO *__restrict__ out, int B,
+                                                       long long hw, int C, int vec) {
+    const long long nq = (long long)B * ((hw + 3) / 4);
+    const long long qpf = (hw + 3) / 4;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
          q += (long long)gridDim.x * blockDim.x) {
-        const long long b = q / hw, p = q - b * hw;
+        const long long b = q / qpf, p0 = (q - b * qpf) * 4;
         const long long fb = b * hw * C;
-#pragma unroll 4
-        for (int c = 0; c < C; ++c) {
-            const float v = IO<TI>::ld(in + fb + (IN_PL ? c * hw + p : p * C + c));
-            IO<TO>::st(out + fb + (OUT_PL ? c * hw + p : p * C + c), v);
+        const int np = (int)min(4LL, hw - p0);
+        float v[4][4];
+        // gather 4 pixels x C channels
+        if (IN_PL) {
+            for (int c = 0; c < C; ++c) {
+                const TI *src = in + fb + c * hw + p0;
+                if (vec && np == 4) {
+                    float t[4];
+                    Vec4<TI>::ld(src, t);
+                    for (int k = 0; k < 4; ++k) v[k][c] = t[k];
+                } else {
+                    for (int k = 0; k < np; ++k) v[k][c] = IO<TI>::ld(src + k);
+                }
+            }
+        } else {
+            const TI *src = in + fb + p0 * C;
+            if (vec && np == 4) {
+                float t[16];
+                for (int j = 0; j < C; ++j) Vec4<TI>::ld(src + 4 * j, t + 4 * j);
+                for (int k = 0; k < 4; ++k)
+                    for (int c = 0; c < C; ++c) v[k][c] = t[k * C + c];
+            } else {
+                for (int k = 0; k < np; ++k)
+                    for (int c = 0; c < C; ++c) v[k][c] = IO<TI>::ld(src + k * C + c);
+            }
+        }
+        if (OUT_PL) {
+            for (int c = 0; c < C; ++c) {
+                TO *dst = out + fb + c * hw + p0;
+                if (vec && np == 4) {
+                    const float t[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
+                    Vec4<TO>::st(dst, t);
+                } else {
+                    for (int k = 0; k < np; ++k) IO<TO>::st(dst + k, v[k][c]);
+                }
+            }
+        } else {
+            TO *dst = out + fb + p0 * C;
+            if (vec && np == 4) {
+                float t[16];
+                for (int k = 0; k < 4; ++k)
+                    for (int c = 0; c < C; ++c) t[k * C + c] = v[k][c];
+                for (int j = 0; j < C; ++j) Vec4<TO>::st(dst + 4 * j, t + 4 * j);
+            } else {
+                for (int k = 0; k < np; ++k)
+                    for (int c = 0; c < C; ++c) IO<TO>::st(dst + k * C + c, v[k][c]);
+            }
         }
     }
 }
@@ -588,8 +661,11 @@ __global__ void relayout_kernel(const TI *__restrict__ in, TO *__restrict__ out,
 int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_pl, int B, int H, int W,
              int C, cudaStream_t s) {
     const long long hw = (long long)H * W;
-    const unsigned grid = (unsigned)std::min<long long>((B * hw + 255) / 256, 148 * 32);
-#define SKC_RL(TI, TO, IP, OP) relayout_kernel<TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, C)
+    const unsigned grid = (unsigned)std::min<long long>((B * ((hw + 3) / 4) + 255) / 256, 148 * 16);
+    // 16-byte (fp32) / 8-byte (fp16) vector accesses need hw % 4 == 0 and aligned bases
+    const size_t ia = idt == SKC_F32 ? 16 : 8, oa = odt == SKC_F32 ? 16 : 8;
+    const int vec = (hw % 4 == 0) && ((uintptr_t)in % ia == 0) && ((uintptr_t)out % oa == 0);
+#define SKC_RL(TI, TO, IP, OP) relayout_kernel<TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, C, vec)
     if (!in_pl && out_pl) {
         if (idt == SKC_F32) SKC_RL(float, float, false, true); else SKC_RL(__half, float, false, true);
     } else if (in_pl && !out_pl) {
@@ -604,13 +680,19 @@ int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_p
 
 // Chain I/O policy: 0 = the first layer reads HWC and the last writes HWC
 // directly; 1 = planar everywhere with relayout passes at both ends; 2 = only
-// the output side goes through a relayout pass (default).
-static int chain_policy() {
+// the output side goes through a relayout pass.  Default (-1): relayout the
+// input too when it is fp16 (the per-channel fp16 gather is the slow case).
+static int chain_policy_env() {
     static const int v = [] {
         const char *e = std::getenv("SKC_CHAIN_IO");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : -1;
     }();
     return v;
+}
+static int chain_policy(int in_dtype) {
+    const int v = chain_policy_env();
+    if (v >= 0) return v;
+    return in_dtype == SKC_F16 ? 1 : 2;
 }
 
 // HWC output layer with the long-layer fp16 fallback (fp32 temporary + convert).
@@ -692,7 +774,7 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     cudaStream_t s = (cudaStream_t)stream;
     if (L == 1) return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, layout[0], boundary, s);
     // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
-    const int pol = chain_policy();
+    const int pol = chain_policy(in_dtype);
     const bool pre = pol == 1, post = pol == 1 || pol == 2;
     const size_t n = (size_t)B * H * W * C;
     void *buf[2] = {nullptr, nullptr};
