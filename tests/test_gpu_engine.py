@@ -231,3 +231,28 @@ def test_dense_and_tap_paths_agree(skc, orc):
             taps_out = np.load(f"{td}/out{k}.npy")
             dense_out = skc.apply_sparse_layer(img, skc.SparseLayer(off, w))
             assert normwise(dense_out, taps_out) < 2e-6
+
+
+def test_chain_io_policies_agree(skc):
+    """SKC_CHAIN_IO 0/1/2 (direct HWC I/O vs relayout passes) give identical chains."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from paper_2512_04556_b200 import synth
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "img = np.load(sys.argv[1]); cpx = synth.c0_complex() if img.dtype == np.float32 else synth.kawase_complex();"
+            "np.save(sys.argv[2], skc.apply_complex(img, cpx, boundary='clamp'))")
+    root = str(__import__("pathlib").Path(__file__).parent.parent)
+    rng = np.random.default_rng(5)
+    with tempfile.TemporaryDirectory() as td:
+        for img in (rng.random((97, 130, 3)).astype(np.float32), rng.random((61, 77, 4)).astype(np.float16)):
+            np.save(f"{td}/in.npy", img)
+            outs = []
+            for pol in ("0", "1", "2"):
+                env = dict(os.environ, SKC_CHAIN_IO=pol)
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/o{pol}.npy"], check=True,
+                               env=env, cwd=root)
+                outs.append(np.load(f"{td}/o{pol}.npy"))
+            assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
