@@ -598,9 +598,9 @@ template <> struct Vec4<__half> {
     }
 };
 
-template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
+template <int C, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(256) relayout_kernel(const TI *__restrict__ in, TO *__restrict__ out, int B,
-                                                       long long hw, int C, int vec) {
+                                                       long long hw, int vec) {
     const long long nq = (long long)B * ((hw + 3) / 4);
     const long long qpf = (hw + 3) / 4;
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
@@ -611,48 +611,48 @@ __global__ void __launch_bounds__(256) relayout_kernel(const TI *__restrict__ in
         float v[4][4];
         // gather 4 pixels x C channels
         if (IN_PL) {
-            for (int c = 0; c < C; ++c) {
+            _Pragma("unroll") for (int c = 0; c < C; ++c) {
                 const TI *src = in + fb + c * hw + p0;
                 if (vec && np == 4) {
                     float t[4];
                     Vec4<TI>::ld(src, t);
-                    for (int k = 0; k < 4; ++k) v[k][c] = t[k];
+                    _Pragma("unroll") for (int k = 0; k < 4; ++k) v[k][c] = t[k];
                 } else {
-                    for (int k = 0; k < np; ++k) v[k][c] = IO<TI>::ld(src + k);
+                    _Pragma("unroll") for (int k = 0; k < 4; ++k) if (k < np) v[k][c] = IO<TI>::ld(src + k);
                 }
             }
         } else {
             const TI *src = in + fb + p0 * C;
             if (vec && np == 4) {
-                float t[16];
-                for (int j = 0; j < C; ++j) Vec4<TI>::ld(src + 4 * j, t + 4 * j);
-                for (int k = 0; k < 4; ++k)
-                    for (int c = 0; c < C; ++c) v[k][c] = t[k * C + c];
+                float t[4 * C];
+                _Pragma("unroll") for (int j = 0; j < C; ++j) Vec4<TI>::ld(src + 4 * j, t + 4 * j);
+                _Pragma("unroll") for (int k = 0; k < 4; ++k)
+                    _Pragma("unroll") for (int c = 0; c < C; ++c) v[k][c] = t[k * C + c];
             } else {
-                for (int k = 0; k < np; ++k)
-                    for (int c = 0; c < C; ++c) v[k][c] = IO<TI>::ld(src + k * C + c);
+                _Pragma("unroll") for (int k = 0; k < 4; ++k) if (k < np)
+                    _Pragma("unroll") for (int c = 0; c < C; ++c) v[k][c] = IO<TI>::ld(src + k * C + c);
             }
         }
         if (OUT_PL) {
-            for (int c = 0; c < C; ++c) {
+            _Pragma("unroll") for (int c = 0; c < C; ++c) {
                 TO *dst = out + fb + c * hw + p0;
                 if (vec && np == 4) {
                     const float t[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
                     Vec4<TO>::st(dst, t);
                 } else {
-                    for (int k = 0; k < np; ++k) IO<TO>::st(dst + k, v[k][c]);
+                    _Pragma("unroll") for (int k = 0; k < 4; ++k) if (k < np) IO<TO>::st(dst + k, v[k][c]);
                 }
             }
         } else {
             TO *dst = out + fb + p0 * C;
             if (vec && np == 4) {
-                float t[16];
-                for (int k = 0; k < 4; ++k)
-                    for (int c = 0; c < C; ++c) t[k * C + c] = v[k][c];
-                for (int j = 0; j < C; ++j) Vec4<TO>::st(dst + 4 * j, t + 4 * j);
+                float t[4 * C];
+                _Pragma("unroll") for (int k = 0; k < 4; ++k)
+                    _Pragma("unroll") for (int c = 0; c < C; ++c) t[k * C + c] = v[k][c];
+                _Pragma("unroll") for (int j = 0; j < C; ++j) Vec4<TO>::st(dst + 4 * j, t + 4 * j);
             } else {
-                for (int k = 0; k < np; ++k)
-                    for (int c = 0; c < C; ++c) IO<TO>::st(dst + k * C + c, v[k][c]);
+                _Pragma("unroll") for (int k = 0; k < 4; ++k) if (k < np)
+                    _Pragma("unroll") for (int c = 0; c < C; ++c) IO<TO>::st(dst + k * C + c, v[k][c]);
             }
         }
     }
@@ -665,11 +665,17 @@ int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_p
     // 16-byte (fp32) / 8-byte (fp16) vector accesses need hw % 4 == 0 and aligned bases
     const size_t ia = idt == SKC_F32 ? 16 : 8, oa = odt == SKC_F32 ? 16 : 8;
     const int vec = (hw % 4 == 0) && ((uintptr_t)in % ia == 0) && ((uintptr_t)out % oa == 0);
-#define SKC_RL(TI, TO, IP, OP) relayout_kernel<TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, C, vec)
+#define SKC_RL(TI, TO, IP, OP)                                                                          \
+    switch (C) {                                                                                        \
+        case 1: relayout_kernel<1, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
+        case 2: relayout_kernel<2, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
+        case 3: relayout_kernel<3, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
+        default: relayout_kernel<4, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
+    }
     if (!in_pl && out_pl) {
-        if (idt == SKC_F32) SKC_RL(float, float, false, true); else SKC_RL(__half, float, false, true);
+        if (idt == SKC_F32) { SKC_RL(float, float, false, true); } else { SKC_RL(__half, float, false, true); }
     } else if (in_pl && !out_pl) {
-        if (odt == SKC_F32) SKC_RL(float, float, true, false); else SKC_RL(float, __half, true, false);
+        if (odt == SKC_F32) { SKC_RL(float, float, true, false); } else { SKC_RL(float, __half, true, false); }
     } else {
         return fail(SKC_EBADARG, "relayout converts between HWC and planar fp32");
     }
