@@ -33,13 +33,24 @@ constexpr int kFitThreads = 512;
 constexpr int kFitWarps = kFitThreads / 32;
 constexpr int kFitMaxL = 8;
 constexpr int kFitMaxP = 256;     // total taps per complex
-constexpr int kFitChunk = 64;     // taps per reduction chunk
 constexpr int kNeedGrow = 100;    // internal status: scratch canvas too small
+constexpr int kFitSmem = 200 * 1024;   // dynamic shared memory per CTA (state + arena)
+constexpr int kFKR = 4, kFMC = 4;      // register block of the pixel passes
+constexpr int kMaxTapsPerWarp = 4;     // correlation taps a warp carries at once
 
 enum FitMode { MODE_FIT = 0, MODE_BACKWARD = 1, MODE_IR = 2 };
 
+// Live box of an intermediate in canvas coordinates; empty when w or h <= 0.
 struct Box {
-    int x0, x1, y0, y1;  // inclusive bounds; empty when x1 < x0 or y1 < y0
+    int x0, y0, w, h;
+};
+
+// A box plus its compact row-major data (row stride = w).  `p` is a generic
+// pointer into the shared-memory arena or, when the arena is full, into the
+// CTA's global scratch slot -- the passes do not care which.
+struct Buf {
+    float *p;
+    int x0, y0, w, h;
 };
 
 struct FitParams {
@@ -47,13 +58,13 @@ struct FitParams {
     int layout[kFitMaxL];
     int start[kFitMaxL + 1];
     skc_fit_cfg cfg;
-    int cap;            // scratch canvas capacity
+    int cap;            // scratch canvas capacity (global slots are cap*cap floats)
     int canvas_fixed;   // MODE_BACKWARD / MODE_IR canvas
     float *state;       // MODE_FIT
     const float *tgts;  // (B, M, M)
     float *trace;       // (B, steps+1)
     int *status;        // (B, 4)
-    float *scratch;     // (B, L+2, cap, cap)
+    float *scratch;     // (B, L+1, cap, cap) global overflow slots
     const float *taps_in;  // MODE_BACKWARD / MODE_IR: (B, L, nmax, 3)
     float *loss_out;       // MODE_BACKWARD
     float *grads_out;      // MODE_BACKWARD: (B, L, nmax, 3)
@@ -68,21 +79,17 @@ struct FitSmem {
     float2 frac[kFitMaxP];  // fx, fy
     int2 ixy[kFitMaxP];     // floor(ox), floor(oy)
     float3 grad[kFitMaxP];  // d_ox, d_oy, d_w
-    double part[kFitWarps][3][kFitChunk];
     double red[kFitWarps];
     Box box[kFitMaxL + 1];
+    int4 dr[kFitMaxL];      // per layer corner range: dxmin, dxmax, dymin, dymax
+    float *bufp[kFitMaxL + 1];
+    float one;
     int canvas;
     int flag;
     int bad_layer, bad_sample;
 };
 
-__device__ __forceinline__ bool inbox(const Box &b, int y, int x) {
-    return y >= b.y0 && y <= b.y1 && x >= b.x0 && x <= b.x1;
-}
-
-__device__ __forceinline__ float rd(const float *buf, int cap, const Box &b, int y, int x) {
-    return inbox(b, y, x) ? buf[y * cap + x] : 0.f;
-}
+constexpr int kArenaFloats = (kFitSmem - (int)((sizeof(FitSmem) + 15) / 16 * 16)) / 4;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -90,7 +97,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Deterministic block sum of one double (result valid in thread 0 and returned to all).
+// Deterministic block sum of one double (result returned to all threads).
 __device__ double block_sum(FitSmem &S, double v) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     v = warp_sum(v);
@@ -114,8 +121,14 @@ __device__ __forceinline__ float loss_grad(float d, int kind, float eps) {
     return 2.f * d;
 }
 
-__device__ __forceinline__ float *sbuf(const FitParams &p, int b, int k) {
-    return p.scratch + ((size_t)b * (p.L + 2) + k) * (size_t)p.cap * p.cap;
+__device__ __forceinline__ float ld_chk(const Buf &b, int y, int x) {
+    const unsigned dy = (unsigned)(y - b.y0), dx = (unsigned)(x - b.x0);
+    return (dy < (unsigned)b.h && dx < (unsigned)b.w) ? b.p[dy * b.w + dx] : 0.f;
+}
+
+__device__ __forceinline__ Buf buf_of(const FitSmem &S, int l) {
+    const Box &bx = S.box[l];
+    return Buf{S.bufp[l], bx.x0, bx.y0, bx.w, bx.h};
 }
 
 // Effective weights (optim.py:164-165; softmax 159-161) -- one thread per layer.
@@ -140,8 +153,10 @@ __device__ void effective_weights(const FitParams &p, FitSmem &S) {
     __syncthreads();
 }
 
-// Tap tables (sample_shifted, engine.py:118-130) and live boxes.
-__device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S) {
+// Tap tables (sample_shifted, engine.py:118-130), live boxes and the buffer
+// arena: the IR's box first, then intermediates from the last layer down, go
+// to shared memory while they fit, the rest to the CTA's global slots.
+__device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S, float *arena, float *gslots) {
     for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
         const float ox = S.off[q].x, oy = S.off[q].y, w = S.w[q];
         const float fx0 = floorf(ox), fy0 = floorf(oy);
@@ -154,7 +169,9 @@ __device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const int c = S.canvas / 2, last = S.canvas - 1;
-        S.box[0] = Box{c, c, c, c};
+        S.box[0] = Box{c, c, 1, 1};
+        S.one = 1.f;
+        S.bufp[0] = &S.one;
         for (int l = 0; l < p.L; ++l) {
             int dxmin = 1 << 30, dxmax = -(1 << 30), dymin = 1 << 30, dymax = -(1 << 30);
             for (int i = 0; i < p.layout[l]; ++i) {
@@ -164,57 +181,131 @@ __device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S) {
                 dymin = min(dymin, d.y);
                 dymax = max(dymax, d.y + 1);
             }
-            const Box &a = S.box[l];
-            Box nb;
-            // I_{l+1}[y] = sum cw I_l[y + d]  =>  support of I_{l+1} = support(I_l) - d
-            nb.x0 = max(0, a.x0 - dxmax);
-            nb.x1 = min(last, a.x1 - dxmin);
-            nb.y0 = max(0, a.y0 - dymax);
-            nb.y1 = min(last, a.y1 - dymin);
-            if (a.x1 < a.x0 || a.y1 < a.y0) nb = Box{0, -1, 0, -1};
+            S.dr[l] = make_int4(dxmin, dxmax, dymin, dymax);
+            const Box a = S.box[l];
+            Box nb{0, 0, 0, 0};
+            if (a.w > 0 && a.h > 0) {
+                // I_{l+1}[y] = sum cw I_l[y + d]  =>  support(I_{l+1}) = support(I_l) - d
+                const int x0 = max(0, a.x0 - dxmax), x1 = min(last, a.x0 + a.w - 1 - dxmin);
+                const int y0 = max(0, a.y0 - dymax), y1 = min(last, a.y0 + a.h - 1 - dymin);
+                nb = Box{x0, y0, x1 - x0 + 1, y1 - y0 + 1};
+            }
             S.box[l + 1] = nb;
+        }
+        int used = 0;
+        for (int l = p.L; l >= 1; --l) {
+            const Box &bx = S.box[l];
+            const int n = (max(bx.w, 0) * max(bx.h, 0) + 3) & ~3;
+            if (used + n <= kArenaFloats) {
+                S.bufp[l] = arena + used;
+                used += n;
+            } else {
+                S.bufp[l] = gslots + (size_t)(l - 1) * p.cap * p.cap;
+            }
         }
     }
     __syncthreads();
 }
 
+// out(y, x) += sum over taps of the 4 corner products, for one KR x MC block.
+// `rd(y, x)` returns the source value at canvas (y, x) (checked or not); the
+// window of tap i starts at source (y0 + sy(i), x0 + sx(i)).
+template <bool ADJ, bool CHECK>
+__device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSmem &S, const Buf &src,
+                                           int s0, int n, int y0, int x0) {
+    for (int i = 0; i < n; ++i) {
+        const int2 d = S.ixy[s0 + i];
+        const float4 w = S.cw[s0 + i];
+        // forward: out(y,x) reads src(y + d + corner); adjoint: src(y - d - corner)
+        const int wy = ADJ ? y0 - d.y - 1 : y0 + d.y;
+        const int wx = ADJ ? x0 - d.x - 1 : x0 + d.x;
+        float win[kFKR + 1][kFMC + 1];
+        if (CHECK) {
+#pragma unroll
+            for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c <= kFMC; ++c) win[r][c] = ld_chk(src, wy + r, wx + c);
+        } else {
+            const float *q = src.p + (wy - src.y0) * src.w + (wx - src.x0);
+#pragma unroll
+            for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * src.w + c];
+        }
+#pragma unroll
+        for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+            for (int c = 0; c < kFMC; ++c) {
+                float v = acc[r][c];
+                if (!ADJ) {
+                    v = fmaf(w.x, win[r][c], v);
+                    v = fmaf(w.y, win[r][c + 1], v);
+                    v = fmaf(w.z, win[r + 1][c], v);
+                    v = fmaf(w.w, win[r + 1][c + 1], v);
+                } else {
+                    v = fmaf(w.x, win[r + 1][c + 1], v);
+                    v = fmaf(w.y, win[r + 1][c], v);
+                    v = fmaf(w.z, win[r][c + 1], v);
+                    v = fmaf(w.w, win[r][c], v);
+                }
+                acc[r][c] = v;
+            }
+    }
+}
+
+// One gather pass over dst's box: forward layer l (ADJ=false, dst = I_{l+1})
+// or the adjoint of layer l (ADJ=true, src = g_{l+1}, dst = g_l).  Returns the
+// block-wide "non-finite seen" flag.
+template <bool ADJ>
+__device__ int gather_pass(const FitParams &p, FitSmem &S, int l, const Buf src, const Buf dst) {
+    const int s0 = p.start[l], n = p.layout[l];
+    const int4 dr = S.dr[l];
+    // rows/cols of src a block's window can touch, relative to its origin
+    const int ry0 = ADJ ? -dr.w : dr.z, ry1 = ADJ ? kFKR - 1 - dr.z : kFKR - 1 + dr.w;
+    const int rx0 = ADJ ? -dr.y : dr.x, rx1 = ADJ ? kFMC - 1 - dr.x : kFMC - 1 + dr.y;
+    const int nbx = (dst.w + kFMC - 1) / kFMC, nby = (dst.h + kFKR - 1) / kFKR;
+    int bad = 0;
+    for (int blk = threadIdx.x; blk < nbx * nby; blk += blockDim.x) {
+        const int by = blk / nbx, bx = blk - by * nbx;
+        const int y0 = dst.y0 + by * kFKR, x0 = dst.x0 + bx * kFMC;
+        float acc[kFKR][kFMC];
+#pragma unroll
+        for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+            for (int c = 0; c < kFMC; ++c) acc[r][c] = 0.f;
+        const bool inside = y0 + ry0 >= src.y0 && y0 + ry1 < src.y0 + src.h && x0 + rx0 >= src.x0 &&
+                            x0 + rx1 < src.x0 + src.w;
+        if (inside)
+            block_taps<ADJ, false>(acc, S, src, s0, n, y0, x0);
+        else
+            block_taps<ADJ, true>(acc, S, src, s0, n, y0, x0);
+#pragma unroll
+        for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+            for (int c = 0; c < kFMC; ++c) {
+                const int y = y0 + r, x = x0 + c;
+                if (y < dst.y0 + dst.h && x < dst.x0 + dst.w) {
+                    dst.p[(y - dst.y0) * dst.w + (x - dst.x0)] = acc[r][c];
+                    bad |= !isfinite(acc[r][c]);
+                }
+            }
+    }
+    return __syncthreads_or(bad);
+}
+
 // Forward chain on the live boxes (_forward_ir, optim.py:204-222).  Returns
 // false (and fills bad_layer/bad_sample) on a non-finite intermediate.
-__device__ bool forward(const FitParams &p, FitSmem &S, int b) {
-    const int cap = p.cap;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    float *b0 = sbuf(p, b, 0);
-    const int c = S.canvas / 2;
-    if (threadIdx.x == 0) b0[c * cap + c] = 1.f;
-    __syncthreads();
+__device__ bool forward(const FitParams &p, FitSmem &S) {
     for (int l = 0; l < p.L; ++l) {
-        const float *src = sbuf(p, b, l);
-        float *dst = sbuf(p, b, l + 1);
-        const Box a = S.box[l], o = S.box[l + 1];
-        const int s0 = p.start[l], n = p.layout[l];
+        const Box o = S.box[l + 1];
         int bad = 0;
-        for (int y = o.y0 + ty; y <= o.y1; y += kFitWarps) {
-            for (int x = o.x0 + tx; x <= o.x1; x += 32) {
-                float acc = 0.f;
-                for (int i = 0; i < n; ++i) {
-                    const int2 d = S.ixy[s0 + i];
-                    const float4 w = S.cw[s0 + i];
-                    const int yy = y + d.y, xx = x + d.x;
-                    acc = fmaf(w.x, rd(src, cap, a, yy, xx), acc);
-                    acc = fmaf(w.y, rd(src, cap, a, yy, xx + 1), acc);
-                    acc = fmaf(w.z, rd(src, cap, a, yy + 1, xx), acc);
-                    acc = fmaf(w.w, rd(src, cap, a, yy + 1, xx + 1), acc);
-                }
-                dst[y * cap + x] = acc;
-                bad |= !isfinite(acc);
-            }
-        }
-        if (__syncthreads_or(bad)) {
+        if (o.w > 0 && o.h > 0) bad = gather_pass<false>(p, S, l, buf_of(S, l), buf_of(S, l + 1));
+        if (bad) {
             if (threadIdx.x == 0) {
                 S.bad_layer = l;
                 S.bad_sample = -1;
-                for (int i = 0; i < n; ++i) {
-                    const int q = s0 + i;
+                for (int i = 0; i < p.layout[l]; ++i) {
+                    const int q = p.start[l] + i;
                     if (!(isfinite(S.off[q].x) && isfinite(S.off[q].y) && isfinite(S.w[q]))) {
                         S.bad_sample = i;
                         break;
@@ -235,103 +326,130 @@ __device__ __forceinline__ float tgt_at(const FitParams &p, int b, int canvas, i
     return __ldg(p.tgts + ((size_t)b * p.M + ty) * p.M + tx);
 }
 
-// Loss over the whole canvas (the IR is zero outside its live box); the
-// loss gradient is stored over the live box of the IR only -- the reverse
-// sweep never reads it elsewhere.
+// Loss over the whole canvas (the IR is zero outside its live box); the loss
+// gradient overwrites the IR on its box -- the reverse sweep reads it nowhere else.
 __device__ double loss_and_grad(const FitParams &p, FitSmem &S, int b) {
-    const int cap = p.cap, canvas = S.canvas;
-    float *ir = sbuf(p, b, p.L);
-    const Box o = S.box[p.L];
+    const int canvas = S.canvas;
+    const Buf g = buf_of(S, p.L);
     double part = 0.0;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int y = ty; y < canvas; y += kFitWarps) {
         for (int x = tx; x < canvas; x += 32) {
-            const bool in = inbox(o, y, x);
-            const float v = in ? ir[y * cap + x] : 0.f;
+            const unsigned dy = (unsigned)(y - g.y0), dx = (unsigned)(x - g.x0);
+            const bool in = dy < (unsigned)g.h && dx < (unsigned)g.w;
+            const float v = in ? g.p[dy * g.w + dx] : 0.f;
             const float d = v - tgt_at(p, b, canvas, y, x);
             part += (double)loss_term(d, p.cfg.loss_kind, p.cfg.loss_eps);
-            if (in) ir[y * cap + x] = loss_grad(d, p.cfg.loss_kind, p.cfg.loss_eps);
+            if (in) g.p[dy * g.w + dx] = loss_grad(d, p.cfg.loss_kind, p.cfg.loss_eps);
         }
     }
     return block_sum(S, part);
 }
 
-// Reverse sweep (_backward_pass, optim.py:231-263).  Writes S.grad.
-__device__ void backward_sweep(const FitParams &p, FitSmem &S, int b) {
-    const int cap = p.cap;
+// Per-tap gradients of layer l (_backward_pass, optim.py:231-263) from the
+// four corner correlations C_c = <g_{l+1}, I_l shifted by corner c>:
+//   d_w = sum_c a_c C_c, d_ox = w[(1-fy)(C10-C00) + fy(C11-C01)],
+//   d_oy = w[(1-fx)(C01-C00) + fx(C11-C10)].
+// Each warp owns up to kMaxTapsPerWarp taps and sweeps the whole box of
+// g_{l+1}; per-block sums are fp32, accumulated across blocks in float64 and
+// reduced by a fixed shuffle tree (deterministic, no atomics).
+__device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, const Buf g) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tx = lane, ty = warp;
-    int gcur = p.L;          // buffer holding g_{l+1}
-    for (int l = p.L - 1; l >= 0; --l) {
-        const float *I = sbuf(p, b, l);
-        const float *g = sbuf(p, b, gcur);
-        const Box bi = S.box[l], bg = S.box[l + 1];
-        const int s0 = p.start[l], n = p.layout[l];
-        for (int c0 = 0; c0 < n; c0 += kFitChunk) {
-            const int c1 = min(n, c0 + kFitChunk);
-            for (int i = c0; i < c1; ++i) {
-                const int2 d = S.ixy[s0 + i];
-                const float fx = S.frac[s0 + i].x, fy = S.frac[s0 + i].y;
-                const float a00 = (1.f - fx) * (1.f - fy), a10 = fx * (1.f - fy);
-                const float a01 = (1.f - fx) * fy, a11 = fx * fy;
-                double sw = 0.0, sx = 0.0, sy = 0.0;
-                for (int y = bg.y0 + ty; y <= bg.y1; y += kFitWarps) {
-                    for (int x = bg.x0 + tx; x <= bg.x1; x += 32) {
-                        const float gv = g[y * cap + x];
-                        const int yy = y + d.y, xx = x + d.x;
-                        const float s00 = rd(I, cap, bi, yy, xx), s10 = rd(I, cap, bi, yy, xx + 1);
-                        const float s01 = rd(I, cap, bi, yy + 1, xx), s11 = rd(I, cap, bi, yy + 1, xx + 1);
-                        const float smp = a00 * s00 + a10 * s10 + a01 * s01 + a11 * s11;
-                        const float ddx = (1.f - fy) * (s10 - s00) + fy * (s11 - s01);
-                        const float ddy = (1.f - fx) * (s01 - s00) + fx * (s11 - s10);
-                        sw += (double)(gv * smp);
-                        sx += (double)(gv * ddx);
-                        sy += (double)(gv * ddy);
+    const int s0 = p.start[l], n = p.layout[l];
+    const int nbx = (g.w + kFMC - 1) / kFMC, nby = (g.h + kFKR - 1) / kFKR;
+    const int4 dr = S.dr[l];
+    for (int t0 = warp * kMaxTapsPerWarp; t0 < n; t0 += kFitWarps * kMaxTapsPerWarp) {
+        const int nt = min(kMaxTapsPerWarp, n - t0);
+        double C[kMaxTapsPerWarp][4];
+#pragma unroll
+        for (int k = 0; k < kMaxTapsPerWarp; ++k)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) C[k][c] = 0.0;
+        for (int blk = lane; blk < nbx * nby; blk += 32) {
+            const int by = blk / nbx, bx = blk - by * nbx;
+            const int y0 = g.y0 + by * kFKR, x0 = g.x0 + bx * kFMC;
+            float gv[kFKR][kFMC];
+#pragma unroll
+            for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c < kFMC; ++c) {
+                    const int y = y0 + r, x = x0 + c;
+                    gv[r][c] = (y < g.y0 + g.h && x < g.x0 + g.w) ? g.p[(y - g.y0) * g.w + (x - g.x0)] : 0.f;
+                }
+            const bool inside = y0 + dr.z >= I.y0 && y0 + kFKR - 1 + dr.w < I.y0 + I.h &&
+                                x0 + dr.x >= I.x0 && x0 + kFMC - 1 + dr.y < I.x0 + I.w;
+#pragma unroll
+            for (int k = 0; k < kMaxTapsPerWarp; ++k) {
+                if (k >= nt) break;
+                const int2 d = S.ixy[s0 + t0 + k];
+                float win[kFKR + 1][kFMC + 1];
+                if (inside) {
+                    const float *q = I.p + (y0 + d.y - I.y0) * I.w + (x0 + d.x - I.x0);
+#pragma unroll
+                    for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                        for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * I.w + c];
+                } else {
+#pragma unroll
+                    for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                        for (int c = 0; c <= kFMC; ++c) win[r][c] = ld_chk(I, y0 + d.y + r, x0 + d.x + c);
+                }
+                float c00 = 0.f, c10 = 0.f, c01 = 0.f, c11 = 0.f;
+#pragma unroll
+                for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+                    for (int c = 0; c < kFMC; ++c) {
+                        const float v = gv[r][c];
+                        c00 = fmaf(v, win[r][c], c00);
+                        c10 = fmaf(v, win[r][c + 1], c10);
+                        c01 = fmaf(v, win[r + 1][c], c01);
+                        c11 = fmaf(v, win[r + 1][c + 1], c11);
                     }
-                }
-                sw = warp_sum(sw);
-                sx = warp_sum(sx);
-                sy = warp_sum(sy);
-                if (lane == 0) {
-                    S.part[warp][0][i - c0] = sw;
-                    S.part[warp][1][i - c0] = sx;
-                    S.part[warp][2][i - c0] = sy;
-                }
+                C[k][0] += c00;
+                C[k][1] += c10;
+                C[k][2] += c01;
+                C[k][3] += c11;
             }
-            __syncthreads();
-            for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-                double tw = 0.0, txx = 0.0, tyy = 0.0;
-                for (int k = 0; k < kFitWarps; ++k) {
-                    tw += S.part[k][0][i - c0];
-                    txx += S.part[k][1][i - c0];
-                    tyy += S.part[k][2][i - c0];
-                }
-                const float w = S.w[s0 + i];
-                S.grad[s0 + i] = make_float3((float)(w * txx), (float)(w * tyy), (float)tw);
-            }
-            __syncthreads();
         }
-        if (l > 0) {
-            // adjoint: g_l[q] = sum_i w_i bilinear(g_{l+1}, q - o_i) on the box of I_l
-            const int gnext = (gcur == p.L) ? p.L + 1 : p.L;
-            float *gn = sbuf(p, b, gnext);
-            for (int y = bi.y0 + ty; y <= bi.y1; y += kFitWarps) {
-                for (int x = bi.x0 + tx; x <= bi.x1; x += 32) {
-                    float acc = 0.f;
-                    for (int i = 0; i < n; ++i) {
-                        const int2 d = S.ixy[s0 + i];
-                        const float4 w = S.cw[s0 + i];
-                        const int yy = y - d.y, xx = x - d.x;
-                        acc = fmaf(w.x, rd(g, cap, bg, yy, xx), acc);
-                        acc = fmaf(w.y, rd(g, cap, bg, yy, xx - 1), acc);
-                        acc = fmaf(w.z, rd(g, cap, bg, yy - 1, xx), acc);
-                        acc = fmaf(w.w, rd(g, cap, bg, yy - 1, xx - 1), acc);
-                    }
-                    gn[y * cap + x] = acc;
-                }
+#pragma unroll
+        for (int k = 0; k < kMaxTapsPerWarp; ++k) {
+            if (k >= nt) break;
+            double c4[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) c4[c] = warp_sum(C[k][c]);
+            if (lane == 0) {
+                const int q = s0 + t0 + k;
+                const double fx = S.frac[q].x, fy = S.frac[q].y, w = S.w[q];
+                const double dw = (1 - fx) * (1 - fy) * c4[0] + fx * (1 - fy) * c4[1] + (1 - fx) * fy * c4[2] +
+                                  fx * fy * c4[3];
+                const double dx = w * ((1 - fy) * (c4[1] - c4[0]) + fy * (c4[3] - c4[2]));
+                const double dy = w * ((1 - fx) * (c4[2] - c4[0]) + fx * (c4[3] - c4[1]));
+                S.grad[q] = make_float3((float)dx, (float)dy, (float)dw);
             }
-            __syncthreads();
-            gcur = gnext;
+        }
+    }
+}
+
+// Reverse sweep: gradients of layer l, then (l > 0) the adjoint into I_l's
+// buffer, which corr(l) no longer needs.
+__device__ void backward_sweep(const FitParams &p, FitSmem &S) {
+    for (int l = p.L - 1; l >= 0; --l) {
+        const Buf I = buf_of(S, l), g = buf_of(S, l + 1);
+        if (g.w > 0 && g.h > 0) {
+            correlate(p, S, l, I, g);
+        } else {
+            for (int q = p.start[l] + threadIdx.x; q < p.start[l + 1]; q += blockDim.x)
+                S.grad[q] = make_float3(0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        if (l > 0 && I.w > 0 && I.h > 0) {
+            if (g.w > 0 && g.h > 0) {
+                gather_pass<true>(p, S, l, g, I);
+            } else {
+                for (int e = threadIdx.x; e < I.w * I.h; e += blockDim.x) I.p[e] = 0.f;
+                __syncthreads();
+            }
         }
     }
 }
@@ -390,9 +508,11 @@ __device__ __forceinline__ int &hdr_i(float *st, int k) { return reinterpret_cas
 __global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant__ FitParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
+    float *arena = reinterpret_cast<float *>(smem_raw + (sizeof(FitSmem) + 15) / 16 * 16);
     const int b = blockIdx.x;
     const int blk = p.L * p.nmax * 3;
     int *status = p.status + 4 * b;
+    float *gslots = p.scratch + (size_t)b * p.L * p.cap * p.cap;
 
     if (p.mode != MODE_FIT) {
         // backward()/synthesize_ir(): parameters come in as effective weights
@@ -405,8 +525,8 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant_
         }
         if (threadIdx.x == 0) S.canvas = p.canvas_fixed;
         __syncthreads();
-        build_taps_and_boxes(p, S);
-        const bool ok = forward(p, S, b);
+        build_taps_and_boxes(p, S, arena, gslots);
+        const bool ok = forward(p, S);
         if (!ok) {
             if (threadIdx.x == 0) {
                 status[0] = SKC_ENONFINITE;
@@ -418,19 +538,18 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant_
         }
         if (p.mode == MODE_IR) {
             const int cv = S.canvas;
-            const Box o = S.box[p.L];
-            const float *ir = sbuf(p, b, p.L);
+            const Buf ir = buf_of(S, p.L);
             float *out = p.ir_out + (size_t)b * cv * cv;
             for (int e = threadIdx.x; e < cv * cv; e += blockDim.x) {
                 const int y = e / cv, x = e - y * cv;
-                out[e] = inbox(o, y, x) ? ir[y * p.cap + x] : 0.f;
+                out[e] = ld_chk(ir, y, x);
             }
             if (threadIdx.x == 0) status[0] = SKC_OK;
             return;
         }
         const double loss = loss_and_grad(p, S, b);
         __syncthreads();
-        backward_sweep(p, S, b);
+        backward_sweep(p, S);
         float *go = p.grads_out + (size_t)b * blk;
         for (int q = threadIdx.x; q < p.P; q += blockDim.x) {
             const int r = param_index(p, q);
@@ -486,8 +605,8 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant_
         }
         __syncthreads();
         if (S.flag) { code = kNeedGrow; break; }
-        build_taps_and_boxes(p, S);
-        if (!forward(p, S, b)) {
+        build_taps_and_boxes(p, S, arena, gslots);
+        if (!forward(p, S)) {
             code = SKC_ENONFINITE;
             err_layer = S.bad_layer;
             err_sample = S.bad_sample;
@@ -508,7 +627,7 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant_
         }
         if (step == p.cfg.steps) { step = p.cfg.steps + 1; break; }
         __syncthreads();
-        backward_sweep(p, S, b);
+        backward_sweep(p, S);
         // _chain_weight_norm (optim.py:266-275)
         if (p.cfg.weight_norm == SKC_WN_SOFM) {
             if (threadIdx.x < p.L) {
@@ -690,7 +809,7 @@ static int fill_params(FitParams &p, int B, const int *layout, int L, int nmax, 
 
 static int set_fit_attrs() {
     static bool attr = false;
-    const int smem = (int)sizeof(FitSmem);
+    const int smem = kFitSmem;
     if (!attr) {
         SKC_CUDA(cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         SKC_CUDA(cudaFuncSetAttribute(fit_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -703,14 +822,14 @@ static int set_fit_attrs() {
 static int fit_launch(const FitParams &p, cudaStream_t s) {
     int rc = set_fit_attrs();
     if (rc) return rc;
-    fit_kernel<<<p.B, kFitThreads, sizeof(FitSmem), s>>>(p);
+    fit_kernel<<<p.B, kFitThreads, kFitSmem, s>>>(p);
     SKC_LAUNCH_CHECK("fit_kernel");
     return SKC_OK;
 }
 
 static int alloc_scratch(FitParams &p, int cap, cudaStream_t s) {
     p.cap = cap;
-    const size_t bytes = (size_t)p.B * (p.L + 2) * cap * cap * sizeof(float);
+    const size_t bytes = (size_t)p.B * p.L * cap * cap * sizeof(float);
     void *ptr = nullptr;
     int rc = pool_alloc(&ptr, bytes, s);
     if (rc) return rc;
