@@ -168,7 +168,13 @@ class Chain:
         if pol < 0:   # the library default (skc_layer.cu chain_policy)
             pol = 1 if self.storage == torch.float16 else 2
         self.policy = pol
-        self.launches_per_step = len(self.taps) + (2 if pol == 1 else 1 if pol == 2 else 0)
+        from paper_2512_04556_b200 import _native as nat
+        self.all_taps = np.ascontiguousarray(self.cpx.taps())
+        lay = np.ascontiguousarray(self.cpx.layout, dtype=np.int32)
+        self.fused = bool(nat.lib().skc_chain_is_fused(nat.dbl(self.all_taps), nat.ints(lay), lay.size,
+                                                        self.h, self.w, self.c,
+                                                        1 if self.storage == torch.float16 else 0))
+        self.launches_per_step = 1 if self.fused else len(self.taps) + (2 if pol == 1 else 1 if pol == 2 else 0)
         self.units_per_step = self.nf * self.h * self.w
         esz = 2 if self.storage == torch.float16 else 4
         # algorithmic HBM bytes per launch: image in + out in their storage dtypes
@@ -190,7 +196,7 @@ class Chain:
                        "frames_per_gpu": self.nf,
                        "l2": "inputs larger than L2, no flush" if npx * esz > 126e6 else "L2 flushed between steps"}
         self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if npx * esz <= 126e6 else None
-        self.kernel = "layer kernels (dense + tap tile)"
+        self.kernel = "fused_chain_kernel" if self.fused else "layer kernels (dense stencil + tap tile)"
 
     def step(self, stream, events=None):
         from paper_2512_04556_b200 import _native as nat
@@ -202,6 +208,18 @@ class Chain:
         # the launch sequence skc_chain_fwd runs (SKC_CHAIN_IO policy: HWC in ->
         # planar fp32 layers -> relayout to HWC out), issued one launch at a
         # time so each can be timed
+        if self.fused:
+            if events is not None:
+                events[0][0].record(stream)
+            lay = np.ascontiguousarray(self.cpx.layout, dtype=np.int32)
+            rc = lib.skc_chain_fwd(nat.ptr(src), sdt, nat.ptr(self.out), dt_store, self.nf, self.h, self.w,
+                                   self.c, nat.dbl(self.all_taps), nat.ints(lay), lay.size,
+                                   0 if self.boundary == "zero" else 1, sp)
+            if rc:
+                raise RuntimeError(nat.last_error())
+            if events is not None:
+                events[0][1].record(stream)
+            return
         pol = self.policy
         seq = []
         if pol == 1:

@@ -87,6 +87,11 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
                      int out_layout, int B, int H, int W, int C,
                      const double *taps, int S, int boundary, void *stream);
 
+/* 1 when skc_chain_fwd runs this complex as one fused launch (small total
+ * reach, <= 16 taps per layer: the config-3 Kawase fast path), else 0. */
+int skc_chain_is_fused(const double *taps, const int *layout, int L, int H, int W, int C,
+                       int out_dtype);
+
 /* Layout/dtype conversion HWC <-> planar fp32 (the chain's bracketing passes). */
 int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
                  int out_layout, int B, int H, int W, int C, void *stream);

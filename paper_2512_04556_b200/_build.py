@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libskc.so"
-SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_fit.cu"]
+SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_fused.cu", "skc_fit.cu"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -779,6 +779,9 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     if (!finite_taps(taps, (int)total)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
     cudaStream_t s = (cudaStream_t)stream;
     if (L == 1) return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, layout[0], boundary, s);
+    rc = fused_chain(in, in_dtype, out, out_dtype, B, H, W, C, taps, layout, L, boundary, s);
+    if (rc != -1) return rc;
+    rc = SKC_OK;
     // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
     const int pol = chain_policy(in_dtype);
     const bool pre = pol == 1, post = pol == 1 || pol == 2;

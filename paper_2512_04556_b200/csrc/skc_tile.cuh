@@ -105,6 +105,11 @@ __device__ __forceinline__ void store_px<float>(float *p, float v, int accumulat
 constexpr int kMaxDense = 9;
 int dense_size_for(int span);  // smallest compiled D >= span, or 0
 
+// Fused small-reach chain (skc_fused.cu); -1 = not eligible.
+int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
+                const double *taps, const int *layout, int L, int boundary, cudaStream_t s,
+                bool dry = false);
+
 // Argument checks shared by the image entry points (skc_layer.cu).
 int check_image_args(const void *in, int idt, const void *out, int odt, int B, int H, int W, int C,
                      int boundary);

@@ -256,3 +256,41 @@ def test_chain_io_policies_agree(skc):
                                env=env, cwd=root)
                 outs.append(np.load(f"{td}/o{pol}.npy"))
             assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+def test_fused_chain_matches_oracle_and_unfused(skc, orc):
+    """Small-reach chains run as one fused launch (skc_chain_is_fused); check it
+    against the oracle on ragged sizes, both boundaries, fp32 and fp16, and
+    bit-for-bit-close against the per-layer path (SKC_FUSED=0)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    kaw = synth.kawase_complex()
+    t = np.ascontiguousarray(kaw.taps())
+    lay = np.ascontiguousarray(kaw.layout, dtype=np.int32)
+    assert nat.lib().skc_chain_is_fused(nat.dbl(t), nat.ints(lay), 6, 2160, 3840, 4, 1) == 1
+    rng = np.random.default_rng(31)
+    layers = [(l.offsets, l.weights) for l in kaw.layers]
+    for shape in [(5, 7, 4), (50, 33, 1), (131, 197, 3), (96, 128, 4)]:
+        img = rng.random(shape).astype(np.float32)
+        for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+            ref = orc.apply_complex(img.astype(np.float64), layers, oid)
+            assert normwise(skc.apply_complex(img, kaw, boundary=mode), ref) < TOL32, (shape, mode)
+            h = img.astype(np.float16)
+            refh = orc.apply_complex(h.astype(np.float64), layers, oid)
+            assert normwise(skc.apply_complex(h, kaw, boundary=mode).astype(np.float64), refh) < TOL16
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "np.save(sys.argv[2], skc.apply_complex(np.load(sys.argv[1]), synth.kawase_complex(), boundary='clamp'))")
+    root = str(__import__("pathlib").Path(__file__).parent.parent)
+    img = rng.random((140, 210, 4)).astype(np.float32)
+    with tempfile.TemporaryDirectory() as td:
+        np.save(f"{td}/in.npy", img)
+        subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/unfused.npy"], check=True,
+                       env=dict(os.environ, SKC_FUSED="0"), cwd=root)
+        unf = np.load(f"{td}/unfused.npy")
+    fused = skc.apply_complex(img, kaw, boundary="clamp")
+    assert normwise(fused, unf) < 1e-6
