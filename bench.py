@@ -331,14 +331,15 @@ class SV:
         self.flush.zero_()
 
     def e2e_setup(self):
-        self.host_in = self.frame.cpu().numpy()
-        self.host_pmap = self.pmap.cpu().numpy()
-        n = self.host_in.nbytes + self.host_pmap.nbytes
-        return n, self.host_in.nbytes
+        self.host_in = self.frame.cpu().pin_memory()
+        self.host_pmap = self.pmap.cpu().pin_memory()
+        self.host_out = torch_mod().empty_like(self.host_in).pin_memory()
+        n = self.host_in.numel() * 4 + self.host_pmap.numel() * 4
+        return n, self.host_in.numel() * 4
 
     def e2e_step(self):
         import paper_2512_04556_b200 as skc
-        skc.sv_filter(self.host_in, self.basis, self.host_pmap)
+        skc.sv_filter(self.host_in, self.basis, self.host_pmap, out=self.host_out)
 
     def cpu_sample(self, threads):
         from oracle import oracle as orc

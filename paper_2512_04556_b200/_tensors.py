@@ -31,6 +31,7 @@ class Image:
     def __init__(self, img, batched: bool = False, device=None):
         t = torch()
         self.kind = "torch" if isinstance(img, t.Tensor) else "numpy"
+        self.cpu_tensor = False
         if self.kind == "numpy":
             arr = np.asarray(img)
             if not np.issubdtype(arr.dtype, np.floating):
@@ -41,8 +42,10 @@ class Image:
             ten = t.from_numpy(np.ascontiguousarray(host)).to(dev, non_blocking=False)
         else:
             ten = img
+            self.cpu_tensor = not ten.is_cuda
             if not ten.is_cuda:
-                ten = ten.to("cuda" if device is None else device)
+                dev = t.device("cuda", t.cuda.current_device()) if device is None else t.device(device)
+                ten = ten.to(dev, non_blocking=ten.is_pinned())
             if ten.dtype not in (t.float32, t.float16):
                 ten = ten.to(t.float32)
             ten = ten.contiguous()
@@ -71,16 +74,22 @@ class Image:
         t = torch()
         return t.empty_like(self.tensor, dtype=self.tensor.dtype if dtype is None else dtype)
 
-    def restore(self, out):
-        """Undo the shape/kind normalisation on a result tensor (B, H, W, C)."""
+    def restore(self, out, dest=None):
+        """Undo the shape/kind normalisation on a result tensor (B, H, W, C).
+
+        `dest` (optional torch tensor, e.g. pinned host memory) receives the
+        result with a stream-ordered copy and is returned."""
         if not self.batched:
             out = out[0]
             if self.orig_ndim == 2:
                 out = out[..., 0]
         elif self.orig_ndim == 3:
             out = out[..., 0]
+        if dest is not None:
+            dest.copy_(out.view(dest.shape), non_blocking=True)
+            return dest
         if self.kind == "torch":
-            return out
+            return out.cpu() if self.cpu_tensor else out
         res = out.cpu().numpy()
         if self.np_dtype == np.float64:
             res = res.astype(np.float64)

@@ -35,12 +35,13 @@ constexpr int kFitMaxL = 8;
 constexpr int kFitMaxP = 256;     // total taps per complex
 constexpr int kNeedGrow = 100;    // internal status: scratch canvas too small
 constexpr int kFitSmem = 200 * 1024;   // dynamic shared memory per CTA (state + arena)
-constexpr int kFKR = 4, kFMC = 4;      // register block of the pixel passes
+constexpr int kFKR = 5, kFMC = 4;      // register block of the pixel passes (KR odd)
 constexpr int kMaxTapsPerWarp = 4;     // correlation taps a warp carries at once
 
 enum FitMode { MODE_FIT = 0, MODE_BACKWARD = 1, MODE_IR = 2 };
 
 // Live box of an intermediate in canvas coordinates; empty when w or h <= 0.
+__host__ __device__ __forceinline__ int odd_stride(int w) { return w | 1; }
 struct Box {
     int x0, y0, w, h;
 };
@@ -51,6 +52,7 @@ struct Box {
 struct Buf {
     float *p;
     int x0, y0, w, h;
+    int s;   // row stride, odd: with KR odd the 32 lanes' 5x4 block origins hit 32 banks
 };
 
 struct FitParams {
@@ -123,12 +125,12 @@ __device__ __forceinline__ float loss_grad(float d, int kind, float eps) {
 
 __device__ __forceinline__ float ld_chk(const Buf &b, int y, int x) {
     const unsigned dy = (unsigned)(y - b.y0), dx = (unsigned)(x - b.x0);
-    return (dy < (unsigned)b.h && dx < (unsigned)b.w) ? b.p[dy * b.w + dx] : 0.f;
+    return (dy < (unsigned)b.h && dx < (unsigned)b.w) ? b.p[dy * b.s + dx] : 0.f;
 }
 
 __device__ __forceinline__ Buf buf_of(const FitSmem &S, int l) {
     const Box &bx = S.box[l];
-    return Buf{S.bufp[l], bx.x0, bx.y0, bx.w, bx.h};
+    return Buf{S.bufp[l], bx.x0, bx.y0, bx.w, bx.h, l == 0 ? 1 : odd_stride(bx.w)};
 }
 
 // Effective weights (optim.py:164-165; softmax 159-161) -- one thread per layer.
@@ -195,7 +197,7 @@ __device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S, float *aren
         int used = 0;
         for (int l = p.L; l >= 1; --l) {
             const Box &bx = S.box[l];
-            const int n = (max(bx.w, 0) * max(bx.h, 0) + 3) & ~3;
+            const int n = (max(bx.w, 0) > 0 ? odd_stride(bx.w) * max(bx.h, 0) : 0) + 3 & ~3;
             if (used + n <= kArenaFloats) {
                 S.bufp[l] = arena + used;
                 used += n;
@@ -226,11 +228,11 @@ __device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSm
 #pragma unroll
                 for (int c = 0; c <= kFMC; ++c) win[r][c] = ld_chk(src, wy + r, wx + c);
         } else {
-            const float *q = src.p + (wy - src.y0) * src.w + (wx - src.x0);
+            const float *q = src.p + (wy - src.y0) * src.s + (wx - src.x0);
 #pragma unroll
             for (int r = 0; r <= kFKR; ++r)
 #pragma unroll
-                for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * src.w + c];
+                for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * src.s + c];
         }
 #pragma unroll
         for (int r = 0; r < kFKR; ++r)
@@ -264,9 +266,12 @@ __device__ int gather_pass(const FitParams &p, FitSmem &S, int l, const Buf src,
     const int ry0 = ADJ ? -dr.w : dr.z, ry1 = ADJ ? kFKR - 1 - dr.z : kFKR - 1 + dr.w;
     const int rx0 = ADJ ? -dr.y : dr.x, rx1 = ADJ ? kFMC - 1 - dr.x : kFMC - 1 + dr.y;
     const int nbx = (dst.w + kFMC - 1) / kFMC, nby = (dst.h + kFKR - 1) / kFKR;
+    const int wtw = (nbx + 7) / 8, wth = (nby + 3) / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int bad = 0;
-    for (int blk = threadIdx.x; blk < nbx * nby; blk += blockDim.x) {
-        const int by = blk / nbx, bx = blk - by * nbx;
+    for (int wt = warp; wt < wtw * wth; wt += kFitWarps) {
+        const int bx = (wt % wtw) * 8 + (lane & 7), by = (wt / wtw) * 4 + (lane >> 3);
+        if (bx >= nbx || by >= nby) continue;
         const int y0 = dst.y0 + by * kFKR, x0 = dst.x0 + bx * kFMC;
         float acc[kFKR][kFMC];
 #pragma unroll
@@ -285,7 +290,7 @@ __device__ int gather_pass(const FitParams &p, FitSmem &S, int l, const Buf src,
             for (int c = 0; c < kFMC; ++c) {
                 const int y = y0 + r, x = x0 + c;
                 if (y < dst.y0 + dst.h && x < dst.x0 + dst.w) {
-                    dst.p[(y - dst.y0) * dst.w + (x - dst.x0)] = acc[r][c];
+                    dst.p[(y - dst.y0) * dst.s + (x - dst.x0)] = acc[r][c];
                     bad |= !isfinite(acc[r][c]);
                 }
             }
@@ -337,10 +342,10 @@ __device__ double loss_and_grad(const FitParams &p, FitSmem &S, int b) {
         for (int x = tx; x < canvas; x += 32) {
             const unsigned dy = (unsigned)(y - g.y0), dx = (unsigned)(x - g.x0);
             const bool in = dy < (unsigned)g.h && dx < (unsigned)g.w;
-            const float v = in ? g.p[dy * g.w + dx] : 0.f;
+            const float v = in ? g.p[dy * g.s + dx] : 0.f;
             const float d = v - tgt_at(p, b, canvas, y, x);
             part += (double)loss_term(d, p.cfg.loss_kind, p.cfg.loss_eps);
-            if (in) g.p[dy * g.w + dx] = loss_grad(d, p.cfg.loss_kind, p.cfg.loss_eps);
+            if (in) g.p[dy * g.s + dx] = loss_grad(d, p.cfg.loss_kind, p.cfg.loss_eps);
         }
     }
     return block_sum(S, part);
@@ -358,15 +363,20 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
     const int s0 = p.start[l], n = p.layout[l];
     const int nbx = (g.w + kFMC - 1) / kFMC, nby = (g.h + kFKR - 1) / kFKR;
     const int4 dr = S.dr[l];
-    for (int t0 = warp * kMaxTapsPerWarp; t0 < n; t0 += kFitWarps * kMaxTapsPerWarp) {
-        const int nt = min(kMaxTapsPerWarp, n - t0);
+    // taps spread evenly over the warps, at most kMaxTapsPerWarp per sweep
+    const int tpw = min(kMaxTapsPerWarp, (n + kFitWarps - 1) / kFitWarps);
+    for (int t0 = warp * tpw; t0 < n; t0 += kFitWarps * tpw) {
+        const int nt = min(tpw, n - t0);
         double C[kMaxTapsPerWarp][4];
 #pragma unroll
         for (int k = 0; k < kMaxTapsPerWarp; ++k)
 #pragma unroll
             for (int c = 0; c < 4; ++c) C[k][c] = 0.0;
-        for (int blk = lane; blk < nbx * nby; blk += 32) {
-            const int by = blk / nbx, bx = blk - by * nbx;
+        // lanes sweep the blocks in 8 x 4 warp tiles (conflict-free with odd strides)
+        const int wtw = (nbx + 7) / 8, wth = (nby + 3) / 4;
+        for (int wt = 0; wt < wtw * wth; ++wt) {
+            const int bx = (wt % wtw) * 8 + (lane & 7), by = (wt / wtw) * 4 + (lane >> 3);
+            if (bx >= nbx || by >= nby) continue;
             const int y0 = g.y0 + by * kFKR, x0 = g.x0 + bx * kFMC;
             float gv[kFKR][kFMC];
 #pragma unroll
@@ -374,7 +384,7 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
 #pragma unroll
                 for (int c = 0; c < kFMC; ++c) {
                     const int y = y0 + r, x = x0 + c;
-                    gv[r][c] = (y < g.y0 + g.h && x < g.x0 + g.w) ? g.p[(y - g.y0) * g.w + (x - g.x0)] : 0.f;
+                    gv[r][c] = (y < g.y0 + g.h && x < g.x0 + g.w) ? g.p[(y - g.y0) * g.s + (x - g.x0)] : 0.f;
                 }
             const bool inside = y0 + dr.z >= I.y0 && y0 + kFKR - 1 + dr.w < I.y0 + I.h &&
                                 x0 + dr.x >= I.x0 && x0 + kFMC - 1 + dr.y < I.x0 + I.w;
@@ -384,11 +394,11 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
                 const int2 d = S.ixy[s0 + t0 + k];
                 float win[kFKR + 1][kFMC + 1];
                 if (inside) {
-                    const float *q = I.p + (y0 + d.y - I.y0) * I.w + (x0 + d.x - I.x0);
+                    const float *q = I.p + (y0 + d.y - I.y0) * I.s + (x0 + d.x - I.x0);
 #pragma unroll
                     for (int r = 0; r <= kFKR; ++r)
 #pragma unroll
-                        for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * I.w + c];
+                        for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * I.s + c];
                 } else {
 #pragma unroll
                     for (int r = 0; r <= kFKR; ++r)
@@ -447,7 +457,7 @@ __device__ void backward_sweep(const FitParams &p, FitSmem &S) {
             if (g.w > 0 && g.h > 0) {
                 gather_pass<true>(p, S, l, g, I);
             } else {
-                for (int e = threadIdx.x; e < I.w * I.h; e += blockDim.x) I.p[e] = 0.f;
+                for (int e = threadIdx.x; e < I.s * I.h; e += blockDim.x) I.p[e] = 0.f;
                 __syncthreads();
             }
         }

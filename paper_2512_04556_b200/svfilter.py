@@ -110,11 +110,12 @@ def stacked_params(basis: FilterBasis) -> np.ndarray:
     return out
 
 
-def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero"):
+def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero", out=None):
     """Per-pixel blended sparse filtering guided by a parameter map (svfilter.py:171-203).
 
     Each pass re-interpolates that layer's taps per pixel between the two
     bracketing basis entries and gathers bilinearly from the previous pass.
+    Host torch tensors (pinned) with a pinned `out` move with async copies.
     """
     t = torch()
     lib = nat.lib()
@@ -124,7 +125,7 @@ def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero"):
     if pm_shape != (h, w):
         raise EngineError(f"parameter map {pm_shape} must match image {(h, w)}")
     if isinstance(pmap, t.Tensor):
-        pm = pmap.to(device=im.tensor.device, dtype=t.float32).contiguous()
+        pm = pmap.to(device=im.tensor.device, dtype=t.float32, non_blocking=pmap.is_pinned()).contiguous()
     else:
         pm = t.from_numpy(np.ascontiguousarray(pmap, dtype=np.float32)).to(im.tensor.device)
     if boundary not in BOUNDARIES:
@@ -132,11 +133,11 @@ def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero"):
     stack = np.ascontiguousarray(stacked_params(basis))
     ps = np.ascontiguousarray(basis.params, dtype=np.float64)
     layout = np.ascontiguousarray(basis.layout, dtype=np.int32)
-    out = im.empty_like()
-    rc = lib.skc_sv_fwd(nat.ptr(im.tensor), im.dtype_id, nat.ptr(out), im.dtype_id, h, w, c,
+    res = im.empty_like()
+    rc = lib.skc_sv_fwd(nat.ptr(im.tensor), im.dtype_id, nat.ptr(res), im.dtype_id, h, w, c,
                         nat.ptr(pm), nat.dbl(ps), ps.size, nat.dbl(stack), stack.shape[2],
                         nat.ints(layout), layout.size, BOUNDARIES[boundary], nat.stream_ptr())
     if rc == nat.SKC_EBADARG:
         raise EngineError(f"sv_filter: {nat.last_error()}")
     nat.check(rc, "sv_filter")
-    return im.restore(out)
+    return im.restore(res, out)
