@@ -209,6 +209,24 @@ __device__ void build_taps_and_boxes(const FitParams &p, FitSmem &S, float *aren
     __syncthreads();
 }
 
+// Block b of a box with nbx x nby blocks: full groups of 8 block-columns are
+// enumerated 8-wide row by row (a warp's 32 consecutive blocks form an 8 x 4
+// tile: conflict-free with odd strides), the remainder group rem-wide.  Every
+// index in [0, nbx*nby) is a real block, so a linear distribution over threads
+// is perfectly balanced.
+__device__ __forceinline__ void block_of(int b, int nbx, int nby, int &bx, int &by) {
+    const int full = (nbx >> 3) * 8 * nby;
+    if (b < full) {
+        const int g = b / (8 * nby), r = b - g * 8 * nby;
+        by = r >> 3;
+        bx = g * 8 + (r & 7);
+    } else {
+        const int rem = nbx & 7, r = b - full;
+        by = r / rem;
+        bx = (nbx & ~7) + (r - by * rem);
+    }
+}
+
 // out(y, x) += sum over taps of the 4 corner products, for one KR x MC block.
 // `rd(y, x)` returns the source value at canvas (y, x) (checked or not); the
 // window of tap i starts at source (y0 + sy(i), x0 + sx(i)).
@@ -266,12 +284,10 @@ __device__ int gather_pass(const FitParams &p, FitSmem &S, int l, const Buf src,
     const int ry0 = ADJ ? -dr.w : dr.z, ry1 = ADJ ? kFKR - 1 - dr.z : kFKR - 1 + dr.w;
     const int rx0 = ADJ ? -dr.y : dr.x, rx1 = ADJ ? kFMC - 1 - dr.x : kFMC - 1 + dr.y;
     const int nbx = (dst.w + kFMC - 1) / kFMC, nby = (dst.h + kFKR - 1) / kFKR;
-    const int wtw = (nbx + 7) / 8, wth = (nby + 3) / 4;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int bad = 0;
-    for (int wt = warp; wt < wtw * wth; wt += kFitWarps) {
-        const int bx = (wt % wtw) * 8 + (lane & 7), by = (wt / wtw) * 4 + (lane >> 3);
-        if (bx >= nbx || by >= nby) continue;
+    for (int b = threadIdx.x; b < nbx * nby; b += blockDim.x) {
+        int bx, by;
+        block_of(b, nbx, nby, bx, by);
         const int y0 = dst.y0 + by * kFKR, x0 = dst.x0 + bx * kFMC;
         float acc[kFKR][kFMC];
 #pragma unroll
@@ -372,11 +388,9 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
         for (int k = 0; k < kMaxTapsPerWarp; ++k)
 #pragma unroll
             for (int c = 0; c < 4; ++c) C[k][c] = 0.0;
-        // lanes sweep the blocks in 8 x 4 warp tiles (conflict-free with odd strides)
-        const int wtw = (nbx + 7) / 8, wth = (nby + 3) / 4;
-        for (int wt = 0; wt < wtw * wth; ++wt) {
-            const int bx = (wt % wtw) * 8 + (lane & 7), by = (wt / wtw) * 4 + (lane >> 3);
-            if (bx >= nbx || by >= nby) continue;
+        for (int b = lane; b < nbx * nby; b += 32) {
+            int bx, by;
+            block_of(b, nbx, nby, bx, by);
             const int y0 = g.y0 + by * kFKR, x0 = g.x0 + bx * kFMC;
             float gv[kFKR][kFMC];
 #pragma unroll
