@@ -62,7 +62,7 @@ __device__ __forceinline__ void cp_async8(float *dst, const float *src, bool val
 
 // One channel plane of the halo tile into s[rows][pitch].  `frame` points at
 // the (H, W, C) HWC frame or the (C, H, W) planar frame.
-template <typename TI, bool PLANAR>
+template <typename TI, bool PLANAR, bool WAIT = true>
 __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ frame, const LGeom &g,
                                            int c, int gx0, int gy0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -93,7 +93,7 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
                 }
             }
         }
-        cp_async_wait_all();
+        if (WAIT) cp_async_wait_all();
     } else if constexpr (sizeof(TI) == 4) {
         const float *img = reinterpret_cast<const float *>(frame);
         for (int r = warp; r < g.rows; r += nw) {
@@ -239,6 +239,59 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
     for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
 
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
+// Persistent, double-buffered variant for fp32 planar inputs: each CTA walks
+// tiles blockIdx.x, +gridDim.x, ... and issues the cp.async loads of its next
+// tile before computing the current one, so the halo-tile transfer of
+// memory-bound layers (few taps) overlaps the FMAs instead of serialising.
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+template <int KR, typename TO, bool OUT_PL>
+__global__ void __launch_bounds__(kTWX *kTWY * 32)
+    layer_tap_pipe_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                          const __grid_constant__ TapList tl, int tiles_x, int tiles_y, int ntiles) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int TH = kTWY * 8 * KR;
+    const int C = g.C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int plane = g.rows * g.pitch;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * KR + ly * KR;
+    int t = blockIdx.x;
+    if (t >= ntiles) return;
+    {
+        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+        load_plane<float, true, false>(smem, in + b * fs, g, c, tx * kTTW + g.dx0, ty * TH + g.dy0);
+    }
+    cp_async_commit();
+    for (int k = 0; t < ntiles; t += gridDim.x, k ^= 1) {
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) {
+            const int c = tn % C, r = tn / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+            load_plane<float, true, false>(smem + (k ^ 1) * plane, in + b * fs, g, c, tx * kTTW + g.dx0,
+                                           ty * TH + g.dy0);
+        }
+        cp_async_commit();
+        cp_async_wait_one();
+        __syncthreads();
+        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+        const float *base = smem + k * plane + row0 * g.pitch + col0;
+        float acc[KR][8];
+#pragma unroll
+        for (int rr = 0; rr < KR; ++rr)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[rr][j] = 0.f;
+#pragma unroll 1
+        for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+#pragma unroll 1
+        for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+        store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty * TH + row0, tx * kTTW + col0, acc);
+        __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------- dense path ---
@@ -400,6 +453,16 @@ static int tap_kr_override() {
     return v;
 }
 
+// SKC_TAP_PIPE: 1 = always use the persistent double-buffered tap kernel for
+// planar inputs, 0 = never, default: layers with <= 12 taps (memory-bound).
+static int tap_pipe_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_TAP_PIPE");
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_taps(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int t0,
                        int t1, int boundary, int accumulate, cudaStream_t s) {
@@ -436,6 +499,25 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
+    if constexpr (IN_PL) {
+        const int mode = tap_pipe_mode();
+        if ((mode == 1 || (mode < 0 && tl.n <= 12)) && 2 * smem <= (size_t)kMaxSmem) {
+            const int tiles_x = ceil_div(W, kTTW), tiles_y = ceil_div(H, TH);
+            const long long nt = (long long)tiles_x * tiles_y * B * C;
+            if (nt < (1LL << 31)) {
+                const int per_sm = std::max(1, std::min(4, (int)((size_t)kMaxSmem / (2 * smem))));
+                const int grid = (int)std::min<long long>(nt, 148LL * per_sm);
+                auto kern = KR == 7 ? layer_tap_pipe_kernel<7, TO, OUT_PL> : layer_tap_pipe_kernel<5, TO, OUT_PL>;
+                static int a5 = set_smem_attr(layer_tap_pipe_kernel<5, TO, OUT_PL>);
+                static int a7 = set_smem_attr(layer_tap_pipe_kernel<7, TO, OUT_PL>);
+                if (a5 || a7) return a5 ? a5 : a7;
+                kern<<<grid, kTWX * kTWY * 32, 2 * smem, s>>>(reinterpret_cast<const float *>(pin), pout, g, tl,
+                                                                tiles_x, tiles_y, (int)nt);
+                SKC_LAUNCH_CHECK("layer_tap_pipe_kernel");
+                return SKC_OK;
+            }
+        }
+    }
     if (smem <= (size_t)kMaxSmem) {
         auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>;
         static int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
