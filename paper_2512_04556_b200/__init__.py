@@ -50,6 +50,15 @@ from .optim import (
     parse_layout,
     save_theta,
 )
+from .initializers import (
+    InitStrategy,
+    bbox_random_init,
+    build_init,
+    hybrid_init,
+    radial_init,
+    ss_init,
+    support_rejection_sample,
+)
 from .svfilter import FilterBasis, interp_weights, sv_filter, synthesize_filter
 
 __version__ = "0.1.0"

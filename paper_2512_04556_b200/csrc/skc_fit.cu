@@ -29,12 +29,12 @@
 
 namespace skc {
 
-constexpr int kFitThreads = 512;
+constexpr int kFitThreads = 256;       // two CTAs (two targets) per SM
 constexpr int kFitWarps = kFitThreads / 32;
 constexpr int kFitMaxL = 8;
 constexpr int kFitMaxP = 256;     // total taps per complex
 constexpr int kNeedGrow = 100;    // internal status: scratch canvas too small
-constexpr int kFitSmem = 200 * 1024;   // dynamic shared memory per CTA (state + arena)
+constexpr int kFitSmem = 110 * 1024;   // dynamic shared memory per CTA (state + arena)
 constexpr int kFKR = 5, kFMC = 4;      // register block of the pixel passes (KR odd)
 constexpr int kMaxTapsPerWarp = 4;     // correlation taps a warp carries at once
 
@@ -529,7 +529,7 @@ __device__ int project(const FitParams &p, FitSmem &S) {
 
 __device__ __forceinline__ int &hdr_i(float *st, int k) { return reinterpret_cast<int *>(st)[k]; }
 
-__global__ void __launch_bounds__(kFitThreads) fit_kernel(const __grid_constant__ FitParams p) {
+__global__ void __launch_bounds__(kFitThreads, 2) fit_kernel(const __grid_constant__ FitParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
     float *arena = reinterpret_cast<float *>(smem_raw + (sizeof(FitSmem) + 15) / 16 * 16);

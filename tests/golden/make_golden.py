@@ -269,7 +269,36 @@ def gen_kernels():
     np.savez_compressed(OUT / "kernels.npz", **cases)
 
 
+def gen_init():
+    """initializers.py strategies on a few targets (host restatement pin)."""
+    cases = {}
+    targets = {"gauss": sk.gaussian_kernel(2.0), "ring": sk.ring_kernel(5.0, 9.0, 23),
+               "disk": sk.disk_kernel(6.0)}
+    k = 0
+    for tname, tgt in targets.items():
+        for tag in ("rand", "ir", "ss", "ss-ir"):
+            for layout, kws in (((8, 4, 4), False), ((8, 8), True)):
+                if kws and tag not in ("ir", "ss-ir"):
+                    continue
+                cpx = sk.build_init(sk.InitStrategy(tag, seed=3 + k), tgt, layout, kws=kws)
+                off, w, lay = cpx_arrays(cpx)
+                cases[f"n{k}_tgt"] = tgt.weights
+                cases[f"n{k}_tag"] = np.array(tag)
+                cases[f"n{k}_seed"] = np.int64(3 + k)
+                cases[f"n{k}_layout"] = np.array(layout, dtype=np.int64)
+                cases[f"n{k}_kws"] = np.int64(kws)
+                cases[f"n{k}_off"] = off
+                cases[f"n{k}_w"] = w
+                k += 1
+    cases["n_init"] = np.int64(k)
+    off, r = sk.support_rejection_sample(targets["ring"], 12, seed=5, return_radius=True)
+    cases["srs_off"] = off
+    cases["srs_r"] = np.float64(r)
+    np.savez_compressed(OUT / "init.npz", **cases)
+
+
 if __name__ == "__main__":
+    gen_init()
     gen_engine()
     gen_ir()
     gen_sv()

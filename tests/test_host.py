@@ -129,3 +129,18 @@ def test_kawase_exact_reach():
     kaw = synth.kawase_complex()
     assert corner_reach(kaw) == (21, 21, 21, 21)
     assert math.ceil(kaw.reach) == 18
+
+
+def test_initializers_bit_exact_vs_reference(golden):
+    from paper_2512_04556_b200.initializers import InitStrategy, build_init, support_rejection_sample
+    g = golden("init")
+    for k in range(int(g["n_init"])):
+        tgt = skc.DenseKernel(g[f"n{k}_tgt"])
+        cpx = build_init(InitStrategy(str(g[f"n{k}_tag"]), seed=int(g[f"n{k}_seed"])), tgt,
+                         tuple(g[f"n{k}_layout"].tolist()), kws=bool(g[f"n{k}_kws"]))
+        off = np.concatenate([l.offsets for l in cpx.layers])
+        w = np.concatenate([l.weights for l in cpx.layers])
+        assert np.array_equal(off, g[f"n{k}_off"]), k
+        assert np.array_equal(w, g[f"n{k}_w"]), k
+    off, r = support_rejection_sample(skc.ring_kernel(5.0, 9.0, 23), 12, seed=5, return_radius=True)
+    assert np.array_equal(off, g["srs_off"]) and r == float(g["srs_r"])
