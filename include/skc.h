@@ -130,6 +130,20 @@ int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype,
 int skc_ir_batch(const float *taps, int B, const int *layout, int L, int nmax,
                  int canvas, float *out, void *stream);
 
+/*
+ * Energies of B complexes against ONE shared target for parallel tempering
+ * (baselines.pst_fit -> energies_of, baselines.py:175-191, whose IRs come from
+ * ir_batch_compiled, _fastpath.py:88-94): pixel-summed loss of each impulse
+ * response (canvas^2) against the zero-embedded target, +inf where the
+ * response's mass differs from prod_l sum_i w_li by > 1e-6*max(|.|,1) (the
+ * "leak wall") or where an intermediate is non-finite.
+ *   taps : device float32 (B, L, nmax, 3); tgt : device float32 (M, M)
+ *   energies : device float64 (B,)
+ */
+int skc_ir_energies(const float *taps, int B, const int *layout, int L, int nmax, int canvas,
+                    const float *tgt, int M, int loss_kind, float loss_eps, double *energies,
+                    void *stream);
+
 /* Fit configuration (optim.TrainConfig, ConstraintConfig, LossKind). */
 typedef struct skc_fit_cfg {
     int steps;            /* TrainConfig.steps                          */

@@ -38,7 +38,7 @@ constexpr int kFitSmem = 110 * 1024;   // dynamic shared memory per CTA (state +
 constexpr int kFKR = 5, kFMC = 4;      // register block of the pixel passes (KR odd)
 constexpr int kMaxTapsPerWarp = 4;     // correlation taps a warp carries at once
 
-enum FitMode { MODE_FIT = 0, MODE_BACKWARD = 1, MODE_IR = 2 };
+enum FitMode { MODE_FIT = 0, MODE_BACKWARD = 1, MODE_IR = 2, MODE_ENERGY = 3 };
 
 // Live box of an intermediate in canvas coordinates; empty when w or h <= 0.
 __host__ __device__ __forceinline__ int odd_stride(int w) { return w | 1; }
@@ -71,6 +71,8 @@ struct FitParams {
     float *loss_out;       // MODE_BACKWARD
     float *grads_out;      // MODE_BACKWARD: (B, L, nmax, 3)
     float *ir_out;         // MODE_IR: (B, canvas, canvas)
+    double *energy_out;    // MODE_ENERGY: (B,)
+    int tgt_shared;        // MODE_ENERGY: every complex uses target 0
 };
 
 struct FitSmem {
@@ -551,12 +553,46 @@ __global__ void __launch_bounds__(kFitThreads, 2) fit_kernel(const __grid_consta
         __syncthreads();
         build_taps_and_boxes(p, S, arena, gslots);
         const bool ok = forward(p, S);
+        if (!ok && p.mode == MODE_ENERGY) {
+            if (threadIdx.x == 0) p.energy_out[b] = INFINITY;   // rejected like a non-finite proposal
+            return;
+        }
         if (!ok) {
             if (threadIdx.x == 0) {
                 status[0] = SKC_ENONFINITE;
                 status[1] = S.bad_layer;
                 status[2] = S.bad_sample;
                 status[3] = 0;
+            }
+            return;
+        }
+        if (p.mode == MODE_ENERGY) {
+            // baselines.pst_fit energies_of (baselines.py:175-191): pixel-summed
+            // loss against the shared target, plus the "leak wall": a response
+            // whose mass differs from prod_l sum_i w_li (truncated off the
+            // canvas) is invalid (energy +inf)
+            const int cv = S.canvas;
+            const Buf ir = buf_of(S, p.L);
+            const int bt = p.tgt_shared ? 0 : b;
+            double part = 0.0, mass = 0.0;
+            const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+            for (int y = ty; y < cv; y += kFitWarps)
+                for (int x = tx; x < cv; x += 32) {
+                    const float v = ld_chk(ir, y, x);
+                    mass += (double)v;
+                    part += (double)loss_term(v - tgt_at(p, bt, cv, y, x), p.cfg.loss_kind, p.cfg.loss_eps);
+                }
+            const double e = block_sum(S, part);
+            const double m = block_sum(S, mass);
+            if (threadIdx.x == 0) {
+                double expected = 1.0;
+                for (int l = 0; l < p.L; ++l) {
+                    double sw = 0.0;
+                    for (int i = 0; i < p.layout[l]; ++i) sw += (double)S.w[p.start[l] + i];
+                    expected *= sw;
+                }
+                const double tol = 1e-6 * fmax(fabs(expected), 1.0);
+                p.energy_out[b] = fabs(m - expected) > tol ? INFINITY : e;
             }
             return;
         }
@@ -904,6 +940,35 @@ int skc_ir_batch(const float *taps, int B, const int *layout, int L, int nmax, i
         if (hs[4 * b] == SKC_ENONFINITE)
             return fail(SKC_ENONFINITE, "non-finite intermediate at layer " + std::to_string(hs[4 * b + 1]));
     return SKC_OK;
+}
+
+int skc_ir_energies(const float *taps, int B, const int *layout, int L, int nmax, int canvas,
+                    const float *tgt, int M, int loss_kind, float loss_eps, double *energies,
+                    void *stream) {
+    FitParams p;
+    int rc = fill_params(p, B, layout, L, nmax, M);
+    if (rc) return rc;
+    if (!taps || !tgt || !energies) return fail(SKC_EBADARG, "null pointer");
+    if (canvas < M || (canvas & 1) == 0 || (M & 1) == 0) return fail(SKC_EBADARG, "canvas/target must be odd, canvas >= M");
+    if (loss_kind < 0 || loss_kind > 2 || !(loss_eps > 0)) return fail(SKC_EBADARG, "bad loss kind");
+    cudaStream_t s = (cudaStream_t)stream;
+    p.mode = MODE_ENERGY;
+    p.canvas_fixed = canvas;
+    p.taps_in = taps;
+    p.tgts = tgt;
+    p.tgt_shared = 1;
+    p.energy_out = energies;
+    p.cfg.steps = 1;
+    p.cfg.loss_kind = loss_kind;
+    p.cfg.loss_eps = loss_eps;
+    void *st = nullptr;
+    if ((rc = pool_alloc(&st, (size_t)B * 4 * sizeof(int), s))) return rc;
+    p.status = (int *)st;
+    if ((rc = alloc_scratch(p, canvas, s))) { pool_free(st, s); return rc; }
+    rc = fit_launch(p, s);
+    pool_free(p.scratch, s);
+    pool_free(st, s);
+    return rc;
 }
 
 int skc_backward_batch(const float *taps, int B, const int *layout, int L, int nmax,

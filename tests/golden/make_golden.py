@@ -297,7 +297,31 @@ def gen_init():
     np.savez_compressed(OUT / "init.npz", **cases)
 
 
+def gen_pst():
+    """PST energies (baselines.py:175-191) and a short seeded pst_fit trace."""
+    from sparsekern import baselines
+    rng = np.random.default_rng(1006)
+    tgt = sk.DenseKernel(f32(sk.disk_kernel(5.0, 15).weights))
+    off = f32(rng.uniform(-3, 3, (6, 3, 4, 2)))
+    w = f32(rng.uniform(0.05, 1.0, (6, 3, 4)))
+    w /= w.sum(axis=2, keepdims=True)
+    w = f32(w)
+    off[5, 2, 0] = [40.0, 0.5]   # drifts off the canvas: leak wall -> inf
+    canvas = 25
+    irs = engine.synthesize_ir_batch(off, w, canvas)
+    diffs = irs - tgt.embedded(canvas).weights[None]
+    e = np.abs(diffs).sum(axis=(1, 2))
+    expected = np.prod(w.sum(axis=2), axis=1)
+    leak = np.abs(irs.sum(axis=(1, 2)) - expected) > 1e-6 * np.maximum(np.abs(expected), 1.0)
+    e[leak] = np.inf
+    res = baselines.pst_fit(tgt, (4, 4), baselines.PSTConfig(chains=4, iterations=20, seed=2),
+                            sk.InitStrategy("ss", seed=1), sk.LossKind("l1"))
+    np.savez_compressed(OUT / "pst.npz", tgt=tgt.weights, off=off, w=w, canvas=np.int64(canvas),
+                        energies=e, trace=res.trace, best=np.float64(res.best_energy))
+
+
 if __name__ == "__main__":
+    gen_pst()
     gen_init()
     gen_engine()
     gen_ir()

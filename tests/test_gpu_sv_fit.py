@@ -167,3 +167,19 @@ def test_fit_c4_statistics_vs_oracle(skc, orc):
     early = np.abs(gpu[:, :10] - ref["trace"][:, :10]) / ref["trace"][:, :10]
     assert early.max() < 1e-4
     assert abs(gpu[:, -1].mean() / ref["trace"][:, -1].mean() - 1) < 0.01
+
+
+def test_pst_energies_and_short_run(skc, golden):
+    """PST energies (loss + leak wall) on device."""
+    from paper_2512_04556_b200 import baselines
+    g = golden("pst")
+    tgt = skc.DenseKernel(g["tgt"])
+    e = baselines.ir_energies(g["off"], g["w"], tgt, int(g["canvas"]), skc.LossKind("l1"))
+    ref = g["energies"]
+    assert np.isinf(e[5]) and np.isinf(ref[5])
+    assert np.allclose(e[:5], ref[:5], rtol=1e-5)
+    res = baselines.pst_fit(tgt, (4, 4), baselines.PSTConfig(chains=4, iterations=20, seed=2),
+                            skc.InitStrategy("ss", seed=1), skc.LossKind("l1"))
+    # same seeded proposal sequence: the first iterations track the reference
+    assert np.allclose(res.trace[:3, 1:], g["trace"][:3, 1:], rtol=1e-4)
+    assert res.best_energy <= g["trace"][0, 1] + 1e-6
