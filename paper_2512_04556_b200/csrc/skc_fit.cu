@@ -1041,9 +1041,11 @@ int skc_fit_run(float *state, int B, const int *layout, int L, int nmax, const f
         SKC_CUDA(cudaMemcpy2DAsync(hdr.data(), 4 * sizeof(int), state, stride * sizeof(float),
                                    4 * sizeof(int), B, cudaMemcpyDeviceToHost, s));
         SKC_CUDA(cudaStreamSynchronize(s));
+        // generous first capacity (diverging fits grow their canvas every step;
+        // a parked target resumes alone, so relaunches are expensive tails)
         int cap = 1;
         for (int b = 0; b < B; ++b) cap = std::max(cap, hdr[4 * b + 1]);
-        cap += 32 + attempt * 64;
+        cap = attempt == 0 ? 2 * cap + 32 : cap + cap / 2 + 64;
         if ((rc = alloc_scratch(p, cap, s))) return rc;
         rc = fit_launch(p, s);
         if (rc == SKC_OK) {
