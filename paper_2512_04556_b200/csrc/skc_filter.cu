@@ -18,7 +18,7 @@
 namespace skc {
 
 // ------------------------------------------------------- SV filter kernel ---
-constexpr int kSvTW = 64, kSvTH = 32, kSvPx = 8;  // 256 threads x 8 rows
+constexpr int kSvTW = 64, kSvPx = 8;  // 64 x (8 * thread rows) tile; 8 pixels per thread
 constexpr int kMaxBasis = 64;
 
 struct SvParams {
@@ -39,33 +39,36 @@ __device__ __forceinline__ void bracket(float p, const SvParams &q, int &k0, int
     t = (pc - q.ps[k]) / (q.ps[k + 1] - q.ps[k]);
 }
 
-template <int C, typename TI, typename TO>
-__global__ void __launch_bounds__(256)
+// Table rows are per bracket k0: entry (k0, i) = {o[k0] (ox, oy, w), o[k0+1] - o[k0]},
+// so the per-pixel lerp is one FFMA per component.
+template <int C, int TR, typename TI, typename TO>
+__global__ void __launch_bounds__(TR * 64)
     sv_tile_kernel(const TI *__restrict__ in, TO *__restrict__ out, const float *__restrict__ pmap,
                    const float4 *__restrict__ table, const __grid_constant__ SvParams q) {
     extern __shared__ float4 smem4[];
-    float4 *stab = smem4;  // (Mb, n) entries (ox, oy, w, 0)
-    float *tile = reinterpret_cast<float *>(smem4 + q.Mb * q.n);
-    const int tx0 = blockIdx.x * kSvTW, ty0 = blockIdx.y * kSvTH;
-    for (int i = threadIdx.x; i < q.Mb * q.n; i += blockDim.x) stab[i] = table[i];
+    constexpr int TH = TR * kSvPx;
+    const int nrow = q.Mb > 1 ? q.Mb - 1 : 1;
+    float4 *stab = smem4;  // (nrow, n, 2)
+    float *tile = reinterpret_cast<float *>(smem4 + 2 * nrow * q.n);
+    const int tx0 = blockIdx.x * kSvTW, ty0 = blockIdx.y * TH;
+    for (int i = threadIdx.x; i < 2 * nrow * q.n; i += blockDim.x) stab[i] = table[i];
     load_tile<C, TI>(tile, in, q.H, q.W, q.boundary, tx0 + q.dx0, ty0 + q.dy0, q.pitch, q.rows);
     __syncthreads();
 
     const int tx = threadIdx.x & (kSvTW - 1), ty = threadIdx.x / kSvTW;
     const int plane = q.rows * q.pitch, pitch = q.pitch;
     const int gx = tx0 + tx;
-    int e0[kSvPx], e1[kSvPx];
+    int e0[kSvPx];
     float tt[kSvPx];
     float acc[kSvPx][C];
 #pragma unroll
     for (int k = 0; k < kSvPx; ++k) {
-        const int gy = ty0 + ty + 4 * k;
+        const int gy = ty0 + ty + TR * k;
         float p = 0.f;
         if (gy < q.H && gx < q.W) p = __ldg(pmap + (long long)gy * q.W + gx);
         int k0, k1;
         bracket(p, q, k0, k1, tt[k]);
-        e0[k] = k0 * q.n;
-        e1[k] = k1 * q.n;
+        e0[k] = 2 * k0 * q.n;
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[k][c] = 0.f;
     }
@@ -75,18 +78,18 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < q.n; ++i) {
 #pragma unroll
         for (int k = 0; k < kSvPx; ++k) {
-            const float4 a = stab[e0[k] + i];
-            const float4 b = stab[e1[k] + i];
-            const float t = tt[k], u = 1.f - t;
-            // _fastpath.py:109-111: lerp of offsets and weight
-            const float ox = u * a.x + t * b.x;
-            const float oy = u * a.y + t * b.y;
-            const float w = u * a.z + t * b.z;
+            const float4 a = stab[e0[k] + 2 * i];
+            const float4 d = stab[e0[k] + 2 * i + 1];
+            const float t = tt[k];
+            // _fastpath.py:109-111: lerp of offsets and weight between the bracket
+            const float ox = fmaf(t, d.x, a.x);
+            const float oy = fmaf(t, d.y, a.y);
+            const float w = fmaf(t, d.z, a.z);
             const float fx0 = floorf(ox), fy0 = floorf(oy);
             const float fx = ox - fx0, fy = oy - fy0;
-            const float wa = w * (1.f - fy), wb = w * fy;
-            const float c00 = wa * (1.f - fx), c10 = wa * fx, c01 = wb * (1.f - fx), c11 = wb * fx;
-            const int off = base0 + (4 * k + (int)fy0) * pitch + (int)fx0;
+            const float wb = w * fy, wa = w - wb;
+            const float c10 = wa * fx, c00 = wa - c10, c11 = wb * fx, c01 = wb - c11;
+            const int off = base0 + (TR * k + (int)fy0) * pitch + (int)fx0;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const float *sp = tile + c * plane + off;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int k = 0; k < kSvPx; ++k) {
-        const int gy = ty0 + ty + 4 * k;
+        const int gy = ty0 + ty + TR * k;
         if (gy >= q.H || gx >= q.W) continue;
         TO *o = out + ((long long)gy * q.W + gx) * C;
 #pragma unroll
@@ -120,14 +123,13 @@ __global__ void __launch_bounds__(256)
         int k0, k1;
         float t;
         bracket(__ldg(pmap + p), q, k0, k1, t);
-        const float u = 1.f - t;
         float acc[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[c] = 0.f;
         for (int i = 0; i < q.n; ++i) {
-            const float4 a = __ldg(table + k0 * q.n + i);
-            const float4 b = __ldg(table + k1 * q.n + i);
-            const float ox = u * a.x + t * b.x, oy = u * a.y + t * b.y, w = u * a.z + t * b.z;
+            const float4 a = __ldg(table + 2 * (k0 * q.n + i));
+            const float4 d = __ldg(table + 2 * (k0 * q.n + i) + 1);
+            const float ox = fmaf(t, d.x, a.x), oy = fmaf(t, d.y, a.y), w = fmaf(t, d.z, a.z);
             const float fx0 = floorf(ox), fy0 = floorf(oy);
             const float fx = ox - fx0, fy = oy - fy0;
             const float wa = w * (1.f - fy), wb = w * fy;
@@ -151,28 +153,40 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+template <int C, int TR, typename TI, typename TO>
+static int launch_sv_tile(const void *in, void *out, const float *pmap, const float4 *table, SvParams q,
+                          int span_y, cudaStream_t s) {
+    q.rows = TR * kSvPx + span_y;
+    const int nrow = q.Mb > 1 ? q.Mb - 1 : 1;
+    const size_t smem = (size_t)2 * nrow * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
+    if (smem > (size_t)kMaxSmem) return -1;
+    auto kern = sv_tile_kernel<C, TR, TI, TO>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr_set = true;
+    }
+    dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, TR * kSvPx));
+    kern<<<grid, TR * 64, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), pmap, table, q);
+    SKC_LAUNCH_CHECK("sv_tile_kernel");
+    return SKC_OK;
+}
+
+// Big halos get the taller 64 x 64 tile (16 warps, half the halo overfetch);
+// small halos the 64 x 32 tile (more CTAs per SM).
 template <int C, typename TI, typename TO>
 static int launch_sv_t(const void *in, void *out, const float *pmap, const float4 *table,
                        SvParams q, cudaStream_t s) {
-    const size_t smem = (size_t)q.Mb * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
-    const TI *pin = static_cast<const TI *>(in);
-    TO *pout = static_cast<TO *>(out);
-    if (smem <= (size_t)kMaxSmem) {
-        auto kern = sv_tile_kernel<C, TI, TO>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-            attr_set = true;
-        }
-        dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, kSvTH));
-        kern<<<grid, 256, smem, s>>>(pin, pout, pmap, table, q);
-        SKC_LAUNCH_CHECK("sv_tile_kernel");
-    } else {
-        const long long npx = (long long)q.H * q.W;
-        const unsigned grid = (unsigned)std::min<long long>((npx + 255) / 256, 148 * 16);
-        sv_direct_kernel<C, TI, TO><<<grid, 256, 0, s>>>(pin, pout, pmap, table, q);
-        SKC_LAUNCH_CHECK("sv_direct_kernel");
-    }
+    const int span_y = q.rows;  // caller passes the vertical halo span in rows
+    int rc = -1;
+    if (span_y > 24) rc = launch_sv_tile<C, 8, TI, TO>(in, out, pmap, table, q, span_y, s);
+    if (rc == -1) rc = launch_sv_tile<C, 4, TI, TO>(in, out, pmap, table, q, span_y, s);
+    if (rc != -1) return rc;
+    const long long npx = (long long)q.H * q.W;
+    const unsigned grid = (unsigned)std::min<long long>((npx + 255) / 256, 148 * 16);
+    sv_direct_kernel<C, TI, TO><<<grid, 256, 0, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), pmap,
+                                                     table, q);
+    SKC_LAUNCH_CHECK("sv_direct_kernel");
     return SKC_OK;
 }
 
@@ -218,14 +232,19 @@ int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype, int H, in
     cudaStream_t s = (cudaStream_t)stream;
 
     // per-layer tables (Mb, n_l) of (ox, oy, w, 0) in one device upload
+    // rows per bracket k0: {o[k0], o[k0+1] - o[k0]} (the difference in float64)
     std::vector<float4> host;
     std::vector<size_t> start(L);
+    const int nrow = Mb > 1 ? Mb - 1 : 1;
     for (int l = 0; l < L; ++l) {
         start[l] = host.size();
-        for (int k = 0; k < Mb; ++k)
+        for (int k = 0; k < nrow; ++k)
             for (int i = 0; i < layout[l]; ++i) {
-                const double *e = basis + (((size_t)k * L + l) * nmax + i) * 3;
-                host.push_back(make_float4((float)e[0], (float)e[1], (float)e[2], 0.f));
+                const double *e0 = basis + (((size_t)k * L + l) * nmax + i) * 3;
+                const double *e1 = Mb > 1 ? basis + (((size_t)(k + 1) * L + l) * nmax + i) * 3 : e0;
+                host.push_back(make_float4((float)e0[0], (float)e0[1], (float)e0[2], 0.f));
+                host.push_back(make_float4((float)(e1[0] - e0[0]), (float)(e1[1] - e0[1]),
+                                           (float)(e1[2] - e0[2]), 0.f));
             }
     }
     void *dtab = nullptr;
@@ -269,7 +288,7 @@ int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype, int H, in
         int pitch = kSvTW + (dx_max - dx_min);
         if ((pitch & 1) == 0) ++pitch;
         q.pitch = pitch;
-        q.rows = kSvTH + (dy_max - dy_min);
+        q.rows = dy_max - dy_min;   // vertical halo span; the launcher adds the tile height
         const void *src = l == 0 ? in : buf[(l - 1) & 1];
         const int sdt = l == 0 ? in_dtype : SKC_F32;
         void *dst = l == L - 1 ? out : buf[l & 1];
