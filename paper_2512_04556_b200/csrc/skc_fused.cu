@@ -217,9 +217,12 @@ int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_p
 // relayout).  Returns -1 when the chain is not eligible.
 int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
                 const double *taps, const int *layout, int L, int boundary, cudaStream_t s, bool dry) {
+    // Opt-in (SKC_FUSED=1): on B200 the fused launch (1 CTA/SM at 186 KB of
+    // planes, 2x redundant halo work) measured slower than the unfused
+    // planar chain for config 3 (24.9 vs 15.9 ms for 32 frames).
     static const bool enabled = [] {
         const char *e = std::getenv("SKC_FUSED");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     if (!enabled || L < 2 || L > kF2MaxL || B > 65535) return -1;
     F2Params q;

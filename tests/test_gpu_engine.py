@@ -271,26 +271,29 @@ def test_fused_chain_matches_oracle_and_unfused(skc, orc):
     kaw = synth.kawase_complex()
     t = np.ascontiguousarray(kaw.taps())
     lay = np.ascontiguousarray(kaw.layout, dtype=np.int32)
-    assert nat.lib().skc_chain_is_fused(nat.dbl(t), nat.ints(lay), 6, 2160, 3840, 4, 1) == 1
+    root = str(__import__("pathlib").Path(__file__).parent.parent)
+    probe = ("import numpy as np, sys; sys.path.insert(0, '.');"
+             "from paper_2512_04556_b200 import _native as nat, synth; k = synth.kawase_complex();"
+             "t = np.ascontiguousarray(k.taps()); l = np.ascontiguousarray(k.layout, dtype=np.int32);"
+             "sys.exit(0 if nat.lib().skc_chain_is_fused(nat.dbl(t), nat.ints(l), 6, 2160, 3840, 4, 1) == 1 else 3)")
+    subprocess.run([sys.executable, "-c", probe], check=True, env=dict(os.environ, SKC_FUSED="1"), cwd=root)
     rng = np.random.default_rng(31)
     layers = [(l.offsets, l.weights) for l in kaw.layers]
-    for shape in [(5, 7, 4), (50, 33, 1), (131, 197, 3), (96, 128, 4)]:
-        img = rng.random(shape).astype(np.float32)
-        for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
-            ref = orc.apply_complex(img.astype(np.float64), layers, oid)
-            assert normwise(skc.apply_complex(img, kaw, boundary=mode), ref) < TOL32, (shape, mode)
-            h = img.astype(np.float16)
-            refh = orc.apply_complex(h.astype(np.float64), layers, oid)
-            assert normwise(skc.apply_complex(h, kaw, boundary=mode).astype(np.float64), refh) < TOL16
     code = ("import numpy as np, sys; sys.path.insert(0, '.');"
             "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
-            "np.save(sys.argv[2], skc.apply_complex(np.load(sys.argv[1]), synth.kawase_complex(), boundary='clamp'))")
-    root = str(__import__("pathlib").Path(__file__).parent.parent)
-    img = rng.random((140, 210, 4)).astype(np.float32)
+            "x = np.load(sys.argv[1]); np.save(sys.argv[2], skc.apply_complex(x, synth.kawase_complex(), boundary=sys.argv[3]))")
     with tempfile.TemporaryDirectory() as td:
-        np.save(f"{td}/in.npy", img)
-        subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/unfused.npy"], check=True,
-                       env=dict(os.environ, SKC_FUSED="0"), cwd=root)
-        unf = np.load(f"{td}/unfused.npy")
-    fused = skc.apply_complex(img, kaw, boundary="clamp")
-    assert normwise(fused, unf) < 1e-6
+        for k, shape in enumerate([(5, 7, 4), (50, 33, 1), (131, 197, 3), (96, 128, 4), (140, 210, 4)]):
+            img = rng.random(shape).astype(np.float32)
+            for dt, tol in ((np.float32, TOL32), (np.float16, TOL16)):
+                x = img.astype(dt)
+                np.save(f"{td}/in.npy", x)
+                for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                    ref = orc.apply_complex(x.astype(np.float64), layers, oid)
+                    outs = []
+                    for f in ("1", "0"):
+                        subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/o{f}.npy", mode],
+                                       check=True, env=dict(os.environ, SKC_FUSED=f), cwd=root)
+                        outs.append(np.load(f"{td}/o{f}.npy").astype(np.float64))
+                    assert normwise(outs[0], ref) < tol, (shape, mode, dt)
+                    assert normwise(outs[0], outs[1]) < (1e-6 if dt == np.float32 else tol), (shape, mode)
