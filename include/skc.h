@@ -121,6 +121,18 @@ int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype,
                const int *layout, int L, int boundary, void *stream);
 
 /*
+ * 2-D parameter SV filtering (svfilter.sv_filter_grid, svfilter.py:292-319):
+ * a (Mu, Mv) grid of basis complexes, per-pixel bilinear blend of the four
+ * bracketing entries' taps.  fp32 images only.
+ *   pmap2  : device float32 (H, W, 2) = (u, v) per pixel
+ *   basis  : HOST float64 (Mu, Mv, L, nmax, 3)
+ */
+int skc_sv_grid_fwd(const void *in, void *out, int H, int W, int C, const float *pmap2,
+                    const double *params_u, int Mu, const double *params_v, int Mv,
+                    const double *basis, int nmax, const int *layout, int L, int boundary,
+                    void *stream);
+
+/*
  * Batched impulse responses (engine.synthesize_ir / synthesize_ir_batch,
  * engine.py:191-209, 251-303; _fastpath.ir_batch_compiled, _fastpath.py:33-94).
  *   taps : device float32 (B, L, nmax, 3) = (ox, oy, w); zero weights inert

@@ -17,6 +17,7 @@ from .engine import (
     apply_complex_batch,
     apply_sparse_layer,
     auto_canvas,
+    dense_convolve,
     psnr,
     required_canvas,
     sse,
@@ -59,6 +60,16 @@ from .initializers import (
     ss_init,
     support_rejection_sample,
 )
-from .svfilter import FilterBasis, interp_weights, sv_filter, synthesize_filter
+from .svfilter import (
+    FilterBasis,
+    FilterBasisGrid,
+    build_basis,
+    interp_weights,
+    load_basis,
+    save_basis,
+    sv_filter,
+    sv_filter_grid,
+    synthesize_filter,
+)
 
 __version__ = "0.1.0"

@@ -30,7 +30,7 @@ FIT_HDR = 8
 EXPORTS = (
     "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused",
     "skc_chain_fwd",
-    "skc_sv_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
+    "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step",
 )
 
@@ -80,6 +80,7 @@ def _declare(lib):
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,
                                _vp]
+    lib.skc_sv_grid_fwd.argtypes = [_vp, _vp, _i, _i, _i, _vp, _dp, _i, _dp, _i, _dp, _i, _ip, _i, _i, _vp]
     lib.skc_ir_batch.argtypes = [_vp, _i, _ip, _i, _i, _i, _vp, _vp]
     lib.skc_ir_energies.argtypes = [_vp, _i, _ip, _i, _i, _i, _vp, _i, _i, ctypes.c_float, _vp, _vp]
     lib.skc_backward_batch.argtypes = [_vp, _i, _ip, _i, _i, _vp, _i, _i, _i, ctypes.c_float,

@@ -29,14 +29,17 @@ struct SvParams {
 };
 
 // svfilter._bracket (svfilter.py:129-137) in fp32 on the fp32 map.
-__device__ __forceinline__ void bracket(float p, const SvParams &q, int &k0, int &k1, float &t) {
-    if (q.Mb == 1) { k0 = 0; k1 = 0; t = 0.f; return; }
-    const float pc = fminf(fmaxf(p, q.ps[0]), q.ps[q.Mb - 1]);
+__device__ __forceinline__ void bracket_ps(float p, const float *ps, int Mb, int &k0, int &k1, float &t) {
+    if (Mb == 1) { k0 = 0; k1 = 0; t = 0.f; return; }
+    const float pc = fminf(fmaxf(p, ps[0]), ps[Mb - 1]);
     int k = 0;
-    for (int j = 1; j < q.Mb - 1; ++j) k += (q.ps[j] <= pc) ? 1 : 0;
+    for (int j = 1; j < Mb - 1; ++j) k += (ps[j] <= pc) ? 1 : 0;
     k0 = k;
     k1 = k + 1;
-    t = (pc - q.ps[k]) / (q.ps[k + 1] - q.ps[k]);
+    t = (pc - ps[k]) / (ps[k + 1] - ps[k]);
+}
+__device__ __forceinline__ void bracket(float p, const SvParams &q, int &k0, int &k1, float &t) {
+    bracket_ps(p, q.ps, q.Mb, k0, k1, t);
 }
 
 // Table rows are per bracket k0: entry (k0, i) = {o[k0] (ox, oy, w), o[k0+1] - o[k0]},
@@ -210,6 +213,95 @@ static int launch_sv(const void *in, int idt, void *out, int odt, int C, const f
     }
 }
 
+// ------------------------------------------------ 2-D grid SV (next row) ---
+// svfilter.sv_filter_grid (svfilter.py:292-319): per pixel two brackets
+// (u, v) and a bilinear blend of the four surrounding basis entries' taps
+// (weights (1-tu)(1-tv), tu(1-tv), (1-tu)tv, tu tv), then the same bilinear
+// gather from the staged halo tile as the 1-D SV kernel.
+struct SvGridParams {
+    int H, W, Mu, Mv, n, boundary;
+    int dx0, dy0, pitch, rows;
+    float pu[kMaxBasis], pv[kMaxBasis];
+};
+
+template <int C, typename TI, typename TO>
+__global__ void __launch_bounds__(256)
+    sv_grid_kernel(const TI *__restrict__ in, TO *__restrict__ out, const float2 *__restrict__ pmap2,
+                   const float4 *__restrict__ table, const __grid_constant__ SvGridParams q) {
+    extern __shared__ float4 smem4[];
+    constexpr int TR = 4, TH = TR * kSvPx;
+    const int nent = q.Mu * q.Mv * q.n;
+    float4 *stab = smem4;  // (Mu, Mv, n) entries (ox, oy, w, 0)
+    float *tile = reinterpret_cast<float *>(smem4 + nent);
+    const int tx0 = blockIdx.x * kSvTW, ty0 = blockIdx.y * TH;
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) stab[i] = table[i];
+    load_tile<C, TI>(tile, in, q.H, q.W, q.boundary, tx0 + q.dx0, ty0 + q.dy0, q.pitch, q.rows);
+    __syncthreads();
+    const int tx = threadIdx.x & (kSvTW - 1), ty = threadIdx.x / kSvTW;
+    const int plane = q.rows * q.pitch, pitch = q.pitch;
+    const int gx = tx0 + tx;
+    const int base0 = (ty - q.dy0) * pitch + (tx - q.dx0);
+#pragma unroll 1
+    for (int k = 0; k < kSvPx; ++k) {
+        const int gy = ty0 + ty + TR * k;
+        float2 pm = make_float2(0.f, 0.f);
+        if (gy < q.H && gx < q.W) pm = pmap2[(long long)gy * q.W + gx];
+        int u0, u1, v0, v1;
+        float tu, tv;
+        bracket_ps(pm.x, q.pu, q.Mu, u0, u1, tu);
+        bracket_ps(pm.y, q.pv, q.Mv, v0, v1, tv);
+        const float b00 = (1.f - tu) * (1.f - tv), b10 = tu * (1.f - tv), b01 = (1.f - tu) * tv, b11 = tu * tv;
+        const int e00 = (u0 * q.Mv + v0) * q.n, e10 = (u1 * q.Mv + v0) * q.n;
+        const int e01 = (u0 * q.Mv + v1) * q.n, e11 = (u1 * q.Mv + v1) * q.n;
+        float acc[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] = 0.f;
+        for (int i = 0; i < q.n; ++i) {
+            const float4 a = stab[e00 + i], b = stab[e10 + i], cc = stab[e01 + i], d = stab[e11 + i];
+            const float ox = b00 * a.x + b10 * b.x + b01 * cc.x + b11 * d.x;
+            const float oy = b00 * a.y + b10 * b.y + b01 * cc.y + b11 * d.y;
+            const float w = b00 * a.z + b10 * b.z + b01 * cc.z + b11 * d.z;
+            const float fx0 = floorf(ox), fy0 = floorf(oy);
+            const float fx = ox - fx0, fy = oy - fy0;
+            const float wb = w * fy, wa = w - wb;
+            const float c10 = wa * fx, c00 = wa - c10, c11 = wb * fx, c01 = wb - c11;
+            const int off = base0 + (TR * k + (int)fy0) * pitch + (int)fx0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const float *sp = tile + c * plane + off;
+                float v = acc[c];
+                v = fmaf(c00, sp[0], v);
+                v = fmaf(c10, sp[1], v);
+                v = fmaf(c01, sp[pitch], v);
+                v = fmaf(c11, sp[pitch + 1], v);
+                acc[c] = v;
+            }
+        }
+        if (gy < q.H && gx < q.W) {
+            TO *o = out + ((long long)gy * q.W + gx) * C;
+#pragma unroll
+            for (int c = 0; c < C; ++c) IO<TO>::st(o + c, acc[c]);
+        }
+    }
+}
+
+template <int C>
+static int launch_sv_grid_c(const void *in, void *out, const float2 *pmap2, const float4 *table,
+                            const SvGridParams &q, cudaStream_t s) {
+    const size_t smem = (size_t)q.Mu * q.Mv * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
+    if (smem > (size_t)kMaxSmem) return fail(SKC_EBADARG, "grid SV basis/halo too large for shared memory");
+    auto kern = sv_grid_kernel<C, float, float>;
+    static bool attr = false;
+    if (!attr) {
+        SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, 4 * kSvPx));
+    kern<<<grid, 256, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), pmap2, table, q);
+    SKC_LAUNCH_CHECK("sv_grid_kernel");
+    return SKC_OK;
+}
+
 }  // namespace skc
 
 using namespace skc;
@@ -301,4 +393,86 @@ int skc_sv_fwd(const void *in, int in_dtype, void *out, int out_dtype, int H, in
     return rc;
 }
 
+int skc_sv_grid_fwd(const void *in, void *out, int H, int W, int C, const float *pmap2,
+                    const double *params_u, int Mu, const double *params_v, int Mv, const double *basis,
+                    int nmax, const int *layout, int L, int boundary, void *stream) {
+    int rc = check_image_args(in, SKC_F32, out, SKC_F32, 1, H, W, C, boundary);
+    if (rc) return rc;
+    if (!pmap2 || !params_u || !params_v || !basis || !layout) return fail(SKC_EBADARG, "null argument");
+    if (Mu < 1 || Mu > kMaxBasis || Mv < 1 || Mv > kMaxBasis) return fail(SKC_EBADARG, "grid axes must be 1..64");
+    if (L < 1 || nmax < 1) return fail(SKC_EBADARG, "basis needs at least one layer");
+    for (int k = 1; k < Mu; ++k)
+        if (!(params_u[k] > params_u[k - 1])) return fail(SKC_EBADARG, "grid parameters must be strictly increasing");
+    for (int k = 1; k < Mv; ++k)
+        if (!(params_v[k] > params_v[k - 1])) return fail(SKC_EBADARG, "grid parameters must be strictly increasing");
+    for (int l = 0; l < L; ++l)
+        if (layout[l] < 1 || layout[l] > nmax) return fail(SKC_EBADARG, "bad basis layout");
+    if (!finite_taps(basis, Mu * Mv * L * nmax)) return fail(SKC_EBADARG, "basis parameters must be finite");
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<float4> host;
+    std::vector<size_t> start(L);
+    for (int l = 0; l < L; ++l) {
+        start[l] = host.size();
+        for (int k = 0; k < Mu * Mv; ++k)
+            for (int i = 0; i < layout[l]; ++i) {
+                const double *e = basis + (((size_t)k * L + l) * nmax + i) * 3;
+                host.push_back(make_float4((float)e[0], (float)e[1], (float)e[2], 0.f));
+            }
+    }
+    void *dtab = nullptr;
+    if ((rc = pool_alloc(&dtab, host.size() * sizeof(float4), s))) return rc;
+    cudaError_t ce = cudaMemcpyAsync(dtab, host.data(), host.size() * sizeof(float4), cudaMemcpyHostToDevice, s);
+    if (ce != cudaSuccess) { pool_free(dtab, s); return cuda_fail(ce, "cudaMemcpyAsync(grid table)"); }
+    const size_t n = (size_t)H * W * C;
+    void *buf[2] = {nullptr, nullptr};
+    const int nbuf = L > 2 ? 2 : (L - 1);
+    for (int i = 0; i < nbuf && rc == SKC_OK; ++i) rc = pool_alloc(&buf[i], n * sizeof(float), s);
+    SvGridParams q;
+    q.H = H;
+    q.W = W;
+    q.Mu = Mu;
+    q.Mv = Mv;
+    q.boundary = boundary;
+    for (int k = 0; k < Mu; ++k) q.pu[k] = (float)params_u[k];
+    for (int k = 0; k < Mv; ++k) q.pv[k] = (float)params_v[k];
+    for (int l = 0; l < L && rc == SKC_OK; ++l) {
+        const int nl = layout[l];
+        q.n = nl;
+        double lo_x = 0, hi_x = 0, lo_y = 0, hi_y = 0;
+        bool first = true;
+        for (int k = 0; k < Mu * Mv; ++k)
+            for (int i = 0; i < nl; ++i) {
+                const double *e = basis + (((size_t)k * L + l) * nmax + i) * 3;
+                if (first || e[0] < lo_x) lo_x = e[0];
+                if (first || e[0] > hi_x) hi_x = e[0];
+                if (first || e[1] < lo_y) lo_y = e[1];
+                if (first || e[1] > hi_y) hi_y = e[1];
+                first = false;
+            }
+        const int dx_min = (int)std::floor(lo_x) - 1, dx_max = (int)std::floor(hi_x) + 2;
+        const int dy_min = (int)std::floor(lo_y) - 1, dy_max = (int)std::floor(hi_y) + 2;
+        q.dx0 = dx_min;
+        q.dy0 = dy_min;
+        int pitch = kSvTW + (dx_max - dx_min);
+        if ((pitch & 1) == 0) ++pitch;
+        q.pitch = pitch;
+        q.rows = 4 * kSvPx + (dy_max - dy_min);
+        const void *src = l == 0 ? in : buf[(l - 1) & 1];
+        void *dst = l == L - 1 ? out : buf[l & 1];
+        const float4 *tab = (const float4 *)dtab + start[l];
+        const float2 *pm = (const float2 *)pmap2;
+        switch (C) {
+            case 1: rc = launch_sv_grid_c<1>(src, dst, pm, tab, q, s); break;
+            case 2: rc = launch_sv_grid_c<2>(src, dst, pm, tab, q, s); break;
+            case 3: rc = launch_sv_grid_c<3>(src, dst, pm, tab, q, s); break;
+            default: rc = launch_sv_grid_c<4>(src, dst, pm, tab, q, s); break;
+        }
+    }
+    for (int i = 0; i < nbuf; ++i)
+        if (buf[i]) pool_free(buf[i], s);
+    pool_free(dtab, s);
+    return rc;
+}
+
 }  // extern "C"
+

@@ -343,6 +343,79 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
+// HWC-input dense stencil with all channels per CTA (first layer of a chain):
+// the tile rows are contiguous runs of W*C floats in the interleaved image, so
+// they stage with coalesced 4-byte cp.async and stay interleaved in shared
+// memory; windows read with a stride of C words, conflict-free because the
+// pixel pitch is odd and KR is odd (C odd or 1).  Writes planar fp32.
+constexpr int kHWX = 2, kHWY = 2;                  // 128 threads, tile 64 x 80
+constexpr int kHTW = kHWX * 32, kHTH = kHWY * 8 * kDenKR;
+
+template <int D, int C>
+__global__ void __launch_bounds__(kHWX *kHWY * 32)
+    layer_stencil_hwc_kernel(const float *__restrict__ in, float *__restrict__ out, const LGeom g,
+                             const __grid_constant__ DenseList dl) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kDenKR;
+    const int b = blockIdx.z;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = blockIdx.x * kHTW, ty0 = blockIdx.y * kHTH;
+    const int gx0 = tx0 + g.dx0, gy0 = ty0 + g.dy0;
+    const float *frame = in + b * fs;
+    const bool clamp = g.boundary == SKC_CLAMP;
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int rowlen = g.pitch * C;
+        for (int r = warp; r < g.rows; r += nw) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < g.H);
+            gy = min(max(gy, 0), g.H - 1);
+            const float *src = frame + (long long)gy * g.W * C;
+            float *dst = smem + r * rowlen;
+#pragma unroll 4
+            for (int e = lane; e < rowlen; e += 32) {
+                const int col = e / C, c = e - col * C;
+                const int gx = gx0 + col;
+                const bool ok = clamp || (rowin && gx >= 0 && gx < g.W);
+                cp_async4(dst + e, src + (long long)min(max(gx, 0), g.W - 1) * C + c, ok);
+            }
+        }
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kHWX, wy = warp / kHWX;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    const int rs = g.pitch * C;   // row stride in words
+#pragma unroll 1
+    for (int c = 0; c < C; ++c) {
+        const float *pc = smem + row0 * rs + (col0 + dl.col_shift) * C + c;
+        float acc[KR][8];
+#pragma unroll
+        for (int i = 0; i < KR; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+        for (int r = 0; r < KR + D - 1; ++r) {
+            float w[8 + D - 1];
+#pragma unroll
+            for (int j = 0; j < 8 + D - 1; ++j) w[j] = pc[r * rs + j * C];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int i = r - a;
+                if (i < 0 || i >= KR) continue;
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    const float k = dl.k[a * D + bb];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
+                }
+            }
+        }
+        store_block<KR, float, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+    }
+}
+
 // ------------------------------------------------ direct (huge halo) path ---
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(256)
@@ -550,6 +623,35 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
     return SKC_OK;
 }
 
+template <int D, int C>
+static int launch_stencil_hwc_dc(const void *in, void *out, int B, const DenseList &dl, const LGeom &g, size_t smem,
+                                 cudaStream_t s) {
+    auto kern = layer_stencil_hwc_kernel<D, C>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    dim3 grid(ceil_div(g.W, kHTW), ceil_div(g.H, kHTH), B);
+    kern<<<grid, kHWX * kHWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), g, dl);
+    SKC_LAUNCH_CHECK("layer_stencil_hwc_kernel");
+    return SKC_OK;
+}
+
+template <int C>
+static int launch_stencil_hwc_c(const void *in, void *out, int B, int D, const DenseList &dl, const LGeom &g,
+                                size_t smem, cudaStream_t s) {
+    switch (D) {
+        case 3: return launch_stencil_hwc_dc<3, C>(in, out, B, dl, g, smem, s);
+        case 5: return launch_stencil_hwc_dc<5, C>(in, out, B, dl, g, smem, s);
+        case 7: return launch_stencil_hwc_dc<7, C>(in, out, B, dl, g, smem, s);
+        default: return launch_stencil_hwc_dc<9, C>(in, out, B, dl, g, smem, s);
+    }
+}
+
+static int launch_stencil_hwc(const void *in, void *out, int B, int D, int C, const DenseList &dl, const LGeom &g,
+                              size_t smem, cudaStream_t s) {
+    return C == 3 ? launch_stencil_hwc_c<3>(in, out, B, D, dl, g, smem, s)
+                  : launch_stencil_hwc_c<1>(in, out, B, D, dl, g, smem, s);
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int S,
                         int boundary, cudaStream_t s, int *rc) {
@@ -566,6 +668,19 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
         }
     dl.D = D;
     for (int e = 0; e < kMaxDense * kMaxDense; ++e) dl.k[e] = e < D * D ? (float)k[e] : 0.f;
+    if constexpr (!IN_PL && OUT_PL && std::is_same<TI, float>::value) {
+        if (C == 3 || C == 1) {
+            LGeom h = make_geom(H, W, C, boundary, 0, kHTW, kHTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
+                                pl.dy_min + D - 1);
+            h.pitch |= 1;   // odd pixel pitch: conflict-free strided windows
+            dl.col_shift = pl.dx_min - h.dx0;
+            const size_t smem = (size_t)h.rows * h.pitch * C * sizeof(float);
+            if (smem <= (size_t)kMaxSmem) {
+                *rc = launch_stencil_hwc(in, out, B, D, C, dl, h, smem, s);
+                return true;
+            }
+        }
+    }
     LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenTH, pl.dx_min, pl.dx_min + D - 1,
                         pl.dy_min, pl.dy_min + D - 1);
     dl.col_shift = pl.dx_min - g.dx0;

@@ -26,6 +26,7 @@ __all__ = [
     "apply_sparse_layer",
     "apply_complex",
     "apply_complex_batch",
+    "dense_convolve",
     "synthesize_ir",
     "synthesize_ir_batch",
     "required_canvas",
@@ -247,6 +248,21 @@ def apply_complex_batch(imgs, cpx: KernelComplex, boundary: str = "zero", out=No
             out.copy_(res.view(out.shape))
         return out
     return im.restore(res)
+
+
+def dense_convolve(img, kernel: DenseKernel, boundary: str = "zero"):
+    """Dense M x M convolution (engine.py:139-157): out[y,x] = sum_{j,i}
+    img[y-j, x-i] K[c+j, c+i].  Runs as one sparse layer of integer taps
+    (offset (-i, -j), weight K[c+j, c+i], zero entries dropped) through the
+    same device kernels (dense-stencil path for M <= 9)."""
+    w = np.asarray(kernel.weights, dtype=np.float64)
+    r = kernel.radius
+    jj, ii = np.nonzero(w)
+    if jj.size == 0:
+        im = Image(img)
+        return im.restore(im.empty_like().zero_())
+    off = np.stack([-(ii - r), -(jj - r)], axis=1).astype(np.float64)
+    return apply_sparse_layer(img, SparseLayer(off, w[jj, ii]), boundary)
 
 
 def required_canvas(cpx: KernelComplex) -> int:

@@ -320,7 +320,39 @@ def gen_pst():
                         energies=e, trace=res.trace, best=np.float64(res.best_energy))
 
 
+def gen_next():
+    """2-D grid SV and the dense convolution oracle."""
+    rng = np.random.default_rng(1007)
+    layout = (3, 4)
+    base = rand_complex(rng, layout, 2.0)
+    rows = []
+    for iu in range(2):
+        row = []
+        for iv in range(3):
+            layers = []
+            for lay in base.layers:
+                off = f32(lay.offsets * (0.6 + 0.5 * iu + 0.3 * iv) + rng.uniform(-0.2, 0.2, lay.offsets.shape))
+                w = lay.weights * rng.uniform(0.8, 1.2, lay.weights.shape)
+                layers.append(sk.SparseLayer(off, f32(w / w.sum())))
+            row.append(sk.KernelComplex(tuple(layers)))
+        rows.append(tuple(row))
+    grid = svfilter.FilterBasisGrid(np.array([0.0, 1.0]), np.array([0.0, 0.5, 1.0]), tuple(rows))
+    img = f32(rng.uniform(size=(23, 27)))
+    pm2 = f32(np.stack([rng.uniform(-0.2, 1.2, (23, 27)), rng.uniform(-0.2, 1.2, (23, 27))], axis=2))
+    out = svfilter.sv_filter_grid(img, grid, pm2)
+    stack = np.stack([np.stack([stacked(sk.FilterBasis(grid.params_v, rows[iu]))[iv] for iv in range(3)])
+                      for iu in range(2)])
+    k7 = sk.DenseKernel(f32(rng.uniform(-1, 1, (7, 7))))
+    k21 = sk.DenseKernel(f32(rng.uniform(0, 1, (21, 21))))
+    imgc = f32(rng.uniform(size=(30, 26, 3)))
+    np.savez_compressed(OUT / "next.npz", grid_img=img, grid_pm2=pm2, grid_pu=grid.params_u, grid_pv=grid.params_v,
+                        grid_stack=stack, grid_layout=np.array(layout), grid_out=out,
+                        k7=k7.weights, k21=k21.weights, dc_img=imgc, dc7=sk.dense_convolve(imgc, k7),
+                        dc21=sk.dense_convolve(imgc, k21))
+
+
 if __name__ == "__main__":
+    gen_next()
     gen_pst()
     gen_init()
     gen_engine()

@@ -183,3 +183,34 @@ def test_pst_energies_and_short_run(skc, golden):
     # same seeded proposal sequence: the first iterations track the reference
     assert np.allclose(res.trace[:3, 1:], g["trace"][:3, 1:], rtol=1e-4)
     assert res.best_energy <= g["trace"][0, 1] + 1e-6
+
+
+def test_next_rows_grid_sv_and_dense_convolve(skc, golden):
+    """2-D grid SV (sv_filter_grid) and the dense oracle on device."""
+    g = golden("next")
+    st = g["grid_stack"]          # (Mu, Mv, L, N, 3)
+    layout = g["grid_layout"].tolist()
+    rows = []
+    for iu in range(st.shape[0]):
+        rows.append(tuple(skc.KernelComplex(tuple(skc.SparseLayer(st[iu, iv, l, :n, :2], st[iu, iv, l, :n, 2])
+                                                  for l, n in enumerate(layout)))
+                          for iv in range(st.shape[1])))
+    grid = skc.FilterBasisGrid(g["grid_pu"], g["grid_pv"], tuple(rows))
+    out = skc.sv_filter_grid(g["grid_img"], grid, g["grid_pm2"])
+    assert normwise(out, g["grid_out"]) < TOL32
+    assert normwise(skc.dense_convolve(g["dc_img"], skc.DenseKernel(g["k7"])), g["dc7"]) < TOL32
+    assert normwise(skc.dense_convolve(g["dc_img"], skc.DenseKernel(g["k21"])), g["dc21"]) < TOL32
+
+
+def test_build_basis_and_json_roundtrip(skc, tmp_path):
+    basis = skc.build_basis(lambda p: skc.gaussian_kernel(float(p)), [1.0, 1.5], (4, 4),
+                            cfg=skc.TrainConfig(steps=40), init=skc.InitStrategy("ss-ir", seed=0))
+    assert basis.size == 2
+    for f in basis.filters:
+        assert abs(skc.synthesize_ir(f).weights.sum() - 1.0) < 1e-5
+    p = tmp_path / "basis.json"
+    skc.save_basis(basis, p)
+    back = skc.load_basis(p)
+    for fa, fb in zip(basis.filters, back.filters):
+        for la, lb in zip(fa.layers, fb.layers):
+            assert np.array_equal(la.offsets, lb.offsets) and np.array_equal(la.weights, lb.weights)
