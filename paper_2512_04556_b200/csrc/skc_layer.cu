@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -416,6 +417,98 @@ __global__ void __launch_bounds__(kHWX *kHWY * 32)
     }
 }
 
+// Row-rolled dense stencil for planar fp32 inputs (large D): each thread owns a
+// KR=3 x 8 block; a runtime loop walks the window rows in groups of KR, and
+// input row r feeds output row i through stencil row r - i, the table being
+// zero-padded above and below so every (r, i) pair is an unconditional FFMA.
+// Keeps the unrolled body at KR*KR*D*8 FFMAs (instruction-cache resident,
+// unlike the fully unrolled (KR+D-1)-row body for D = 9) and uses an odd row
+// pitch, which makes the per-lane LDS.32 window reads conflict-free
+// (3 * pitch odd -> 8 lane rows hit 8 distinct banks mod 8).
+constexpr int kRollKR = 3, kRlWX = 4, kRlWY = 2;    // 256 threads, tile 128 x 48
+constexpr int kRlTW = kRlWX * 32, kRlTH = kRlWY * 8 * kRollKR;
+constexpr int kRollRows = kMaxDense + 3 * kRollKR;  // padded stencil rows
+
+struct RollList {
+    float k[kRollRows * kMaxDense];  // row (a + KR - 1) holds K[a][.], zero outside 0 <= a < D
+    int D;
+    int col_shift;
+};
+
+__host__ __device__ constexpr int roll_rows_padded(int D) {
+    return ((D + kRollKR - 1 + kRollKR - 1) / kRollKR) * kRollKR;
+}
+
+// Planar fp32 plane into s[rows][pitch] with 4-byte cp.async (any pitch parity).
+__device__ __forceinline__ void load_plane4(float *s, const float *__restrict__ frame, const LGeom &g, int c,
+                                            int gx0, int gy0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool clamp = g.boundary == SKC_CLAMP;
+    const int H = g.H, W = g.W;
+    const float *plane = frame + (long long)c * H * W;
+    for (int r = warp; r < g.rows; r += nw) {
+        int gy = gy0 + r;
+        const bool rowin = clamp || (gy >= 0 && gy < H);
+        gy = min(max(gy, 0), H - 1);
+        const float *src = plane + (long long)gy * W;
+        float *dst = s + r * g.pitch;
+#pragma unroll 4
+        for (int col = lane; col < g.pitch; col += 32) {
+            const int gx = gx0 + col;
+            const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+            cp_async4(dst + col, src + min(max(gx, 0), W - 1), ok);
+        }
+    }
+    cp_async_wait_all();
+}
+
+template <int D, typename TO, bool OUT_PL>
+__global__ void __launch_bounds__(kRlWX *kRlWY * 32, 2)
+    layer_stencil_roll_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                              const __grid_constant__ RollList rl) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kRollKR, RP = roll_rows_padded(D);
+    const int C = g.C;
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = (blockIdx.x / C) * kRlTW, ty0 = blockIdx.y * kRlTH;
+    load_plane4(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kRlWX, wy = warp / kRlWX;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    const int pitch = g.pitch;
+    const float *pc = smem + row0 * pitch + col0 + rl.col_shift;
+
+    float acc[KR][8];
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 1
+    for (int r0 = 0; r0 < RP; r0 += KR) {
+#pragma unroll
+        for (int u = 0; u < KR; ++u) {
+            const float *q = pc + (r0 + u) * pitch;
+            float w[8 + D - 1];
+#pragma unroll
+            for (int j = 0; j < 8 + D - 1; ++j) w[j] = q[j];
+#pragma unroll
+            for (int i = 0; i < KR; ++i) {
+                const float *kr = rl.k + (r0 + u - i + KR - 1) * D;
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    const float k = kr[bb];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
+                }
+            }
+        }
+    }
+    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
 // ------------------------------------------------ direct (huge halo) path ---
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(256)
@@ -623,6 +716,28 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
     return SKC_OK;
 }
 
+template <int D, typename TO, bool OUT_PL>
+static int launch_stencil_roll_d(const void *in, void *out, int B, int C, const RollList &rl, const LGeom &g,
+                                 cudaStream_t s) {
+    auto kern = layer_stencil_roll_kernel<D, TO, OUT_PL>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    dim3 grid(ceil_div(g.W, kRlTW) * C, ceil_div(g.H, kRlTH), B);
+    kern<<<grid, kRlWX * kRlWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<TO *>(out), g, rl);
+    SKC_LAUNCH_CHECK("layer_stencil_roll_kernel");
+    return SKC_OK;
+}
+
+// SKC_STENCIL_ROLL=0 keeps the fully unrolled stencil for planar inputs.
+static bool roll_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_STENCIL_ROLL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 template <int D, int C>
 static int launch_stencil_hwc_dc(const void *in, void *out, int B, const DenseList &dl, const LGeom &g, size_t smem,
                                  cudaStream_t s) {
@@ -679,6 +794,23 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
                 *rc = launch_stencil_hwc(in, out, B, D, C, dl, h, smem, s);
                 return true;
             }
+        }
+    }
+    if constexpr (IN_PL) {
+        if (D >= 7 && roll_enabled()) {
+            LGeom r = make_geom(H, W, C, boundary, 0, kRlTW, kRlTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
+                                pl.dy_min + D - 1);
+            r.pitch |= 1;                                            // odd pitch: conflict-free LDS.32
+            r.rows = kRlTH - kRollKR + (D == 7 ? roll_rows_padded(7) : roll_rows_padded(9));
+            RollList rl;
+            std::memset(&rl, 0, sizeof(rl));
+            rl.D = D;
+            rl.col_shift = pl.dx_min - r.dx0;
+            for (int a = 0; a < D; ++a)
+                for (int bb = 0; bb < D; ++bb) rl.k[(a + kRollKR - 1) * D + bb] = (float)k[a * D + bb];
+            *rc = D == 7 ? launch_stencil_roll_d<7, TO, OUT_PL>(in, out, B, C, rl, r, s)
+                         : launch_stencil_roll_d<9, TO, OUT_PL>(in, out, B, C, rl, r, s);
+            return true;
         }
     }
     LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenTH, pl.dx_min, pl.dx_min + D - 1,

@@ -233,6 +233,43 @@ def test_dense_and_tap_paths_agree(skc, orc):
             assert normwise(dense_out, taps_out) < 2e-6
 
 
+def test_rolled_stencil_inner_layers(skc, orc):
+    """Inner (planar) layers with D = 7 / 9 footprints run the row-rolled
+    stencil; SKC_STENCIL_ROLL=0 forces the fully unrolled one.  Both match the
+    oracle on ragged sizes and both boundaries."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    rng = np.random.default_rng(77)
+    layers = []
+    for reach, n in ((1.9, 16), (3.9, 32), (2.9, 24), (3.9, 40)):   # D = 5, 9, 7, 9
+        off = rng.uniform(-reach, reach, (n, 2))
+        w = rng.random(n)
+        layers.append(skc.SparseLayer(off, w / w.sum()))
+    cpx = skc.KernelComplex(layers)
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc;"
+            "d = np.load(sys.argv[1], allow_pickle=True); L = int(d['L']);"
+            "cpx = skc.KernelComplex([skc.SparseLayer(d[f'o{i}'], d[f'w{i}']) for i in range(L)]);"
+            "np.save(sys.argv[2], skc.apply_complex(d['img'], cpx, sys.argv[3]))")
+    with tempfile.TemporaryDirectory() as td:
+        for h, w in ((97, 131), (200, 333), (49, 50)):
+            img = rng.random((h, w, 3)).astype(np.float32)
+            for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                ref = orc.apply_complex(img.astype(np.float64), [(l.offsets, l.weights) for l in layers], oid)
+                ours = skc.apply_complex(img, cpx, mode)
+                assert normwise(ours, ref) < TOL32
+                np.savez(f"{td}/in.npz", img=img, L=len(layers),
+                         **{f"o{i}": l.offsets for i, l in enumerate(layers)},
+                         **{f"w{i}": l.weights for i, l in enumerate(layers)})
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
+                               env=dict(os.environ, SKC_STENCIL_ROLL="0"), cwd=root)
+                assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6
+
+
 def test_chain_io_policies_agree(skc):
     """SKC_CHAIN_IO 0/1/2 (direct HWC I/O vs relayout passes) give identical chains."""
     import os
