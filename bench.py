@@ -177,17 +177,19 @@ class Chain:
         self.bufs = [torch.empty(npx, dtype=torch.float32, device=dev) for _ in range(2)]
         self.out = torch.empty_like(frames)
         self.taps = [np.ascontiguousarray(l.taps()) for l in self.cpx.layers]
-        pol = int(os.environ.get("SKC_CHAIN_IO", "-1"))
-        if pol < 0:   # the library default (skc_layer.cu chain_policy)
-            pol = 1 if self.storage == torch.float16 else 2
-        self.policy = pol
         from paper_2512_04556_b200 import _native as nat
         self.all_taps = np.ascontiguousarray(self.cpx.taps())
         lay = np.ascontiguousarray(self.cpx.layout, dtype=np.int32)
         self.fused = bool(nat.lib().skc_chain_is_fused(nat.dbl(self.all_taps), nat.ints(lay), lay.size,
                                                         self.h, self.w, self.c,
                                                         1 if self.storage == torch.float16 else 0))
-        self.launches_per_step = 1 if self.fused else len(self.taps) + (2 if pol == 1 else 1 if pol == 2 else 0)
+        io = nat.lib().skc_chain_relayouts(nat.dbl(self.all_taps), nat.ints(lay), lay.size, self.h, self.w, self.c,
+                                           1 if self.storage == torch.float16 else 0,
+                                           0 if self.boundary == "zero" else 1)
+        if io < 0:
+            raise RuntimeError(nat.last_error())
+        self.pre, self.post = bool(io & 1), bool(io & 2)   # the passes skc_chain_fwd runs
+        self.launches_per_step = 1 if self.fused else len(self.taps) + int(self.pre) + int(self.post)
         self.units_per_step = self.nf * self.h * self.w
         esz = 2 if self.storage == torch.float16 else 4
         # algorithmic HBM bytes per launch: image in + out in their storage dtypes
@@ -233,12 +235,11 @@ class Chain:
             if events is not None:
                 events[0][1].record(stream)
             return
-        pol = self.policy
         seq = []
-        if pol == 1:
+        if self.pre:
             seq.append(("relayout", None))
         seq += [("layer", t) for t in self.taps]
-        if pol in (1, 2):
+        if self.post:
             seq.append(("relayout", None))
         bnd = 0 if self.boundary == "zero" else 1
         lay_in = nat.SKC_HWC

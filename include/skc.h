@@ -92,6 +92,13 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
 int skc_chain_is_fused(const double *taps, const int *layout, int L, int H, int W, int C,
                        int out_dtype);
 
+/* The I/O passes skc_chain_fwd brackets a (non-fused) chain with: bit 0 set =
+ * an HWC -> planar relayout before the first layer, bit 1 set = a planar ->
+ * HWC relayout after the last layer (clear when the last layer writes HWC
+ * itself through the cluster epilogue).  Negative on bad arguments. */
+int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int W, int C,
+                        int in_dtype, int boundary);
+
 /* Layout/dtype conversion HWC <-> planar fp32 (the chain's bracketing passes). */
 int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
                  int out_layout, int B, int H, int W, int C, void *stream);

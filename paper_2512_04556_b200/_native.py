@@ -28,7 +28,7 @@ FIT_HDR = 8
 
 # Symbols declared in include/skc.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused",
+    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts",
     "skc_chain_fwd",
     "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step",
@@ -77,6 +77,7 @@ def _declare(lib):
     lib.skc_layer_fwd_ex.argtypes = [_vp, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _dp, _i, _i, _vp]
     lib.skc_relayout.argtypes = [_vp, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _vp]
     lib.skc_chain_is_fused.argtypes = [_dp, _ip, _i, _i, _i, _i, _i]
+    lib.skc_chain_relayouts.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i]
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,
                                _vp]
@@ -107,7 +108,11 @@ def load_library():
     except OSError as exc:
         _load_error = str(exc)
         raise NativeUnavailable(_load_error) from exc
-    _declare(lib)
+    try:
+        _declare(lib)
+    except AttributeError as exc:
+        _load_error = f"{LIB_PATH} is stale ({exc}); rebuild with __graft_entry__.build()"
+        raise NativeUnavailable(_load_error) from exc
     _lib = lib
     return lib
 

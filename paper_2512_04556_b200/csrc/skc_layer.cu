@@ -25,6 +25,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "skc_tile.cuh"
 
 namespace skc {
@@ -79,6 +81,12 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             gy = min(max(gy, 0), H - 1);
             const float *src = plane + (long long)gy * W;
             float *dst = s + r * g.pitch;
+            if (pairs_ok && rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
+                const float *sx = src + gx0;
+#pragma unroll 4
+                for (int col = 2 * lane; col < g.pitch; col += 64) cp_async8(dst + col, sx + col, true);
+                continue;
+            }
             for (int p = lane; 2 * p < g.pitch; p += 32) {
                 const int col = 2 * p;
                 const int gx = gx0 + col;
@@ -103,6 +111,12 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             gy = min(max(gy, 0), H - 1);
             const float *src = img + (long long)gy * W * C + c;
             float *dst = s + r * g.pitch;
+            if (rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
+                const float *sx = src + (long long)gx0 * C;
+#pragma unroll 4
+                for (int col = lane; col < g.pitch; col += 32) cp_async4(dst + col, sx + col * C, true);
+                continue;
+            }
 #pragma unroll 4
             for (int col = lane; col < g.pitch; col += 32) {
                 const int gx = gx0 + col;
@@ -134,6 +148,29 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             }
         }
     }
+}
+
+// Planar fp32 plane into s[rows][pitch] with 4-byte cp.async (any pitch parity).
+__device__ __forceinline__ void load_plane4(float *s, const float *__restrict__ frame, const LGeom &g, int c,
+                                            int gx0, int gy0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool clamp = g.boundary == SKC_CLAMP;
+    const int H = g.H, W = g.W;
+    const float *plane = frame + (long long)c * H * W;
+    for (int r = warp; r < g.rows; r += nw) {
+        int gy = gy0 + r;
+        const bool rowin = clamp || (gy >= 0 && gy < H);
+        gy = min(max(gy, 0), H - 1);
+        const float *src = plane + (long long)gy * W;
+        float *dst = s + r * g.pitch;
+#pragma unroll 4
+        for (int col = lane; col < g.pitch; col += 32) {
+            const int gx = gx0 + col;
+            const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+            cp_async4(dst + col, src + min(max(gx, 0), W - 1), ok);
+        }
+    }
+    cp_async_wait_all();
 }
 
 // Store a KR x 8 block of one channel.
@@ -242,6 +279,85 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
+// Last layer of a chain with an HWC output: the C channel CTAs of one tile
+// form a thread-block cluster (dims C x 1 x 1; the grid is channel-fastest so
+// cluster rank == channel).  After the tap loop each CTA stages its KR x 8
+// blocks in its own (now dead) input tile, the cluster synchronises, and CTA q
+// writes rows q, q + C, ... of the tile as contiguous interleaved HWC runs,
+// reading the other channels from its peers' shared memory (DSMEM).  This
+// replaces the planar store + relayout pass (one full read + write of the
+// image) with coalesced HWC stores.
+constexpr int kStageP = kTTW + 4;  // staging pitch: STS.128 conflict-free (KR*33 odd)
+
+template <int KR, typename TO, int C>
+__global__ void __launch_bounds__(kTWX *kTWY * 32)
+    layer_tap_cl_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                        const __grid_constant__ TapList tl) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) float smem[];
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const long long fs = (long long)g.H * g.W * C;
+    constexpr int TH = kTWY * 8 * KR;
+    const int tx0 = (blockIdx.x / C) * kTTW, ty0 = blockIdx.y * TH;
+    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * KR + ly * KR;
+    {
+        const float *base = smem + row0 * g.pitch + col0;
+        float acc[KR][8];
+#pragma unroll
+        for (int r = 0; r < KR; ++r)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+#pragma unroll 1
+        for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+#pragma unroll 1
+        for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+        __syncthreads();  // every warp is done with the input tile
+#pragma unroll
+        for (int r = 0; r < KR; ++r) {
+            float4 *d = reinterpret_cast<float4 *>(smem + (row0 + r) * kStageP + col0);
+            d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+            d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
+        }
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int q = (int)cl.block_rank();
+    const int nx = min(kTTW, g.W - tx0), nrows = min(TH, g.H - ty0);
+    const int ne = nx * C;                                    // floats per HWC row run
+    const int mine = nrows > q ? (nrows - q + C - 1) / C : 0;  // rows q, q + C, ...
+    const int total = mine * ne;
+    TO *frame = out + b * fs;
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < total; i0 += U * kTWX * kTWY * 32) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * kTWX * kTWY * 32;
+            if (i < total) {
+                const int k = i / ne, e = i - k * ne;
+                const int x = e / C, ch = e - x * C;
+                const float *src = cl.map_shared_rank(smem + (q + C * k) * kStageP + x, ch);
+                v[u] = *src;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * kTWX * kTWY * 32;
+            if (i < total) {
+                const int k = i / ne, e = i - k * ne;
+                IO<TO>::st(frame + ((long long)(ty0 + q + C * k) * g.W + tx0) * C + e, v[u]);
+            }
+        }
+    }
+    cl.sync();  // peers may still be reading this CTA's stage
+}
+
 // Persistent, double-buffered variant for fp32 planar inputs: each CTA walks
 // tiles blockIdx.x, +gridDim.x, ... and issues the cp.async loads of its next
 // tile before computing the current one, so the halo-tile transfer of
@@ -299,17 +415,22 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
 constexpr int kDenKR = 5, kDenWX = 4, kDenWY = 2;  // 256 threads, tile 128 x 80
 constexpr int kDenTW = kDenWX * 32, kDenTH = kDenWY * 8 * kDenKR;
 
-template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+// KR = 3 runs with an odd pitch (planar rows staged with 4-byte cp.async):
+// 3 * pitch odd makes the per-lane LDS.32 window reads conflict-free and the
+// unrolled body is 3/5 the size.
+template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     layer_stencil_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
                          const __grid_constant__ DenseList dl) {
     extern __shared__ __align__(16) float smem[];
-    constexpr int KR = kDenKR;
     const int C = g.C;
     const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * kDenTH;
-    load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * (kDenWY * 8 * KR);
+    if constexpr (IN_PL && KR == 3)
+        load_plane4(smem, reinterpret_cast<const float *>(in) + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    else
+        load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -437,29 +558,6 @@ struct RollList {
 
 __host__ __device__ constexpr int roll_rows_padded(int D) {
     return ((D + kRollKR - 1 + kRollKR - 1) / kRollKR) * kRollKR;
-}
-
-// Planar fp32 plane into s[rows][pitch] with 4-byte cp.async (any pitch parity).
-__device__ __forceinline__ void load_plane4(float *s, const float *__restrict__ frame, const LGeom &g, int c,
-                                            int gx0, int gy0) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const bool clamp = g.boundary == SKC_CLAMP;
-    const int H = g.H, W = g.W;
-    const float *plane = frame + (long long)c * H * W;
-    for (int r = warp; r < g.rows; r += nw) {
-        int gy = gy0 + r;
-        const bool rowin = clamp || (gy >= 0 && gy < H);
-        gy = min(max(gy, 0), H - 1);
-        const float *src = plane + (long long)gy * W;
-        float *dst = s + r * g.pitch;
-#pragma unroll 4
-        for (int col = lane; col < g.pitch; col += 32) {
-            const int gx = gx0 + col;
-            const bool ok = clamp || (rowin && gx >= 0 && gx < W);
-            cp_async4(dst + col, src + min(max(gx, 0), W - 1), ok);
-        }
-    }
-    cp_async_wait_all();
 }
 
 template <int D, typename TO, bool OUT_PL>
@@ -631,6 +729,39 @@ static int tap_pipe_mode() {
     return v;
 }
 
+// SKC_TAP_CLUSTER=0 disables the cluster HWC epilogue (planar + relayout instead).
+static bool tap_cluster_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_TAP_CLUSTER");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+template <int KR, typename TO, int C>
+static int launch_tap_cl(const float *in, TO *out, int B, int H, int W, const LGeom &g, const TapList &tl,
+                         size_t smem, cudaStream_t s) {
+    auto kern = layer_tap_cl_kernel<KR, TO, C>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    constexpr int TH = kTWY * 8 * KR;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
+    cfg.blockDim = dim3(kTWX * kTWY * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SKC_CUDA(cudaLaunchKernelEx(&cfg, kern, in, out, g, tl));
+    SKC_LAUNCH_CHECK("layer_tap_cl_kernel");
+    return SKC_OK;
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_taps(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int t0,
                        int t1, int boundary, int accumulate, cudaStream_t s) {
@@ -667,6 +798,15 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
+    if constexpr (IN_PL && !OUT_PL) {
+        if (!accumulate && (C == 3 || C == 4) && tap_cluster_enabled() && smem <= (size_t)kMaxSmem) {
+            const int rc = C == 3 ? (KR == 7 ? launch_tap_cl<7, TO, 3>(pin, pout, B, H, W, g, tl, smem, s)
+                                             : launch_tap_cl<5, TO, 3>(pin, pout, B, H, W, g, tl, smem, s))
+                                  : (KR == 7 ? launch_tap_cl<7, TO, 4>(pin, pout, B, H, W, g, tl, smem, s)
+                                             : launch_tap_cl<5, TO, 4>(pin, pout, B, H, W, g, tl, smem, s));
+            return rc;
+        }
+    }
     if constexpr (IN_PL) {
         const int mode = tap_pipe_mode();
         if ((mode == 1 || (mode < 0 && tl.n <= 12)) && 2 * smem <= (size_t)kMaxSmem) {
@@ -703,14 +843,14 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     return SKC_OK;
 }
 
-template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int C, const DenseList &dl,
                             const LGeom &g, cudaStream_t s) {
-    auto kern = layer_stencil_kernel<D, TI, TO, IN_PL, OUT_PL>;
+    auto kern = layer_stencil_kernel<D, KR, TI, TO, IN_PL, OUT_PL>;
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
-    dim3 grid(ceil_div(W, kDenTW) * C, ceil_div(H, kDenTH), B);
+    dim3 grid(ceil_div(W, kDenTW) * C, ceil_div(H, kDenWY * 8 * KR), B);
     kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);
     SKC_LAUNCH_CHECK("layer_stencil_kernel");
     return SKC_OK;
@@ -729,11 +869,32 @@ static int launch_stencil_roll_d(const void *in, void *out, int B, int C, const 
     return SKC_OK;
 }
 
-// SKC_STENCIL_ROLL=0 keeps the fully unrolled stencil for planar inputs.
+// SKC_STENCIL_ROLL=1 selects the row-rolled stencil for planar D >= 7 inputs
+// (measured slower than the unrolled one on config 1: 3.79 vs 2.78 ms).
 static bool roll_enabled() {
     static const bool v = [] {
         const char *e = std::getenv("SKC_STENCIL_ROLL");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// SKC_STENCIL_HWC=1 selects the all-channel HWC-input stencil for chain heads
+// (measured slower than the per-channel one on config 1: 2.80 vs 2.09 ms).
+static bool stencil_hwc_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_STENCIL_HWC");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// Rows per thread of the planar stencil: SKC_STENCIL_KR = 3 (odd pitch,
+// conflict-free LDS.32, a smaller unrolled body) or 5 (default).
+static int stencil_kr() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_STENCIL_KR");
+        return e && std::atoi(e) == 3 ? 3 : 5;
     }();
     return v;
 }
@@ -784,7 +945,7 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
     dl.D = D;
     for (int e = 0; e < kMaxDense * kMaxDense; ++e) dl.k[e] = e < D * D ? (float)k[e] : 0.f;
     if constexpr (!IN_PL && OUT_PL && std::is_same<TI, float>::value) {
-        if (C == 3 || C == 1) {
+        if ((C == 3 || C == 1) && stencil_hwc_enabled()) {
             LGeom h = make_geom(H, W, C, boundary, 0, kHTW, kHTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
                                 pl.dy_min + D - 1);
             h.pitch |= 1;   // odd pixel pitch: conflict-free strided windows
@@ -813,14 +974,29 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
             return true;
         }
     }
+    if constexpr (IN_PL && std::is_same<TO, float>::value && OUT_PL) {
+        if (stencil_kr() == 3) {
+            LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenWY * 8 * 3, pl.dx_min, pl.dx_min + D - 1,
+                                pl.dy_min, pl.dy_min + D - 1);
+            g.pitch |= 1;
+            dl.col_shift = pl.dx_min - g.dx0;
+            switch (D) {
+                case 3: *rc = launch_stencil_d<3, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+                case 5: *rc = launch_stencil_d<5, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+                case 7: *rc = launch_stencil_d<7, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+                default: *rc = launch_stencil_d<9, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+            }
+            return true;
+        }
+    }
     LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenTH, pl.dx_min, pl.dx_min + D - 1,
                         pl.dy_min, pl.dy_min + D - 1);
     dl.col_shift = pl.dx_min - g.dx0;
     switch (D) {
-        case 3: *rc = launch_stencil_d<3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-        case 5: *rc = launch_stencil_d<5, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-        case 7: *rc = launch_stencil_d<7, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-        default: *rc = launch_stencil_d<9, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        case 3: *rc = launch_stencil_d<3, kDenKR, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        case 5: *rc = launch_stencil_d<5, kDenKR, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        case 7: *rc = launch_stencil_d<7, kDenKR, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
+        default: *rc = launch_stencil_d<9, kDenKR, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
     }
     return true;
 }
@@ -1032,6 +1208,40 @@ static int chain_policy(int in_dtype) {
     return in_dtype == SKC_F16 ? 1 : 2;
 }
 
+// Would a chain's last layer (planar fp32 in, HWC out) run the cluster tap
+// kernel?  Mirrors the routing of layer_t -> try_stencil -> launch_taps.
+static bool last_layer_direct(int H, int W, int C, const double *taps, int S, int boundary) {
+    if (!tap_cluster_enabled() || (C != 3 && C != 4) || S > kLMaxTaps) return false;
+    const Plan pl = plan_taps(taps, S);
+    if (dense_allowed()) {
+        const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
+        const int D = dense_size_for(std::max(sx, sy));
+        if (D != 0 && D * D < 4 * S) return false;
+    }
+    int dx_min = 1 << 30, dx_max = -(1 << 30), dy_min = 1 << 30, dy_max = -(1 << 30);
+    for (int i = 0; i < S; ++i) {
+        dx_min = std::min(dx_min, pl.ix[i]);
+        dx_max = std::max(dx_max, pl.ix[i] + 1);
+        dy_min = std::min(dy_min, pl.iy[i]);
+        dy_max = std::max(dy_max, pl.iy[i] + 1);
+    }
+    const LGeom g5 = make_geom(H, W, C, boundary, 0, kTTW, kTWY * 8 * 5, dx_min, dx_max, dy_min, dy_max);
+    return (size_t)g5.rows * g5.pitch * sizeof(float) <= (size_t)kMaxSmem;
+}
+
+// The chain's I/O passes (see chain_policy); by default the output relayout
+// is skipped when the last layer runs the cluster HWC epilogue.
+static void chain_io(const double *taps, const int *layout, int L, long long total, int H, int W, int C,
+                     int in_dtype, int boundary, bool *pre, bool *post) {
+    const int pol = chain_policy(in_dtype);
+    *pre = pol == 1;
+    *post = pol == 1 || pol == 2;
+    if (*post && chain_policy_env() < 0) {
+        const double *lt = taps + 3 * (total - layout[L - 1]);
+        if (last_layer_direct(H, W, C, lt, layout[L - 1], boundary)) *post = false;
+    }
+}
+
 // HWC output layer with the long-layer fp16 fallback (fp32 temporary + convert).
 static int last_layer(const void *in, int idt, bool in_pl, void *out, int odt, int B, int H, int W,
                       int C, const double *taps, int S, int boundary, cudaStream_t s) {
@@ -1097,6 +1307,20 @@ int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out
                     (cudaStream_t)stream);
 }
 
+int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int W, int C, int in_dtype,
+                        int boundary) {
+    if (!taps || !layout || L < 1 || H < 1 || W < 1 || C < 1) return fail(SKC_EBADARG, "bad chain arguments");
+    if (L == 1) return 0;
+    long long total = 0;
+    for (int l = 0; l < L; ++l) {
+        if (layout[l] < 1) return fail(SKC_EBADARG, "sparse layer needs at least one sample");
+        total += layout[l];
+    }
+    bool pre, post;
+    chain_io(taps, layout, L, total, H, W, C, in_dtype, boundary, &pre, &post);
+    return (pre ? 1 : 0) | (post ? 2 : 0);
+}
+
 int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
                   int C, const double *taps, const int *layout, int L, int boundary, void *stream) {
     int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
@@ -1114,8 +1338,8 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     if (rc != -1) return rc;
     rc = SKC_OK;
     // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
-    const int pol = chain_policy(in_dtype);
-    const bool pre = pol == 1, post = pol == 1 || pol == 2;
+    bool pre, post;
+    chain_io(taps, layout, L, total, H, W, C, in_dtype, boundary, &pre, &post);
     const size_t n = (size_t)B * H * W * C;
     void *buf[2] = {nullptr, nullptr};
     const int nbuf = (L > 2 || post || pre) ? 2 : 1;

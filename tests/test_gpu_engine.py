@@ -295,6 +295,44 @@ def test_chain_io_policies_agree(skc):
             assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
 
 
+def test_cluster_hwc_epilogue(skc, orc):
+    """A chain whose last layer is a tap layer writes HWC straight from a
+    C-CTA cluster (DSMEM staging) instead of planar + relayout; it must equal
+    the relayout path bit for bit (SKC_TAP_CLUSTER=0) and the oracle, for
+    C = 3 / 4, fp32 / fp16 storage, ragged sizes and both boundaries."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    rng = np.random.default_rng(91)
+    layers = []
+    for reach, n in ((1.5, 8), (6.0, 12), (9.0, 20)):
+        off = rng.uniform(-reach, reach, (n, 2))
+        w = rng.random(n)
+        layers.append(skc.SparseLayer(off, w / w.sum()))
+    cpx = skc.KernelComplex(layers)
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc;"
+            "d = np.load(sys.argv[1]); L = int(d['L']);"
+            "cpx = skc.KernelComplex([skc.SparseLayer(d[f'o{i}'], d[f'w{i}']) for i in range(L)]);"
+            "np.save(sys.argv[2], skc.apply_complex(d['img'], cpx, sys.argv[3]))")
+    with tempfile.TemporaryDirectory() as td:
+        for (h, w, c, dt) in ((131, 257, 3, np.float32), (300, 129, 4, np.float16), (17, 5, 3, np.float32)):
+            img = rng.random((h, w, c)).astype(dt)
+            for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                ours = skc.apply_complex(img, cpx, mode)
+                ref = orc.apply_complex(img.astype(np.float64), [(l.offsets, l.weights) for l in layers], oid)
+                assert normwise(ours, ref) < (TOL32 if dt == np.float32 else 2e-3)
+                np.savez(f"{td}/in.npz", img=img, L=len(layers),
+                         **{f"o{i}": l.offsets for i, l in enumerate(layers)},
+                         **{f"w{i}": l.weights for i, l in enumerate(layers)})
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
+                               env=dict(os.environ, SKC_TAP_CLUSTER="0"), cwd=root)
+                assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy"))
+
+
 def test_fused_chain_matches_oracle_and_unfused(skc, orc):
     """Small-reach chains run as one fused launch (skc_chain_is_fused); check it
     against the oracle on ragged sizes, both boundaries, fp32 and fp16, and
