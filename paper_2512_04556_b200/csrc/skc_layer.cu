@@ -707,8 +707,9 @@ static int set_smem_attr(K kern) {
     return SKC_OK;
 }
 
-// Rows per thread of the tap kernel: SKC_TAP_KR (5 or 7) overrides; default 7
-// when the halo tile of a 7-row block still leaves two CTAs per SM, else 5.
+// Rows per thread of the tap kernel: SKC_TAP_KR (5 or 7) overrides; default 5
+// for layers of <= 16 taps (HBM-bound), else 7 when the halo tile of a 7-row
+// block still leaves two CTAs per SM, else 5.
 static int tap_kr_override() {
     static const int v = [] {
         const char *e = std::getenv("SKC_TAP_KR");
@@ -729,11 +730,14 @@ static int tap_pipe_mode() {
     return v;
 }
 
-// SKC_TAP_CLUSTER=0 disables the cluster HWC epilogue (planar + relayout instead).
+// SKC_TAP_CLUSTER=1 enables the cluster HWC epilogue.  Opt-in: on config 1
+// the clustered last layer took 7.28 ms against 4.39 ms + 0.89 ms for the
+// planar layer + relayout pass (scalar DSMEM gathers and the two cluster
+// barriers cost more than the relayout's extra HBM pass).
 static bool tap_cluster_enabled() {
     static const bool v = [] {
         const char *e = std::getenv("SKC_TAP_CLUSTER");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return v;
 }
@@ -773,7 +777,9 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
         dy_max = std::max(dy_max, pl.iy[i] + 1);
     }
     int KR = tap_kr_override();
-    if (KR != 5 && KR != 7) {
+    if (KR != 5 && KR != 7 && t1 - t0 <= 16) {
+        KR = 5;  // memory-bound layers: smaller tiles, more CTAs in flight (config 3: 2.05 vs 2.17 ms)
+    } else if (KR != 5 && KR != 7) {
         const LGeom g7 = make_geom(H, W, C, boundary, accumulate, kTTW, kTWY * 8 * 7, dx_min, dx_max, dy_min, dy_max);
         KR = ((size_t)g7.rows * g7.pitch * sizeof(float) * 2 <= (size_t)kMaxSmem) ? 7 : 5;
     }

@@ -296,10 +296,11 @@ def test_chain_io_policies_agree(skc):
 
 
 def test_cluster_hwc_epilogue(skc, orc):
-    """A chain whose last layer is a tap layer writes HWC straight from a
-    C-CTA cluster (DSMEM staging) instead of planar + relayout; it must equal
-    the relayout path bit for bit (SKC_TAP_CLUSTER=0) and the oracle, for
-    C = 3 / 4, fp32 / fp16 storage, ragged sizes and both boundaries."""
+    """With SKC_TAP_CLUSTER=1 a chain whose last layer is a tap layer writes
+    HWC straight from a C-CTA cluster (DSMEM staging) instead of planar +
+    relayout; it must equal the default relayout path bit for bit and the
+    oracle, for C = 3 / 4, fp32 / fp16 storage, ragged sizes and both
+    boundaries."""
     import os
     import subprocess
     import sys
@@ -329,7 +330,7 @@ def test_cluster_hwc_epilogue(skc, orc):
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
                 subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
-                               env=dict(os.environ, SKC_TAP_CLUSTER="0"), cwd=root)
+                               env=dict(os.environ, SKC_TAP_CLUSTER="1"), cwd=root)
                 assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy"))
 
 
