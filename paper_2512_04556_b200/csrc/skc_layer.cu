@@ -63,6 +63,43 @@ __device__ __forceinline__ void cp_async8(float *dst, const float *src, bool val
                  "r"(valid ? 8 : 0));
 }
 
+// Interior-row copies with a compile-time chunk count: per lane NCH chunks of
+// E floats at lane stride (E = 2: 8-byte pairs of a planar row; E = 1 with a
+// global element stride `gs`: one channel of an HWC row).  Constant offsets
+// fold into the LDGSTS address fields.
+template <int NCH>
+__device__ __forceinline__ void row_pairs(unsigned sd, const float *sx, int lane, int pitch) {
+#pragma unroll
+    for (int u = 0; u < NCH; ++u)
+        if (u < NCH - 1 || 2 * lane + 64 * u < pitch) cp_async8s(sd + 256 * u, sx + 64 * u);
+}
+template <int NCH>
+__device__ __forceinline__ void row_elems(unsigned sd, const float *sx, int lane, int pitch, int gs) {
+#pragma unroll
+    for (int u = 0; u < NCH; ++u)
+        if (u < NCH - 1 || lane + 32 * u < pitch) cp_async4s(sd + 128 * u, sx + (32 * u) * gs);
+}
+__device__ __forceinline__ void row_pairs_any(unsigned sd, const float *sx, int lane, int pitch) {
+    switch ((pitch + 63) >> 6) {
+        case 1: row_pairs<1>(sd, sx, lane, pitch); break;
+        case 2: row_pairs<2>(sd, sx, lane, pitch); break;
+        case 3: row_pairs<3>(sd, sx, lane, pitch); break;
+        case 4: row_pairs<4>(sd, sx, lane, pitch); break;
+        default:
+            for (int col = 2 * lane; col < pitch; col += 64, sd += 256, sx += 64) cp_async8s(sd, sx);
+    }
+}
+__device__ __forceinline__ void row_elems_any(unsigned sd, const float *sx, int lane, int pitch, int gs) {
+    switch ((pitch + 31) >> 5) {
+        case 3: row_elems<3>(sd, sx, lane, pitch, gs); break;
+        case 4: row_elems<4>(sd, sx, lane, pitch, gs); break;
+        case 5: row_elems<5>(sd, sx, lane, pitch, gs); break;
+        case 6: row_elems<6>(sd, sx, lane, pitch, gs); break;
+        default:
+            for (int col = lane; col < pitch; col += 32, sd += 128, sx += 32 * gs) cp_async4s(sd, sx);
+    }
+}
+
 // One channel plane of the halo tile into s[rows][pitch].  `frame` points at
 // the (H, W, C) HWC frame or the (C, H, W) planar frame.
 template <typename TI, bool PLANAR, bool WAIT = true>
@@ -82,9 +119,8 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             const float *src = plane + (long long)gy * W;
             float *dst = s + r * g.pitch;
             if (pairs_ok && rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
-                const float *sx = src + gx0;
-#pragma unroll 4
-                for (int col = 2 * lane; col < g.pitch; col += 64) cp_async8(dst + col, sx + col, true);
+                row_pairs_any((unsigned)__cvta_generic_to_shared(dst + 2 * lane), src + gx0 + 2 * lane, lane,
+                              g.pitch);
                 continue;
             }
             for (int p = lane; 2 * p < g.pitch; p += 32) {
@@ -112,9 +148,8 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             const float *src = img + (long long)gy * W * C + c;
             float *dst = s + r * g.pitch;
             if (rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
-                const float *sx = src + (long long)gx0 * C;
-#pragma unroll 4
-                for (int col = lane; col < g.pitch; col += 32) cp_async4(dst + col, sx + col * C, true);
+                row_elems_any((unsigned)__cvta_generic_to_shared(dst + lane), src + (long long)(gx0 + lane) * C, lane,
+                              g.pitch, C);
                 continue;
             }
 #pragma unroll 4
@@ -163,6 +198,10 @@ __device__ __forceinline__ void load_plane4(float *s, const float *__restrict__ 
         gy = min(max(gy, 0), H - 1);
         const float *src = plane + (long long)gy * W;
         float *dst = s + r * g.pitch;
+        if (rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
+            row_elems_any((unsigned)__cvta_generic_to_shared(dst + lane), src + gx0 + lane, lane, g.pitch, 1);
+            continue;
+        }
 #pragma unroll 4
         for (int col = lane; col < g.pitch; col += 32) {
             const int gx = gx0 + col;
@@ -538,6 +577,68 @@ __global__ void __launch_bounds__(kHWX *kHWY * 32)
     }
 }
 
+// Stencil-row loop for planar fp32 inputs (D = 7 / 9): each thread owns a
+// 3 x 8 block; a loop over the stencil rows a (unrolled by 3, so the window
+// rows rotate by register renaming) keeps rows a .. a+2 of the input window
+// in registers, loads one new 16-word row per step and issues 3*D*8 FFMAs
+// with the row's weights.  The body is ~11 KB instead of the ~52 KB fully
+// unrolled (KR+D-1)-row body (instruction-fetch stalls), with no padding
+// waste.
+constexpr int kAlKR = 3, kAlWX = 4, kAlWY = 2;       // 256 threads, tile 128 x 48
+constexpr int kAlTW = kAlWX * 32, kAlTH = kAlWY * 8 * kAlKR;
+
+template <int D, typename TO, bool OUT_PL>
+__global__ void __launch_bounds__(kAlWX *kAlWY * 32, 3)
+    layer_stencil_aloop_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                               const __grid_constant__ DenseList dl) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kAlKR, WN = 8 + D - 1;
+    const int C = g.C;
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = (blockIdx.x / C) * kAlTW, ty0 = blockIdx.y * kAlTH;
+    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kAlWX, wy = warp / kAlWX;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    const int pitch = g.pitch;
+    const float *pc = smem + row0 * pitch + col0 + dl.col_shift;
+
+    float acc[KR][8];
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    float w[KR][WN];
+#pragma unroll
+    for (int i = 0; i < KR - 1; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) w[i + 1][j] = pc[i * pitch + j];
+#pragma unroll 3
+    for (int a = 0; a < D; ++a) {
+        // rotate: rows a .. a+KR-1 (renamed away by the unroll)
+#pragma unroll
+        for (int i = 0; i < KR - 1; ++i)
+#pragma unroll
+            for (int j = 0; j < WN; ++j) w[i][j] = w[i + 1][j];
+        const float *q = pc + (a + KR - 1) * pitch;
+#pragma unroll
+        for (int j = 0; j < WN; ++j) w[KR - 1][j] = q[j];
+        const float *kr = dl.k + a * D;
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) {
+            const float k = kr[bb];
+#pragma unroll
+            for (int i = 0; i < KR; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[i][j + bb], acc[i][j]);
+        }
+    }
+    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
 // Row-rolled dense stencil for planar fp32 inputs (large D): each thread owns a
 // KR=3 x 8 block; a runtime loop walks the window rows in groups of KR, and
 // input row r feeds output row i through stencil row r - i, the table being
@@ -875,6 +976,28 @@ static int launch_stencil_roll_d(const void *in, void *out, int B, int C, const 
     return SKC_OK;
 }
 
+template <int D, typename TO, bool OUT_PL>
+static int launch_stencil_aloop_d(const void *in, void *out, int B, int C, const DenseList &dl, const LGeom &g,
+                                  cudaStream_t s) {
+    auto kern = layer_stencil_aloop_kernel<D, TO, OUT_PL>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    dim3 grid(ceil_div(g.W, kAlTW) * C, ceil_div(g.H, kAlTH), B);
+    kern<<<grid, kAlWX * kAlWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<TO *>(out), g, dl);
+    SKC_LAUNCH_CHECK("layer_stencil_aloop_kernel");
+    return SKC_OK;
+}
+
+// SKC_STENCIL_ALOOP=0 keeps the fully unrolled stencil for planar D >= 7.
+static bool aloop_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_STENCIL_ALOOP");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // SKC_STENCIL_ROLL=1 selects the row-rolled stencil for planar D >= 7 inputs
 // (measured slower than the unrolled one on config 1: 3.79 vs 2.78 ms).
 static bool roll_enabled() {
@@ -964,6 +1087,14 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
         }
     }
     if constexpr (IN_PL) {
+        if (D >= 7 && aloop_enabled() && !roll_enabled()) {
+            LGeom a = make_geom(H, W, C, boundary, 0, kAlTW, kAlTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
+                                pl.dy_min + D - 1);
+            dl.col_shift = pl.dx_min - a.dx0;
+            *rc = D == 7 ? launch_stencil_aloop_d<7, TO, OUT_PL>(in, out, B, C, dl, a, s)
+                         : launch_stencil_aloop_d<9, TO, OUT_PL>(in, out, B, C, dl, a, s);
+            return true;
+        }
         if (D >= 7 && roll_enabled()) {
             LGeom r = make_geom(H, W, C, boundary, 0, kRlTW, kRlTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
                                 pl.dy_min + D - 1);

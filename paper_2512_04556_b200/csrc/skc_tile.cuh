@@ -29,6 +29,13 @@ __device__ __forceinline__ void cp_async4(float *dst, const float *src, bool val
                  "r"(valid ? 4 : 0));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+// Variants on a precomputed shared-window address (no per-call cvta), always valid.
+__device__ __forceinline__ void cp_async4s(unsigned saddr, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(src));
+}
+__device__ __forceinline__ void cp_async8s(unsigned saddr, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(src));
+}
 
 template <int C, typename TI>
 __device__ __forceinline__ void load_tile(float *s, const TI *__restrict__ in, int H, int W,

@@ -1,0 +1,9 @@
+# loader rewrite (compile-time chunked interior rows): tests + c0/c1/c3 bench + stencil capture
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_gpu.log
+run() { name=$1; shift; env "$@" python bench.py --no-e2e --no-cpu $BARGS > gpurun_out/b29_$name.json 2> gpurun_out/b29_$name.err; echo "$name rc=$? $(python -c "import json,sys;d=json.loads(open('gpurun_out/b29_$name.json').read().strip().splitlines()[-1]);print(round(d['value'],1), [round(x,3) for x in d['roofline']['per_launch_ms']])")"; }
+BARGS="--config c1"; run c1 SKC_X=0
+BARGS="--config c3"; run c3 SKC_X=0
+BARGS="--config c0"; run c0 SKC_X=0
+BARGS="--config c2"; run c2 SKC_X=0
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"stencil" -c 2 -o gpurun_out/prof29_stencil python bench.py --config c1 --steps 1 --warmup 0 --frames 8 --no-e2e --no-cpu > gpurun_out/ncu29a.log 2>&1; echo ncu_a rc=$?
