@@ -234,9 +234,10 @@ def test_dense_and_tap_paths_agree(skc, orc):
 
 
 def test_rolled_stencil_inner_layers(skc, orc):
-    """Inner (planar) layers with D = 7 / 9 footprints run the row-rolled
-    stencil; SKC_STENCIL_ROLL=0 forces the fully unrolled one.  Both match the
-    oracle on ragged sizes and both boundaries."""
+    """Inner (planar) layers with D = 5 / 7 / 9 footprints: the default fully
+    unrolled stencil and the opt-in variants (SKC_STENCIL_ROLL=1 row-rolled,
+    SKC_STENCIL_ALOOP=1 stencil-row loop, SKC_STENCIL_KR=3 odd pitch) all
+    match the oracle and each other on ragged sizes and both boundaries."""
     import os
     import subprocess
     import sys
@@ -265,9 +266,10 @@ def test_rolled_stencil_inner_layers(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
-                               env=dict(os.environ, SKC_STENCIL_ROLL="0"), cwd=root)
-                assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6
+                for var in ({"SKC_STENCIL_ROLL": "1"}, {"SKC_STENCIL_ALOOP": "1"}, {"SKC_STENCIL_KR": "3"}):
+                    subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
+                                   env=dict(os.environ, **var), cwd=root)
+                    assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6, var
 
 
 def test_chain_io_policies_agree(skc):
