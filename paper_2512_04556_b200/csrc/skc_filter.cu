@@ -115,6 +115,136 @@ __global__ void __launch_bounds__(TR * 64)
     }
 }
 
+// Interleaved-tile variant: the halo tile keeps the image's pixel-interleaved
+// layout in shared memory (pixel stride PS = C, or C + 1 for even C so that
+// neighbouring lanes stay bank-disjoint), so the 2 x 2 corners of all C
+// channels of one tap sit at compile-time offsets {0, PS} x {0, RS} + c from
+// a single per-(tap, pixel) address: 2 integer ops of addressing per
+// tap-pixel instead of ~14 with C separate planes (SASS count).  The floor
+// of the lerped offset uses the round-down add of 1.5 * 2^23 (exact for
+// |o| < 2^22), which yields the integer and the fraction on the FMA pipe.
+template <int C>
+struct SvPix {
+    static constexpr int PS = (C % 2 == 1) ? C : C + 1;
+};
+
+template <int C, typename TI>
+__device__ __forceinline__ void load_tile_il(float *s, const TI *__restrict__ in, int H, int W, int boundary,
+                                             int gx0, int gy0, int pitch, int rows) {
+    constexpr int PS = SvPix<C>::PS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool clamp = boundary == SKC_CLAMP;
+    const int rowlen = pitch * C, rs = pitch * PS;
+    for (int r = warp; r < rows; r += nw) {
+        int gy = gy0 + r;
+        const bool rowin = clamp || (gy >= 0 && gy < H);
+        gy = min(max(gy, 0), H - 1);
+        const TI *src = in + (long long)gy * W * C;
+        float *dst = s + r * rs;
+        const bool interior = rowin && gx0 >= 0 && gx0 + pitch <= W;
+        if constexpr (sizeof(TI) == 4) {
+            const float *sf = reinterpret_cast<const float *>(src);
+            if (interior && PS == C) {
+                const float *sx = sf + (long long)gx0 * C + lane;
+                unsigned sd = (unsigned)__cvta_generic_to_shared(dst + lane);
+#pragma unroll 4
+                for (int e = lane; e < rowlen; e += 32, sd += 128, sx += 32) cp_async4s(sd, sx);
+                continue;
+            }
+#pragma unroll 4
+            for (int e = lane; e < rowlen; e += 32) {
+                const int col = e / C, c = e - col * C;
+                const int gx = gx0 + col;
+                const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                cp_async4(dst + col * PS + c, sf + (long long)min(max(gx, 0), W - 1) * C + c, ok);
+            }
+        } else {
+            for (int e = lane; e < rowlen; e += 32) {
+                const int col = e / C, c = e - col * C;
+                const int gx = gx0 + col;
+                const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                dst[col * PS + c] = ok ? IO<TI>::ld(src + (long long)min(max(gx, 0), W - 1) * C + c) : 0.f;
+            }
+        }
+    }
+    cp_async_wait_all();
+}
+
+template <int C, int TR, typename TI, typename TO>
+__global__ void __launch_bounds__(TR * 64)
+    sv_tile_il_kernel(const TI *__restrict__ in, TO *__restrict__ out, const float *__restrict__ pmap,
+                      const float4 *__restrict__ table, const __grid_constant__ SvParams q) {
+    extern __shared__ float4 smem4[];
+    constexpr int TH = TR * kSvPx, PS = SvPix<C>::PS;
+    const int nrow = q.Mb > 1 ? q.Mb - 1 : 1;
+    float4 *stab = smem4;  // (nrow, n, 2)
+    float *tile = reinterpret_cast<float *>(smem4 + 2 * nrow * q.n);
+    const int tx0 = blockIdx.x * kSvTW, ty0 = blockIdx.y * TH;
+    for (int i = threadIdx.x; i < 2 * nrow * q.n; i += blockDim.x) stab[i] = table[i];
+    load_tile_il<C, TI>(tile, in, q.H, q.W, q.boundary, tx0 + q.dx0, ty0 + q.dy0, q.pitch, q.rows);
+    __syncthreads();
+
+    const int tx = threadIdx.x & (kSvTW - 1), ty = threadIdx.x / kSvTW;
+    const int rs = q.pitch * PS;
+    const int gx = tx0 + tx;
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    constexpr int kMagicBits = 0x4B400000;
+    int e0[kSvPx], pb[kSvPx];
+    float tt[kSvPx];
+    float acc[kSvPx][C];
+#pragma unroll
+    for (int k = 0; k < kSvPx; ++k) {
+        const int gy = ty0 + ty + TR * k;
+        float p = 0.f;
+        if (gy < q.H && gx < q.W) p = __ldg(pmap + (long long)gy * q.W + gx);
+        int k0, k1;
+        bracket(p, q, k0, k1, tt[k]);
+        e0[k] = 2 * k0 * q.n;
+        pb[k] = (ty + TR * k - q.dy0) * rs + (tx - q.dx0) * PS;  // word offset of the pixel's (0, 0) texel
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] = 0.f;
+    }
+#pragma unroll 1
+    for (int i = 0; i < q.n; ++i) {
+#pragma unroll
+        for (int k = 0; k < kSvPx; ++k) {
+            const float4 a = stab[e0[k] + 2 * i];
+            const float4 d = stab[e0[k] + 2 * i + 1];
+            const float t = tt[k];
+            const float ox = fmaf(t, d.x, a.x);  // _fastpath.py:109-111
+            const float oy = fmaf(t, d.y, a.y);
+            const float w = fmaf(t, d.z, a.z);
+            const float bx = __fadd_rd(ox, kMagic), by = __fadd_rd(oy, kMagic);  // kMagic + floor(o)
+            const float fx = ox - (bx - kMagic), fy = oy - (by - kMagic);
+            const float wb = w * fy, wa = w - wb;
+            const float c10 = wa * fx, c00 = wa - c10, c11 = wb * fx, c01 = wb - c11;
+            int iy = __float_as_int(by) - kMagicBits, ix = __float_as_int(bx) - kMagicBits;
+            // opaque to the optimiser: otherwise the magic bias is re-associated into
+            // a separate add in front of every shared load (no room in the LDS offset)
+            asm("" : "+r"(iy), "+r"(ix));
+            const float *sp = tile + (pb[k] + iy * rs + ix * PS);
+            const float *sq = sp + rs;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                float v = acc[k][c];
+                v = fmaf(c00, sp[c], v);
+                v = fmaf(c10, sp[PS + c], v);
+                v = fmaf(c01, sq[c], v);
+                v = fmaf(c11, sq[PS + c], v);
+                acc[k][c] = v;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kSvPx; ++k) {
+        const int gy = ty0 + ty + TR * k;
+        if (gy >= q.H || gx >= q.W) continue;
+        TO *o = out + ((long long)gy * q.W + gx) * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) IO<TO>::st(o + c, acc[k][c]);
+    }
+}
+
 template <int C, typename TI, typename TO>
 __global__ void __launch_bounds__(256)
     sv_direct_kernel(const TI *__restrict__ in, TO *__restrict__ out, const float *__restrict__ pmap,
@@ -156,11 +286,35 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// SKC_SV_PLANAR=1 keeps the channel-planar SV tile (the interleaved one is the default).
+static bool sv_interleaved() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_SV_PLANAR");
+        return !(e && e[0] == '1');
+    }();
+    return v;
+}
+
 template <int C, int TR, typename TI, typename TO>
 static int launch_sv_tile(const void *in, void *out, const float *pmap, const float4 *table, SvParams q,
                           int span_y, cudaStream_t s) {
     q.rows = TR * kSvPx + span_y;
     const int nrow = q.Mb > 1 ? q.Mb - 1 : 1;
+    if (sv_interleaved()) {
+        const size_t smem =
+            (size_t)2 * nrow * q.n * sizeof(float4) + (size_t)SvPix<C>::PS * q.rows * q.pitch * 4;
+        if (smem > (size_t)kMaxSmem) return -1;
+        auto kern = sv_tile_il_kernel<C, TR, TI, TO>;
+        static bool il_attr = false;
+        if (!il_attr) {
+            SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+            il_attr = true;
+        }
+        dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, TR * kSvPx));
+        kern<<<grid, TR * 64, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), pmap, table, q);
+        SKC_LAUNCH_CHECK("sv_tile_il_kernel");
+        return SKC_OK;
+    }
     const size_t smem = (size_t)2 * nrow * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
     if (smem > (size_t)kMaxSmem) return -1;
     auto kern = sv_tile_kernel<C, TR, TI, TO>;

@@ -185,7 +185,7 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
             tile_rows_any<1>((unsigned)__cvta_generic_to_shared(s + warp * g.pitch + lane),
                              img + ((long long)(gy0 + warp) * W + gx0 + lane) * C + c, lane, g.pitch, warp, g.rows,
                              nw, 4u * nw * g.pitch, (long long)nw * W * C, C)) {
-            cp_async_wait_all();
+            if (WAIT) if (WAIT) cp_async_wait_all();
             return;
         }
         for (int r = warp; r < g.rows; r += nw) {
@@ -508,6 +508,35 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
 constexpr int kDenKR = 5, kDenWX = 4, kDenWY = 2;  // 256 threads, tile 128 x 80
 constexpr int kDenTW = kDenWX * 32, kDenTH = kDenWY * 8 * kDenKR;
 
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_one_() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// acc = the D x D stencil over a KR x 8 block whose window starts at pc.
+template <int D, int KR>
+__device__ __forceinline__ void stencil_block(float (&acc)[KR][8], const float *pc, int pitch, const DenseList &dl) {
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int r = 0; r < KR + D - 1; ++r) {
+        float w[8 + D - 1];
+#pragma unroll
+        for (int j = 0; j < 8 + D - 1; ++j) w[j] = pc[r * pitch + j];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int i = r - a;
+            if (i < 0 || i >= KR) continue;
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                const float k = dl.k[a * D + bb];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
+            }
+        }
+    }
+}
+
 // KR = 3 runs with an odd pitch (planar rows staged with 4-byte cp.async):
 // 3 * pitch odd makes the per-lane LDS.32 window reads conflict-free and the
 // unrolled body is 3/5 the size.
@@ -534,28 +563,49 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     const int pitch = g.pitch;
 
     float acc[KR][8];
-#pragma unroll
-    for (int i = 0; i < KR; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll
-    for (int r = 0; r < KR + D - 1; ++r) {
-        float w[8 + D - 1];
-#pragma unroll
-        for (int j = 0; j < 8 + D - 1; ++j) w[j] = pc[r * pitch + j];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const int i = r - a;
-            if (i < 0 || i >= KR) continue;
-#pragma unroll
-            for (int bb = 0; bb < D; ++bb) {
-                const float k = dl.k[a * D + bb];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
-            }
-        }
-    }
+    stencil_block<D, KR>(acc, pc, pitch, dl);
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
+}
+
+// Persistent, double-buffered stencil: each CTA walks tiles blockIdx.x,
+// +gridDim.x, ... and issues the cp.async loads of its next tile before
+// computing the current one, so tile loads overlap the FFMA stream instead of
+// exposing the DRAM latency once per wave of CTAs.
+template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+__global__ void __launch_bounds__(kDenWX *kDenWY * 32)
+    layer_stencil_pipe_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                              const __grid_constant__ DenseList dl, int tiles_x, int tiles_y, int ntiles) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kDenKR, TH = kDenWY * 8 * KR;
+    const int C = g.C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int plane = g.rows * g.pitch;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kDenWX, wy = warp / kDenWX;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    int t = blockIdx.x;
+    if (t >= ntiles) return;
+    {
+        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+        load_plane<TI, IN_PL, false>(smem, in + b * fs, g, c, tx * kDenTW + g.dx0, ty * TH + g.dy0);
+    }
+    cp_async_commit_();
+    for (int k = 0; t < ntiles; t += gridDim.x, k ^= 1) {
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) {
+            const int c = tn % C, r = tn / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+            load_plane<TI, IN_PL, false>(smem + (k ^ 1) * plane, in + b * fs, g, c, tx * kDenTW + g.dx0,
+                                         ty * TH + g.dy0);
+        }
+        cp_async_commit_();
+        cp_async_wait_one_();
+        __syncthreads();
+        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
+        float acc[KR][8];
+        stencil_block<D, KR>(acc, smem + k * plane + row0 * g.pitch + col0 + dl.col_shift, g.pitch, dl);
+        store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty * TH + row0, tx * kDenTW + col0, acc);
+        __syncthreads();
+    }
 }
 
 // HWC-input dense stencil with all channels per CTA (first layer of a chain):
@@ -1004,13 +1054,39 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     return SKC_OK;
 }
 
+// SKC_STENCIL_PIPE=1: persistent double-buffered stencil (tile loads overlap compute).
+static bool stencil_pipe_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_STENCIL_PIPE");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int C, const DenseList &dl,
                             const LGeom &g, cudaStream_t s) {
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    if constexpr (KR == kDenKR) {
+        if (stencil_pipe_enabled() && 2 * smem <= (size_t)kMaxSmem) {
+            const int tiles_x = ceil_div(W, kDenTW), tiles_y = ceil_div(H, kDenWY * 8 * KR);
+            const long long nt = (long long)tiles_x * tiles_y * B * C;
+            if (nt < (1LL << 31)) {
+                auto pk = layer_stencil_pipe_kernel<D, TI, TO, IN_PL, OUT_PL>;
+                static int pattr = set_smem_attr(pk);
+                if (pattr) return pattr;
+                const int per_sm = std::max(1, std::min(4, (int)((size_t)kMaxSmem / (2 * smem))));
+                const int grid = (int)std::min<long long>(nt, 148LL * per_sm);
+                pk<<<grid, kDenWX * kDenWY * 32, 2 * smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out),
+                                                                g, dl, tiles_x, tiles_y, (int)nt);
+                SKC_LAUNCH_CHECK("layer_stencil_pipe_kernel");
+                return SKC_OK;
+            }
+        }
+    }
     auto kern = layer_stencil_kernel<D, KR, TI, TO, IN_PL, OUT_PL>;
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
     dim3 grid(ceil_div(W, kDenTW) * C, ceil_div(H, kDenWY * 8 * KR), B);
     kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);
     SKC_LAUNCH_CHECK("layer_stencil_kernel");

@@ -237,7 +237,8 @@ def test_rolled_stencil_inner_layers(skc, orc):
     """Inner (planar) layers with D = 5 / 7 / 9 footprints: the default fully
     unrolled stencil and the opt-in variants (SKC_STENCIL_ROLL=1 row-rolled,
     SKC_STENCIL_ALOOP=1 stencil-row loop, SKC_STENCIL_KR=3 odd pitch,
-    SKC_STENCIL_HWC=1 all-channel HWC chain head) all
+    SKC_STENCIL_HWC=1 all-channel HWC chain head, SKC_STENCIL_PIPE=1
+    persistent double-buffered) all
     match the oracle and each other on ragged sizes and both boundaries."""
     import os
     import subprocess
@@ -268,7 +269,7 @@ def test_rolled_stencil_inner_layers(skc, orc):
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
                 for var in ({"SKC_STENCIL_ROLL": "1"}, {"SKC_STENCIL_ALOOP": "1"}, {"SKC_STENCIL_KR": "3"},
-                            {"SKC_STENCIL_HWC": "1"}):
+                            {"SKC_STENCIL_HWC": "1"}, {"SKC_STENCIL_PIPE": "1"}):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6, var

@@ -58,6 +58,42 @@ def test_sv_c2_window_vs_oracle(skc, orc):
     assert normwise(out[y0 + m:y1 - m, x0 + m:x1 - m], ref[m:-m, m:-m]) < TOL32
 
 
+def test_sv_tile_layouts_agree(skc, orc):
+    """The interleaved SV tile (default) and the channel-planar one
+    (SKC_SV_PLANAR=1) compute the same sums in the same order: identical
+    outputs for C = 1 / 3 / 4, fp32 and fp16 storage, both boundaries; both
+    match the oracle."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    from paper_2512_04556_b200 import synth
+    from paper_2512_04556_b200.svfilter import stacked_params
+    basis = synth.c2_basis()
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "d = np.load(sys.argv[1]);"
+            "np.save(sys.argv[2], skc.sv_filter(d['img'], synth.c2_basis(), d['pmap'], boundary=sys.argv[3]))")
+    rng = np.random.default_rng(17)
+    with tempfile.TemporaryDirectory() as td:
+        for (h, w, c, dt) in ((157, 203, 3, np.float32), (96, 130, 4, np.float16), (70, 91, 1, np.float32)):
+            img = rng.random((h, w, c)).astype(dt)
+            if c == 1:
+                img = img[..., 0]
+            pmap = rng.random((h, w)).astype(np.float32)
+            for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                ours = np.asarray(skc.sv_filter(img, basis, pmap, boundary=mode))
+                ref = orc.sv_filter(img.astype(np.float64), pmap, basis.params, stacked_params(basis),
+                                    basis.layout, oid)
+                assert normwise(ours, ref) < (TOL32 if dt == np.float32 else 2e-3)
+                np.savez(f"{td}/in.npz", img=img, pmap=pmap)
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/o.npy", mode], check=True,
+                               env=dict(os.environ, SKC_SV_PLANAR="1"), cwd=root)
+                assert np.array_equal(ours, np.load(f"{td}/o.npy"))
+
+
 def test_sv_constant_map_equals_uniform(skc):
     from paper_2512_04556_b200 import synth
     basis = synth.c2_basis()
