@@ -80,6 +80,14 @@ def smem_peak_gbps():
     return 148 * 128 * 1.965
 
 
+def smem_peaks():
+    p = ROOT / "profiles" / "smem_peak.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {"lds64_GBps": 148 * 128 * 1.965, "lds32_GBps": 148 * 128 * 1.965}
+
+
 def ncu_traffic(config):
     """DRAM bytes (read + write) per launch of the dominant kernel at the bench
     batch, from the committed ncu capture (profiles/ncu_traffic.json)."""
@@ -199,6 +207,33 @@ class Chain:
             bi = esz if k == 0 else 4
             bo = esz if k == self.launches_per_step - 1 else 4
             self.alg_bytes.append(px * (bi + bo))
+        # algorithmic shared-memory load bytes per launch (the register-blocked
+        # windows the chosen kernel reads; skc_layer_plan says which kernel runs)
+        self.smem_bytes, self.smem_kind = [], []
+        if not self.fused:
+            seq = (["relayout"] if self.pre else []) + list(range(len(self.taps))) + (["relayout"] if self.post else [])
+            import ctypes
+            for item in seq:
+                if item == "relayout":
+                    self.smem_bytes.append(0)
+                    self.smem_kind.append("relayout")
+                    continue
+                t = self.taps[item]
+                kind, par = ctypes.c_int(), ctypes.c_int()
+                nat.lib().skc_layer_plan(nat.dbl(t), t.shape[0], self.h, self.w, self.c,
+                                         0 if self.boundary == "zero" else 1, ctypes.byref(kind), ctypes.byref(par))
+                npx = self.nf * self.h * self.w * self.c
+                if kind.value == 0:      # tap tile: (KR+1) x 9 words per tap per KR x 8 block
+                    kr = par.value
+                    self.smem_bytes.append(t.shape[0] * npx * (kr + 1) * 9 * 4 / (8 * kr))
+                    self.smem_kind.append(f"tap tile KR={kr} (LDS.64 + LDS.32)")
+                elif kind.value == 1:    # dense stencil: (5+D-1) rows x (8+D-1) words per 5 x 8 block
+                    d = par.value
+                    self.smem_bytes.append(npx * (5 + d - 1) * (8 + d - 1) * 4 / 40)
+                    self.smem_kind.append(f"dense stencil D={d} (LDS.32)")
+                else:
+                    self.smem_bytes.append(0)
+                    self.smem_kind.append("direct gather (global)")
         self.metric = {
             "c1": "filtered Mpix/s (1264x2665 RGB, 4 layers x 32 taps)",
             "c0": "filtered Mpix/s (512x512 RGB, 4 layers x 12 taps, clamp-to-edge)",
@@ -666,6 +701,16 @@ def run_ours(args):
             "gpu_launches": args.steps * nl,
             "clocks": clk,
         }
+        if getattr(wl, "smem_bytes", None) and wl.smem_bytes[dom] > 0:
+            pk = smem_peaks()
+            peak_s = pk["lds64_GBps"] if "tap" in wl.smem_kind[dom] else pk["lds32_GBps"]
+            ach = wl.smem_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
+            line["roofline"]["smem"] = {
+                "kernel": wl.smem_kind[dom], "bytes_per_launch": wl.smem_bytes[dom], "achieved_GBps": ach,
+                "peak_GBps": peak_s, "frac": ach / peak_s,
+                "peak_kind": "measured (profiles/smem_peak.json, tools/smem_peak.cu)",
+                "note": "the dominant launch is bound by shared-memory load bandwidth, not HBM: algorithmic "
+                        "shared-memory bytes of its register-blocked windows / its event-timed duration"}
         if isinstance(wl, Chain) and not getattr(wl, "fused", False):
             fma = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * wl.units_per_step
             line["roofline"]["fp32_fma"] = {

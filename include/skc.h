@@ -99,6 +99,12 @@ int skc_chain_is_fused(const double *taps, const int *layout, int L, int H, int 
 int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int W, int C,
                         int in_dtype, int boundary);
 
+/* Which kernel family skc_layer_fwd(_ex) runs for this layer with the default
+ * switches: *kind = 0 tap tile (*param = rows per thread KR), 1 dense stencil
+ * (*param = D), 2 direct gather.  Lets callers compute a launch's algorithmic
+ * shared-memory traffic (bench roofline). */
+int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary, int *kind, int *param);
+
 /* Layout/dtype conversion HWC <-> planar fp32 (the chain's bracketing passes). */
 int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
                  int out_layout, int B, int H, int W, int C, void *stream);

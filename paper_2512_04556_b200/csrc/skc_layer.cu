@@ -971,6 +971,17 @@ static int launch_tap_cl(const float *in, TO *out, int B, int H, int W, const LG
     return SKC_OK;
 }
 
+// Rows per thread of the tap tile for a layer of `ntaps` taps with the given
+// corner footprint (see tap_kr_override).
+static int tap_kr_for(int H, int W, int C, int boundary, int accumulate, int dx_min, int dx_max, int dy_min,
+                      int dy_max, int ntaps) {
+    const int KR = tap_kr_override();
+    if (KR == 5 || KR == 7) return KR;
+    if (ntaps <= 16) return 5;  // memory-bound layers: smaller tiles, more CTAs in flight (config 3: 2.05 vs 2.17 ms)
+    const LGeom g7 = make_geom(H, W, C, boundary, accumulate, kTTW, kTWY * 8 * 7, dx_min, dx_max, dy_min, dy_max);
+    return ((size_t)g7.rows * g7.pitch * sizeof(float) * 2 <= (size_t)kMaxSmem) ? 7 : 5;
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_taps(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int t0,
                        int t1, int boundary, int accumulate, cudaStream_t s) {
@@ -981,13 +992,7 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
         dy_min = std::min(dy_min, pl.iy[i]);
         dy_max = std::max(dy_max, pl.iy[i] + 1);
     }
-    int KR = tap_kr_override();
-    if (KR != 5 && KR != 7 && t1 - t0 <= 16) {
-        KR = 5;  // memory-bound layers: smaller tiles, more CTAs in flight (config 3: 2.05 vs 2.17 ms)
-    } else if (KR != 5 && KR != 7) {
-        const LGeom g7 = make_geom(H, W, C, boundary, accumulate, kTTW, kTWY * 8 * 7, dx_min, dx_max, dy_min, dy_max);
-        KR = ((size_t)g7.rows * g7.pitch * sizeof(float) * 2 <= (size_t)kMaxSmem) ? 7 : 5;
-    }
+    const int KR = tap_kr_for(H, W, C, boundary, accumulate, dx_min, dx_max, dy_min, dy_max, t1 - t0);
     const int TH = kTWY * 8 * KR;
     LGeom g = make_geom(H, W, C, boundary, accumulate, kTTW, TH, dx_min, dx_max, dy_min, dy_max);
     TapList tl;
@@ -1574,6 +1579,38 @@ int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out
         return fail(SKC_EBADARG, "planar tensors are fp32");
     return relayout(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, out_layout == SKC_CHW, B, H, W, C,
                     (cudaStream_t)stream);
+}
+
+int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary, int *kind, int *param) {
+    if (!taps || S < 1 || H < 1 || W < 1 || C < 1 || !kind || !param) return fail(SKC_EBADARG, "bad layer arguments");
+    const Plan pl = plan_taps(taps, S);
+    if (dense_allowed()) {
+        const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
+        const int D = dense_size_for(std::max(sx, sy));
+        if (D != 0 && D * D < 4 * S) {
+            *kind = 1;
+            *param = D;
+            return SKC_OK;
+        }
+    }
+    const int n = std::min(S, kLMaxTaps);
+    int dx_min = 1 << 30, dx_max = -(1 << 30), dy_min = 1 << 30, dy_max = -(1 << 30);
+    for (int i = 0; i < n; ++i) {
+        dx_min = std::min(dx_min, pl.ix[i]);
+        dx_max = std::max(dx_max, pl.ix[i] + 1);
+        dy_min = std::min(dy_min, pl.iy[i]);
+        dy_max = std::max(dy_max, pl.iy[i] + 1);
+    }
+    const int KR = tap_kr_for(H, W, C, boundary, 0, dx_min, dx_max, dy_min, dy_max, n);
+    const LGeom g = make_geom(H, W, C, boundary, 0, kTTW, kTWY * 8 * KR, dx_min, dx_max, dy_min, dy_max);
+    if ((size_t)g.rows * g.pitch * sizeof(float) > (size_t)kMaxSmem) {
+        *kind = 2;
+        *param = 0;
+    } else {
+        *kind = 0;
+        *param = KR;
+    }
+    return SKC_OK;
 }
 
 int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int W, int C, int in_dtype,
