@@ -296,6 +296,36 @@ __device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom 
 }
 
 // --------------------------------------------------------------- tap path ---
+// Staged HWC epilogue (see layer_tap_kernel): tile rows of one channel.
+constexpr int kStagePitch = 132;  // 128 + 4: STS.128 conflict-free for odd KR (KR * 33 odd)
+
+template <int KR, typename TO>
+__device__ __forceinline__ void stage_store_hwc(float *smem, const float (&acc)[KR][8], TO *__restrict__ frame,
+                                                const LGeom &g, int c, int ty0, int tx0, int row0, int col0) {
+    __syncthreads();  // every warp is done reading the input tile
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+        float4 *d = reinterpret_cast<float4 *>(smem + (row0 + r) * kStagePitch + col0);
+        d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
+    }
+    __syncthreads();
+    constexpr int TH = 2 * 8 * KR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int C = g.C;
+    const int nx = min(128, g.W - tx0), nr = min(TH, g.H - ty0);
+    for (int r = warp; r < nr; r += nw) {
+        TO *dst = frame + ((long long)(ty0 + r) * g.W + tx0) * C + c;
+        const float *src = smem + r * kStagePitch;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = lane + 32 * u;
+            if (x < nx) IO<TO>::st(dst + (long long)x * C, src[x]);
+        }
+    }
+}
+
+
 constexpr int kTWX = 4, kTWY = 2;                 // 256 threads, tile 128 x (16 * KR)
 constexpr int kTTW = kTWX * 32;
 
@@ -369,6 +399,17 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
 #pragma unroll 1
     for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
 
+    if constexpr (IN_PL && !OUT_PL) {
+        if (!g.accumulate) {
+            // HWC output from a channel CTA: stage the tile in the dead input
+            // tile, then every warp writes whole tile rows with lanes along x
+            // (stride-C addresses: 32 lanes cover 3-4 contiguous lines, and
+            // the C channel CTAs of the tile, which run together, complete
+            // the sectors in L2) instead of 8 scattered rows per instruction.
+            stage_store_hwc<KR, TO>(smem, acc, out + b * fs, g, c, ty0, tx0, row0, col0);
+            return;
+        }
+    }
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
@@ -1482,10 +1523,22 @@ static int chain_policy(int in_dtype) {
     return in_dtype == SKC_F16 ? 1 : 2;
 }
 
-// Would a chain's last layer (planar fp32 in, HWC out) run the cluster tap
-// kernel?  Mirrors the routing of layer_t -> try_stencil -> launch_taps.
+// SKC_TAP_HWC_STAGE=0: chains end with planar + relayout even when the last
+// layer is a tap layer (whose kernel can write HWC through its staged epilogue).
+static bool tap_hwc_stage_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_TAP_HWC_STAGE");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+// Would a chain's last layer (planar fp32 in, HWC out) run a tap kernel that
+// writes HWC itself (staged epilogue, or the cluster one)?  Mirrors the
+// routing of layer_t -> try_stencil -> launch_taps.
 static bool last_layer_direct(int H, int W, int C, const double *taps, int S, int boundary) {
-    if (!tap_cluster_enabled() || (C != 3 && C != 4) || S > kLMaxTaps) return false;
+    const bool cluster = tap_cluster_enabled() && (C == 3 || C == 4);
+    if ((!cluster && !tap_hwc_stage_enabled()) || S > kLMaxTaps) return false;
     const Plan pl = plan_taps(taps, S);
     if (dense_allowed()) {
         const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;

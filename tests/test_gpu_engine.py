@@ -301,11 +301,11 @@ def test_chain_io_policies_agree(skc):
 
 
 def test_cluster_hwc_epilogue(skc, orc):
-    """With SKC_TAP_CLUSTER=1 a chain whose last layer is a tap layer writes
-    HWC straight from a C-CTA cluster (DSMEM staging) instead of planar +
-    relayout; it must equal the default relayout path bit for bit and the
-    oracle, for C = 3 / 4, fp32 / fp16 storage, ragged sizes and both
-    boundaries."""
+    """A chain whose last layer is a tap layer writes HWC straight from the
+    tap kernel (default: staged epilogue; SKC_TAP_CLUSTER=1: C-CTA cluster
+    with DSMEM) instead of planar + relayout (SKC_TAP_HWC_STAGE=0); all three
+    agree bit for bit and match the oracle, for C = 3 / 4, fp32 / fp16
+    storage, ragged sizes and both boundaries."""
     import os
     import subprocess
     import sys
@@ -334,9 +334,10 @@ def test_cluster_hwc_epilogue(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
-                               env=dict(os.environ, SKC_TAP_CLUSTER="1"), cwd=root)
-                assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy"))
+                for var in ({"SKC_TAP_CLUSTER": "1"}, {"SKC_TAP_HWC_STAGE": "0"}):
+                    subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
+                                   env=dict(os.environ, **var), cwd=root)
+                    assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy")), var
 
 
 def test_fused_chain_matches_oracle_and_unfused(skc, orc):
