@@ -672,6 +672,20 @@ __global__ void __launch_bounds__(kHWX *kHWY * 32)
     {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
         const int rowlen = g.pitch * C;
+        if (gx0 >= 0 && gx0 + g.pitch <= g.W && gy0 >= 0 && gy0 + g.rows <= g.H) {
+            // interior tile: every tile row is one contiguous run of pitch * C floats
+            const float *sx = frame + ((long long)(gy0 + warp) * g.W + gx0) * C + lane;
+            unsigned sd = (unsigned)__cvta_generic_to_shared(smem + warp * rowlen + lane);
+            const long long gstep = (long long)nw * g.W * C;
+            const unsigned sstep = 4u * nw * rowlen;
+            for (int r = warp; r < g.rows; r += nw, sx += gstep, sd += sstep) {
+                const float *p = sx;
+                unsigned q = sd;
+#pragma unroll 4
+                for (int e = lane; e < rowlen; e += 32, p += 32, q += 128) cp_async4s(q, p);
+            }
+            cp_async_wait_all();
+        } else
         for (int r = warp; r < g.rows; r += nw) {
             int gy = gy0 + r;
             const bool rowin = clamp || (gy >= 0 && gy < g.H);
