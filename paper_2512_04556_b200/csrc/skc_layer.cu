@@ -209,6 +209,25 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
         cp_async_wait_all();
     } else {
         constexpr int U = 8;
+        if (gx0 >= 0 && gx0 + g.pitch <= W && gy0 >= 0 && gy0 + g.rows <= H) {
+            // interior tile: U independent strided loads in flight per lane, no clamping
+            const TI *sx = frame + ((long long)(gy0 + warp) * W + gx0 + lane) * C + c;
+            float *dx = s + warp * g.pitch + lane;
+            const long long gstep = (long long)nw * W * C;
+            for (int r = warp; r < g.rows; r += nw, sx += gstep, dx += nw * g.pitch) {
+                for (int c0 = lane; c0 < g.pitch; c0 += 32 * U) {
+                    float v[U];
+                    const int o = c0 - lane;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        v[u] = (c0 + 32 * u < g.pitch) ? IO<TI>::ld(sx + (long long)(o + 32 * u) * C) : 0.f;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (c0 + 32 * u < g.pitch) dx[o + 32 * u] = v[u];
+                }
+            }
+            return;
+        }
         for (int r = warp; r < g.rows; r += nw) {
             int gy = gy0 + r;
             const bool rowin = clamp || (gy >= 0 && gy < H);

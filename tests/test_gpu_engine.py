@@ -289,7 +289,8 @@ def test_chain_io_policies_agree(skc):
     root = str(__import__("pathlib").Path(__file__).parent.parent)
     rng = np.random.default_rng(5)
     with tempfile.TemporaryDirectory() as td:
-        for img in (rng.random((97, 130, 3)).astype(np.float32), rng.random((61, 77, 4)).astype(np.float16)):
+        for img in (rng.random((97, 130, 3)).astype(np.float32), rng.random((61, 77, 4)).astype(np.float16),
+                    rng.random((300, 700, 4)).astype(np.float16), rng.random((333, 517, 3)).astype(np.float32)):
             np.save(f"{td}/in.npy", img)
             outs = []
             for pol in ("0", "1", "2"):
