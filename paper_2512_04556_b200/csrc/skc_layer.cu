@@ -348,10 +348,15 @@ __device__ __forceinline__ void stage_store_hwc(float *smem, const float (&acc)[
 constexpr int kTWX = 4, kTWY = 2;                 // 256 threads, tile 128 x (16 * KR)
 constexpr int kTTW = kTWX * 32;
 
-template <int KR>
+// SH: the ninth window column (even taps: column 8; odd taps: column 0) is
+// the neighbouring lane's first / last column, fetched with a shuffle; only
+// the lanes at the warp's block edge (lx = 3 / lx = 0: 8 lanes, bank-disjoint)
+// read it from shared memory.  Replaces the 2-way-conflicted LDS.32.
+template <int KR, bool SH = false>
 __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, int pitch, float4 w,
                                          bool odd) {
     float a[9], b[9];
+    const int lx = threadIdx.x & 3;
     auto load_row = [&](const float *q, float (&v)[9]) {
         if (!odd) {
 #pragma unroll
@@ -360,14 +365,26 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
                 v[2 * k] = t.x;
                 v[2 * k + 1] = t.y;
             }
-            v[8] = q[8];
+            if constexpr (SH) {
+                float t = __shfl_down_sync(0xffffffffu, v[0], 1);
+                if (lx == 3) t = q[8];
+                v[8] = t;
+            } else {
+                v[8] = q[8];
+            }
         } else {
-            v[0] = q[0];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const float2 t = reinterpret_cast<const float2 *>(q + 1)[k];
                 v[2 * k + 1] = t.x;
                 v[2 * k + 2] = t.y;
+            }
+            if constexpr (SH) {
+                float t = __shfl_up_sync(0xffffffffu, v[8], 1);
+                if (lx == 0) t = q[0];
+                v[0] = t;
+            } else {
+                v[0] = q[0];
             }
         }
     };
@@ -389,7 +406,7 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
     }
 }
 
-template <int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
+template <int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL, bool SH = false>
 __global__ void __launch_bounds__(kTWX *kTWY * 32)
     layer_tap_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
                      const __grid_constant__ TapList tl) {
@@ -414,9 +431,9 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
 #pragma unroll 1
-    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR, SH>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
 #pragma unroll 1
-    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR, SH>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
 
     if constexpr (IN_PL && !OUT_PL) {
         if (!g.accumulate) {
@@ -1045,6 +1062,15 @@ static int launch_tap_cl(const float *in, TO *out, int B, int H, int W, const LG
     return SKC_OK;
 }
 
+// SKC_TAP_SHFL=1: ninth window column by warp shuffle (see tap_rows).
+static bool tap_shfl_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_TAP_SHFL");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // Rows per thread of the tap tile for a layer of `ntaps` taps with the given
 // corner footprint (see tap_kr_override).
 static int tap_kr_for(int H, int W, int C, int boundary, int accumulate, int dx_min, int dx_max, int dy_min,
@@ -1114,6 +1140,19 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
                 SKC_LAUNCH_CHECK("layer_tap_pipe_kernel");
                 return SKC_OK;
             }
+        }
+    }
+    if constexpr (IN_PL) {
+        if (tap_shfl_enabled() && smem <= (size_t)kMaxSmem) {
+            auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL, true>
+                                : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL, true>;
+            static int sa5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL, true>);
+            static int sa7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL, true>);
+            if (sa5 || sa7) return sa5 ? sa5 : sa7;
+            dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
+            kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
+            SKC_LAUNCH_CHECK("layer_tap_kernel");
+            return SKC_OK;
         }
     }
     if (smem <= (size_t)kMaxSmem) {

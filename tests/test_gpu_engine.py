@@ -335,7 +335,7 @@ def test_cluster_hwc_epilogue(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                for var in ({"SKC_TAP_CLUSTER": "1"}, {"SKC_TAP_HWC_STAGE": "0"}):
+                for var in ({"SKC_TAP_CLUSTER": "1"}, {"SKC_TAP_HWC_STAGE": "0"}, {"SKC_TAP_SHFL": "1"}):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy")), var
