@@ -234,8 +234,8 @@ __device__ __forceinline__ void block_of(int b, int nbx, int nby, int &bx, int &
 // window of tap i starts at source (y0 + sy(i), x0 + sx(i)).
 template <bool ADJ, bool CHECK>
 __device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSmem &S, const Buf &src,
-                                           int s0, int n, int y0, int x0) {
-    for (int i = 0; i < n; ++i) {
+                                           int s0, int n, int y0, int x0, int i0 = 0, int di = 1) {
+    for (int i = i0; i < n; i += di) {
         const int2 d = S.ixy[s0 + i];
         const float4 w = S.cw[s0 + i];
         // forward: out(y,x) reads src(y + d + corner); adjoint: src(y - d - corner)
@@ -287,6 +287,52 @@ __device__ int gather_pass(const FitParams &p, FitSmem &S, int l, const Buf src,
     const int rx0 = ADJ ? -dr.y : dr.x, rx1 = ADJ ? kFMC - 1 - dr.x : kFMC - 1 + dr.y;
     const int nbx = (dst.w + kFMC - 1) / kFMC, nby = (dst.h + kFKR - 1) / kFKR;
     int bad = 0;
+    // Small boxes (the first layers of an impulse response): fewer blocks than
+    // threads, so G = 2^k consecutive lanes share a block and split its taps
+    // (lane g takes taps g, g + G, ...); the G partial sums are combined by a
+    // fixed xor-shuffle tree -- deterministic, and every thread stays busy.
+    int G = 1;
+    while (G < 32 && 2 * G * nbx * nby <= (int)blockDim.x && 2 * G <= n) G *= 2;
+    if (G > 1) {
+        const int b = threadIdx.x / G, g = threadIdx.x & (G - 1);
+        const bool live = b < nbx * nby;
+        float acc[kFKR][kFMC];
+#pragma unroll
+        for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+            for (int c = 0; c < kFMC; ++c) acc[r][c] = 0.f;
+        int y0 = 0, x0 = 0;
+        if (live) {
+            int bx, by;
+            block_of(b, nbx, nby, bx, by);
+            y0 = dst.y0 + by * kFKR;
+            x0 = dst.x0 + bx * kFMC;
+            const bool inside = y0 + ry0 >= src.y0 && y0 + ry1 < src.y0 + src.h && x0 + rx0 >= src.x0 &&
+                                x0 + rx1 < src.x0 + src.w;
+            if (inside)
+                block_taps<ADJ, false>(acc, S, src, s0, n, y0, x0, g, G);
+            else
+                block_taps<ADJ, true>(acc, S, src, s0, n, y0, x0, g, G);
+        }
+        for (int o = G >> 1; o > 0; o >>= 1)
+#pragma unroll
+            for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c < kFMC; ++c) acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], o);
+        if (live && g == 0) {
+#pragma unroll
+            for (int r = 0; r < kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c < kFMC; ++c) {
+                    const int y = y0 + r, x = x0 + c;
+                    if (y < dst.y0 + dst.h && x < dst.x0 + dst.w) {
+                        dst.p[(y - dst.y0) * dst.s + (x - dst.x0)] = acc[r][c];
+                        bad |= !isfinite(acc[r][c]);
+                    }
+                }
+        }
+        return __syncthreads_or(bad);
+    }
     for (int b = threadIdx.x; b < nbx * nby; b += blockDim.x) {
         int bx, by;
         block_of(b, nbx, nby, bx, by);
@@ -357,7 +403,8 @@ __device__ double loss_and_grad(const FitParams &p, FitSmem &S, int b) {
     double part = 0.0;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int y = ty; y < canvas; y += kFitWarps) {
-        for (int x = tx; x < canvas; x += 32) {
+#pragma unroll 4
+        for (int x = tx; x < canvas; x += 32) {  // unrolled: several target loads in flight
             const unsigned dy = (unsigned)(y - g.y0), dx = (unsigned)(x - g.x0);
             const bool in = dy < (unsigned)g.h && dx < (unsigned)g.w;
             const float v = in ? g.p[dy * g.s + dx] : 0.f;
