@@ -403,8 +403,7 @@ __device__ double loss_and_grad(const FitParams &p, FitSmem &S, int b) {
     double part = 0.0;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int y = ty; y < canvas; y += kFitWarps) {
-#pragma unroll 4
-        for (int x = tx; x < canvas; x += 32) {  // unrolled: several target loads in flight
+        for (int x = tx; x < canvas; x += 32) {
             const unsigned dy = (unsigned)(y - g.y0), dx = (unsigned)(x - g.x0);
             const bool in = dy < (unsigned)g.h && dx < (unsigned)g.w;
             const float v = in ? g.p[dy * g.s + dx] : 0.f;
