@@ -1,13 +1,16 @@
-// skc_layer.cu -- uniform sparse-layer kernels (sm_100a), v3.
+// skc_layer.cu -- uniform sparse-layer kernels (sm_100a).
 //
 // Reference: engine.apply_sparse_layer (engine.py:160-170) -> sample_shifted
 // (118-130) -> _accum_shift (106-115); engine.apply_complex (173-178).
 //
-// Work decomposition: one CTA = one (output tile, channel) pair.  The chain's
-// intermediates are fp32 *planar* (B, C, H, W): only the first layer reads the
-// caller's HWC image and only the last writes HWC, so every inner layer loads
-// its halo tile as contiguous rows with 8-byte cp.async (LDGSTS, zero-fill at
-// the image edge) and stores 8-pixel row segments with 16-byte stores.
+// Work decomposition: one CTA = one (output tile, channel) pair, channel-
+// fastest grid.  The chain's intermediates are fp32 *planar* (B, C, H, W): the
+// first layer reads the caller's HWC image (fp16 inputs go through a relayout
+// pass first) and the last writes HWC through the tap kernel's staged
+// epilogue (or a relayout pass after a stencil), so every inner layer loads its
+// halo tile as contiguous rows with 8-byte cp.async (LDGSTS, zero-fill at the
+// image edge; interior tiles take a pointer-increment fast path) and stores
+// 8-pixel row segments with 16-byte stores.
 //
 // Tap path (layer_tap_kernel): a uniform tap is 4 integer shifts with constant
 // weights; the host folds each tap into (shared-memory offset of corner 00,
@@ -15,17 +18,17 @@
 // output block (KR odd); per tap it reads a (KR+1) x 9 window -- 4 LDS.64 +
 // 1 LDS.32 per row, bank-conflict free for LDS.64 because the row pitch is
 // 2 mod 4 and KR is odd -- and issues 32*KR FFMAs with uniform-register
-// weights.  Dense path (layer_dense_kernel): when the merged corner footprint
-// fits D x D (D <= 9) with D^2 < 4S the host merges coincident corners into a
-// stencil whose weights are compile-time constant-bank operands.
+// weights.  Dense path: when the merged corner footprint fits D x D (D <= 9)
+// with D^2 < 4S the host merges coincident corners into a stencil; planar
+// inner layers with D >= 7 run it with packed-FP32 FFMA2 on output-row pairs
+// (layer_stencil2_kernel), the others with constant-bank FFMA operands
+// (layer_stencil_kernel).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
-
-#include <cooperative_groups.h>
 
 #include "skc_tile.cuh"
 
@@ -251,40 +254,6 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
     }
 }
 
-// Planar fp32 plane into s[rows][pitch] with 4-byte cp.async (any pitch parity).
-__device__ __forceinline__ void load_plane4(float *s, const float *__restrict__ frame, const LGeom &g, int c,
-                                            int gx0, int gy0) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const bool clamp = g.boundary == SKC_CLAMP;
-    const int H = g.H, W = g.W;
-    const float *plane = frame + (long long)c * H * W;
-    if (gx0 >= 0 && gx0 + g.pitch <= W && gy0 >= 0 && gy0 + g.rows <= H &&
-        tile_rows_any<1>((unsigned)__cvta_generic_to_shared(s + warp * g.pitch + lane),
-                         plane + (long long)(gy0 + warp) * W + gx0 + lane, lane, g.pitch, warp, g.rows, nw,
-                         4u * nw * g.pitch, (long long)nw * W, 1)) {
-        cp_async_wait_all();
-        return;
-    }
-    for (int r = warp; r < g.rows; r += nw) {
-        int gy = gy0 + r;
-        const bool rowin = clamp || (gy >= 0 && gy < H);
-        gy = min(max(gy, 0), H - 1);
-        const float *src = plane + (long long)gy * W;
-        float *dst = s + r * g.pitch;
-        if (rowin && gx0 >= 0 && gx0 + g.pitch <= W) {  // interior row: no clamping
-            row_elems_any((unsigned)__cvta_generic_to_shared(dst + lane), src + gx0 + lane, lane, g.pitch, 1);
-            continue;
-        }
-#pragma unroll 4
-        for (int col = lane; col < g.pitch; col += 32) {
-            const int gx = gx0 + col;
-            const bool ok = clamp || (rowin && gx >= 0 && gx < W);
-            cp_async4(dst + col, src + min(max(gx, 0), W - 1), ok);
-        }
-    }
-    cp_async_wait_all();
-}
-
 // Store a KR x 8 block of one channel.
 template <int KR, typename TO, bool PLANAR>
 __device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom &g, int c, int gy0,
@@ -348,15 +317,10 @@ __device__ __forceinline__ void stage_store_hwc(float *smem, const float (&acc)[
 constexpr int kTWX = 4, kTWY = 2;                 // 256 threads, tile 128 x (16 * KR)
 constexpr int kTTW = kTWX * 32;
 
-// SH: the ninth window column (even taps: column 8; odd taps: column 0) is
-// the neighbouring lane's first / last column, fetched with a shuffle; only
-// the lanes at the warp's block edge (lx = 3 / lx = 0: 8 lanes, bank-disjoint)
-// read it from shared memory.  Replaces the 2-way-conflicted LDS.32.
-template <int KR, bool SH = false>
+template <int KR>
 __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, int pitch, float4 w,
                                          bool odd) {
     float a[9], b[9];
-    const int lx = threadIdx.x & 3;
     auto load_row = [&](const float *q, float (&v)[9]) {
         if (!odd) {
 #pragma unroll
@@ -365,13 +329,7 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
                 v[2 * k] = t.x;
                 v[2 * k + 1] = t.y;
             }
-            if constexpr (SH) {
-                float t = __shfl_down_sync(0xffffffffu, v[0], 1);
-                if (lx == 3) t = q[8];
-                v[8] = t;
-            } else {
-                v[8] = q[8];
-            }
+            v[8] = q[8];
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -379,13 +337,7 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
                 v[2 * k + 1] = t.x;
                 v[2 * k + 2] = t.y;
             }
-            if constexpr (SH) {
-                float t = __shfl_up_sync(0xffffffffu, v[8], 1);
-                if (lx == 0) t = q[0];
-                v[0] = t;
-            } else {
-                v[0] = q[0];
-            }
+            v[0] = q[0];
         }
     };
     load_row(p, a);
@@ -406,7 +358,7 @@ __device__ __forceinline__ void tap_rows(float (&acc)[KR][8], const float *p, in
     }
 }
 
-template <int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL, bool SH = false>
+template <int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(kTWX *kTWY * 32)
     layer_tap_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
                      const __grid_constant__ TapList tl) {
@@ -431,9 +383,9 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
 #pragma unroll 1
-    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR, SH>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
 #pragma unroll 1
-    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR, SH>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
 
     if constexpr (IN_PL && !OUT_PL) {
         if (!g.accumulate) {
@@ -449,144 +401,9 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
-// Last layer of a chain with an HWC output: the C channel CTAs of one tile
-// form a thread-block cluster (dims C x 1 x 1; the grid is channel-fastest so
-// cluster rank == channel).  After the tap loop each CTA stages its KR x 8
-// blocks in its own (now dead) input tile, the cluster synchronises, and CTA q
-// writes rows q, q + C, ... of the tile as contiguous interleaved HWC runs,
-// reading the other channels from its peers' shared memory (DSMEM).  This
-// replaces the planar store + relayout pass (one full read + write of the
-// image) with coalesced HWC stores.
-constexpr int kStageP = kTTW + 4;  // staging pitch: STS.128 conflict-free (KR*33 odd)
-
-template <int KR, typename TO, int C>
-__global__ void __launch_bounds__(kTWX *kTWY * 32)
-    layer_tap_cl_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
-                        const __grid_constant__ TapList tl) {
-    namespace cg = cooperative_groups;
-    extern __shared__ __align__(16) float smem[];
-    const int b = blockIdx.z, c = blockIdx.x % C;
-    const long long fs = (long long)g.H * g.W * C;
-    constexpr int TH = kTWY * 8 * KR;
-    const int tx0 = (blockIdx.x / C) * kTTW, ty0 = blockIdx.y * TH;
-    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
-    const int col0 = wx * 32 + lx * 8;
-    const int row0 = wy * 8 * KR + ly * KR;
-    {
-        const float *base = smem + row0 * g.pitch + col0;
-        float acc[KR][8];
-#pragma unroll
-        for (int r = 0; r < KR; ++r)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
-#pragma unroll 1
-        for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
-#pragma unroll 1
-        for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
-        __syncthreads();  // every warp is done with the input tile
-#pragma unroll
-        for (int r = 0; r < KR; ++r) {
-            float4 *d = reinterpret_cast<float4 *>(smem + (row0 + r) * kStageP + col0);
-            d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
-            d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
-        }
-    }
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    const int q = (int)cl.block_rank();
-    const int nx = min(kTTW, g.W - tx0), nrows = min(TH, g.H - ty0);
-    const int ne = nx * C;                                    // floats per HWC row run
-    const int mine = nrows > q ? (nrows - q + C - 1) / C : 0;  // rows q, q + C, ...
-    const int total = mine * ne;
-    TO *frame = out + b * fs;
-    constexpr int U = 4;
-    for (int i0 = threadIdx.x; i0 < total; i0 += U * kTWX * kTWY * 32) {
-        float v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * kTWX * kTWY * 32;
-            if (i < total) {
-                const int k = i / ne, e = i - k * ne;
-                const int x = e / C, ch = e - x * C;
-                const float *src = cl.map_shared_rank(smem + (q + C * k) * kStageP + x, ch);
-                v[u] = *src;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * kTWX * kTWY * 32;
-            if (i < total) {
-                const int k = i / ne, e = i - k * ne;
-                IO<TO>::st(frame + ((long long)(ty0 + q + C * k) * g.W + tx0) * C + e, v[u]);
-            }
-        }
-    }
-    cl.sync();  // peers may still be reading this CTA's stage
-}
-
-// Persistent, double-buffered variant for fp32 planar inputs: each CTA walks
-// tiles blockIdx.x, +gridDim.x, ... and issues the cp.async loads of its next
-// tile before computing the current one, so the halo-tile transfer of
-// memory-bound layers (few taps) overlaps the FMAs instead of serialising.
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
-template <int KR, typename TO, bool OUT_PL>
-__global__ void __launch_bounds__(kTWX *kTWY * 32)
-    layer_tap_pipe_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
-                          const __grid_constant__ TapList tl, int tiles_x, int tiles_y, int ntiles) {
-    extern __shared__ __align__(16) float smem[];
-    constexpr int TH = kTWY * 8 * KR;
-    const int C = g.C;
-    const long long fs = (long long)g.H * g.W * C;
-    const int plane = g.rows * g.pitch;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
-    const int col0 = wx * 32 + lx * 8;
-    const int row0 = wy * 8 * KR + ly * KR;
-    int t = blockIdx.x;
-    if (t >= ntiles) return;
-    {
-        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-        load_plane<float, true, false>(smem, in + b * fs, g, c, tx * kTTW + g.dx0, ty * TH + g.dy0);
-    }
-    cp_async_commit();
-    for (int k = 0; t < ntiles; t += gridDim.x, k ^= 1) {
-        const int tn = t + gridDim.x;
-        if (tn < ntiles) {
-            const int c = tn % C, r = tn / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-            load_plane<float, true, false>(smem + (k ^ 1) * plane, in + b * fs, g, c, tx * kTTW + g.dx0,
-                                           ty * TH + g.dy0);
-        }
-        cp_async_commit();
-        cp_async_wait_one();
-        __syncthreads();
-        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-        const float *base = smem + k * plane + row0 * g.pitch + col0;
-        float acc[KR][8];
-#pragma unroll
-        for (int rr = 0; rr < KR; ++rr)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[rr][j] = 0.f;
-#pragma unroll 1
-        for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
-#pragma unroll 1
-        for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
-        store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty * TH + row0, tx * kTTW + col0, acc);
-        __syncthreads();
-    }
-}
-
 // ------------------------------------------------------------- dense path ---
 constexpr int kDenKR = 5, kDenWX = 4, kDenWY = 2;  // 256 threads, tile 128 x 80
 constexpr int kDenTW = kDenWX * 32, kDenTH = kDenWY * 8 * kDenKR;
-
-__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_one_() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 // acc = the D x D stencil over a KR x 8 block whose window starts at pc.
 template <int D, int KR>
@@ -614,9 +431,96 @@ __device__ __forceinline__ void stencil_block(float (&acc)[KR][8], const float *
     }
 }
 
-// KR = 3 runs with an odd pitch (planar rows staged with 4-byte cp.async):
-// 3 * pitch odd makes the per-lane LDS.32 window reads conflict-free and the
-// unrolled body is 3/5 the size.
+// Packed-FP32 dense stencil (FFMA2, sm_100): each thread owns KR2 = 6 rows x
+// 8 columns as 3 row pairs; one fma.rn.f32x2 updates (out[2p][j],
+// out[2p+1][j]) with the weight pair (K[a][b], K[a-1][b]) -- adjacent in a
+// host-prepared table, loaded as one 64-bit operand -- times the broadcast
+// input texel w[j+b] (the .F32 scalar operand form).  No register pairing of
+// inputs is needed, and every instruction does two FMAs.  Rows a = 0 and a = D
+// of the table hold a zero in the missing half (10% padding work at D = 9).
+constexpr int kF2KR = 6, kF2TH = kDenWY * 8 * kF2KR;  // tile 128 x 96
+
+struct DenseList2 {
+    float2 k2[(kMaxDense + 1) * kMaxDense];  // k2[a][b] = (K[a][b], K[a-1][b]), zero outside 0..D-1
+    int D;
+    int col_shift;
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a);
+    unsigned long long rb = *reinterpret_cast<unsigned long long *>(&b);
+    unsigned long long rc = *reinterpret_cast<unsigned long long *>(&c), rd;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+    return *reinterpret_cast<float2 *>(&rd);
+}
+
+// Planar fp32 in and out (the chain's inner layers).  SH = col_shift & 1:
+// window rows are read with LDS.64 from the 8-byte-aligned column at or before
+// the window start.
+template <int D, int SH>
+__global__ void __launch_bounds__(kDenWX *kDenWY * 32)
+    layer_stencil2_kernel(const float *__restrict__ in, float *__restrict__ out, const LGeom g,
+                          const __grid_constant__ DenseList2 dl) {
+    extern __shared__ __align__(16) float smem[];
+    constexpr int KR = kF2KR, NP = KR / 2;
+    const int C = g.C;
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const long long fs = (long long)g.H * g.W * C;
+    const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * kF2TH;
+    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kDenWX, wy = warp / kDenWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * KR + ly * KR;
+    const float *pc = smem + row0 * g.pitch + col0 + dl.col_shift;
+    const int pitch = g.pitch;
+
+    float2 acc[NP][8];
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < KR + D - 1; ++r) {
+        float w[8 + D - 1 + 1];
+        {
+            constexpr int NV = (8 + D - 1 + SH + 1) / 2;
+            float raw[2 * NV];
+            const float2 *q2 = reinterpret_cast<const float2 *>(pc - SH + r * pitch);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float2 t = q2[v];
+                raw[2 * v] = t.x;
+                raw[2 * v + 1] = t.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 8 + D - 1; ++j) w[j] = raw[j + SH];
+        }
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            const int a = r - 2 * pp;  // row 2pp takes stencil row a, row 2pp+1 row a-1
+            if (a < 0 || a > D) continue;
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                const float2 kk = dl.k2[a * D + bb];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[pp][j] = ffma2(kk, make_float2(w[j + bb], w[j + bb]), acc[pp][j]);
+            }
+        }
+    }
+    float res[KR][8];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            res[2 * pp][j] = acc[pp][j].x;
+            res[2 * pp + 1][j] = acc[pp][j].y;
+        }
+    store_block<KR, float, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, res);
+}
+
 template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     layer_stencil_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
@@ -626,10 +530,7 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
     const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * (kDenWY * 8 * KR);
-    if constexpr (IN_PL && KR == 3)
-        load_plane4(smem, reinterpret_cast<const float *>(in) + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
-    else
-        load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    load_plane<TI, IN_PL>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -641,265 +542,6 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
 
     float acc[KR][8];
     stencil_block<D, KR>(acc, pc, pitch, dl);
-    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
-}
-
-// Persistent, double-buffered stencil: each CTA walks tiles blockIdx.x,
-// +gridDim.x, ... and issues the cp.async loads of its next tile before
-// computing the current one, so tile loads overlap the FFMA stream instead of
-// exposing the DRAM latency once per wave of CTAs.
-template <int D, typename TI, typename TO, bool IN_PL, bool OUT_PL>
-__global__ void __launch_bounds__(kDenWX *kDenWY * 32)
-    layer_stencil_pipe_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
-                              const __grid_constant__ DenseList dl, int tiles_x, int tiles_y, int ntiles) {
-    extern __shared__ __align__(16) float smem[];
-    constexpr int KR = kDenKR, TH = kDenWY * 8 * KR;
-    const int C = g.C;
-    const long long fs = (long long)g.H * g.W * C;
-    const int plane = g.rows * g.pitch;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kDenWX, wy = warp / kDenWX;
-    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
-    int t = blockIdx.x;
-    if (t >= ntiles) return;
-    {
-        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-        load_plane<TI, IN_PL, false>(smem, in + b * fs, g, c, tx * kDenTW + g.dx0, ty * TH + g.dy0);
-    }
-    cp_async_commit_();
-    for (int k = 0; t < ntiles; t += gridDim.x, k ^= 1) {
-        const int tn = t + gridDim.x;
-        if (tn < ntiles) {
-            const int c = tn % C, r = tn / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-            load_plane<TI, IN_PL, false>(smem + (k ^ 1) * plane, in + b * fs, g, c, tx * kDenTW + g.dx0,
-                                         ty * TH + g.dy0);
-        }
-        cp_async_commit_();
-        cp_async_wait_one_();
-        __syncthreads();
-        const int c = t % C, r = t / C, tx = r % tiles_x, r2 = r / tiles_x, ty = r2 % tiles_y, b = r2 / tiles_y;
-        float acc[KR][8];
-        stencil_block<D, KR>(acc, smem + k * plane + row0 * g.pitch + col0 + dl.col_shift, g.pitch, dl);
-        store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty * TH + row0, tx * kDenTW + col0, acc);
-        __syncthreads();
-    }
-}
-
-// HWC-input dense stencil with all channels per CTA (first layer of a chain):
-// the tile rows are contiguous runs of W*C floats in the interleaved image, so
-// they stage with coalesced 4-byte cp.async and stay interleaved in shared
-// memory; windows read with a stride of C words, conflict-free because the
-// pixel pitch is odd and KR is odd (C odd or 1).  Writes planar fp32.
-constexpr int kHWX = 2, kHWY = 2;                  // 128 threads, tile 64 x 80
-constexpr int kHTW = kHWX * 32, kHTH = kHWY * 8 * kDenKR;
-
-template <int D, int C>
-__global__ void __launch_bounds__(kHWX *kHWY * 32)
-    layer_stencil_hwc_kernel(const float *__restrict__ in, float *__restrict__ out, const LGeom g,
-                             const __grid_constant__ DenseList dl) {
-    extern __shared__ __align__(16) float smem[];
-    constexpr int KR = kDenKR;
-    const int b = blockIdx.z;
-    const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = blockIdx.x * kHTW, ty0 = blockIdx.y * kHTH;
-    const int gx0 = tx0 + g.dx0, gy0 = ty0 + g.dy0;
-    const float *frame = in + b * fs;
-    const bool clamp = g.boundary == SKC_CLAMP;
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        const int rowlen = g.pitch * C;
-        if (gx0 >= 0 && gx0 + g.pitch <= g.W && gy0 >= 0 && gy0 + g.rows <= g.H) {
-            // interior tile: every tile row is one contiguous run of pitch * C floats
-            const float *sx = frame + ((long long)(gy0 + warp) * g.W + gx0) * C + lane;
-            unsigned sd = (unsigned)__cvta_generic_to_shared(smem + warp * rowlen + lane);
-            const long long gstep = (long long)nw * g.W * C;
-            const unsigned sstep = 4u * nw * rowlen;
-            for (int r = warp; r < g.rows; r += nw, sx += gstep, sd += sstep) {
-                const float *p = sx;
-                unsigned q = sd;
-#pragma unroll 4
-                for (int e = lane; e < rowlen; e += 32, p += 32, q += 128) cp_async4s(q, p);
-            }
-            cp_async_wait_all();
-        } else
-        for (int r = warp; r < g.rows; r += nw) {
-            int gy = gy0 + r;
-            const bool rowin = clamp || (gy >= 0 && gy < g.H);
-            gy = min(max(gy, 0), g.H - 1);
-            const float *src = frame + (long long)gy * g.W * C;
-            float *dst = smem + r * rowlen;
-#pragma unroll 4
-            for (int e = lane; e < rowlen; e += 32) {
-                const int col = e / C, c = e - col * C;
-                const int gx = gx0 + col;
-                const bool ok = clamp || (rowin && gx >= 0 && gx < g.W);
-                cp_async4(dst + e, src + (long long)min(max(gx, 0), g.W - 1) * C + c, ok);
-            }
-        }
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kHWX, wy = warp / kHWX;
-    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
-    const int rs = g.pitch * C;   // row stride in words
-#pragma unroll 1
-    for (int c = 0; c < C; ++c) {
-        const float *pc = smem + row0 * rs + (col0 + dl.col_shift) * C + c;
-        float acc[KR][8];
-#pragma unroll
-        for (int i = 0; i < KR; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll
-        for (int r = 0; r < KR + D - 1; ++r) {
-            float w[8 + D - 1];
-#pragma unroll
-            for (int j = 0; j < 8 + D - 1; ++j) w[j] = pc[r * rs + j * C];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                const int i = r - a;
-                if (i < 0 || i >= KR) continue;
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) {
-                    const float k = dl.k[a * D + bb];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
-                }
-            }
-        }
-        store_block<KR, float, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
-    }
-}
-
-// Stencil-row loop for planar fp32 inputs (D = 7 / 9): each thread owns a
-// 3 x 8 block; a loop over the stencil rows a (unrolled by 3, so the window
-// rows rotate by register renaming) keeps rows a .. a+2 of the input window
-// in registers, loads one new 16-word row per step and issues 3*D*8 FFMAs
-// with the row's weights.  The body is ~11 KB instead of the ~52 KB fully
-// unrolled (KR+D-1)-row body (instruction-fetch stalls), with no padding
-// waste.
-constexpr int kAlKR = 3, kAlWX = 4, kAlWY = 2;       // 256 threads, tile 128 x 48
-constexpr int kAlTW = kAlWX * 32, kAlTH = kAlWY * 8 * kAlKR;
-
-template <int D, typename TO, bool OUT_PL>
-__global__ void __launch_bounds__(kAlWX *kAlWY * 32, 3)
-    layer_stencil_aloop_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
-                               const __grid_constant__ DenseList dl) {
-    extern __shared__ __align__(16) float smem[];
-    constexpr int KR = kAlKR, WN = 8 + D - 1;
-    const int C = g.C;
-    const int b = blockIdx.z, c = blockIdx.x % C;
-    const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = (blockIdx.x / C) * kAlTW, ty0 = blockIdx.y * kAlTH;
-    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kAlWX, wy = warp / kAlWX;
-    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
-    const int pitch = g.pitch;
-    const float *pc = smem + row0 * pitch + col0 + dl.col_shift;
-
-    float acc[KR][8];
-#pragma unroll
-    for (int i = 0; i < KR; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-    float w[KR][WN];
-#pragma unroll
-    for (int i = 0; i < KR - 1; ++i)
-#pragma unroll
-        for (int j = 0; j < WN; ++j) w[i + 1][j] = pc[i * pitch + j];
-#pragma unroll 3
-    for (int a = 0; a < D; ++a) {
-        // rotate: rows a .. a+KR-1 (renamed away by the unroll)
-#pragma unroll
-        for (int i = 0; i < KR - 1; ++i)
-#pragma unroll
-            for (int j = 0; j < WN; ++j) w[i][j] = w[i + 1][j];
-        const float *q = pc + (a + KR - 1) * pitch;
-#pragma unroll
-        for (int j = 0; j < WN; ++j) w[KR - 1][j] = q[j];
-        const float *kr = dl.k + a * D;
-#pragma unroll
-        for (int bb = 0; bb < D; ++bb) {
-            const float k = kr[bb];
-#pragma unroll
-            for (int i = 0; i < KR; ++i)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[i][j + bb], acc[i][j]);
-        }
-    }
-    store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
-}
-
-// Row-rolled dense stencil for planar fp32 inputs (large D): each thread owns a
-// KR=3 x 8 block; a runtime loop walks the window rows in groups of KR, and
-// input row r feeds output row i through stencil row r - i, the table being
-// zero-padded above and below so every (r, i) pair is an unconditional FFMA.
-// Keeps the unrolled body at KR*KR*D*8 FFMAs (instruction-cache resident,
-// unlike the fully unrolled (KR+D-1)-row body for D = 9) and uses an odd row
-// pitch, which makes the per-lane LDS.32 window reads conflict-free
-// (3 * pitch odd -> 8 lane rows hit 8 distinct banks mod 8).
-constexpr int kRollKR = 3, kRlWX = 4, kRlWY = 2;    // 256 threads, tile 128 x 48
-constexpr int kRlTW = kRlWX * 32, kRlTH = kRlWY * 8 * kRollKR;
-constexpr int kRollRows = kMaxDense + 3 * kRollKR;  // padded stencil rows
-
-struct RollList {
-    float k[kRollRows * kMaxDense];  // row (a + KR - 1) holds K[a][.], zero outside 0 <= a < D
-    int D;
-    int col_shift;
-};
-
-__host__ __device__ constexpr int roll_rows_padded(int D) {
-    return ((D + kRollKR - 1 + kRollKR - 1) / kRollKR) * kRollKR;
-}
-
-template <int D, typename TO, bool OUT_PL>
-__global__ void __launch_bounds__(kRlWX *kRlWY * 32, 2)
-    layer_stencil_roll_kernel(const float *__restrict__ in, TO *__restrict__ out, const LGeom g,
-                              const __grid_constant__ RollList rl) {
-    extern __shared__ __align__(16) float smem[];
-    constexpr int KR = kRollKR, RP = roll_rows_padded(D);
-    const int C = g.C;
-    const int b = blockIdx.z, c = blockIdx.x % C;
-    const long long fs = (long long)g.H * g.W * C;
-    const int tx0 = (blockIdx.x / C) * kRlTW, ty0 = blockIdx.y * kRlTH;
-    load_plane4(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = lane & 3, ly = lane >> 2, wx = warp % kRlWX, wy = warp / kRlWX;
-    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
-    const int pitch = g.pitch;
-    const float *pc = smem + row0 * pitch + col0 + rl.col_shift;
-
-    float acc[KR][8];
-#pragma unroll
-    for (int i = 0; i < KR; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-#pragma unroll 1
-    for (int r0 = 0; r0 < RP; r0 += KR) {
-#pragma unroll
-        for (int u = 0; u < KR; ++u) {
-            const float *q = pc + (r0 + u) * pitch;
-            float w[8 + D - 1];
-#pragma unroll
-            for (int j = 0; j < 8 + D - 1; ++j) w[j] = q[j];
-#pragma unroll
-            for (int i = 0; i < KR; ++i) {
-                const float *kr = rl.k + (r0 + u - i + KR - 1) * D;
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) {
-                    const float k = kr[bb];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(k, w[j + bb], acc[i][j]);
-                }
-            }
-        }
-    }
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
@@ -1014,63 +656,6 @@ static int tap_kr_override() {
     return v;
 }
 
-// SKC_TAP_PIPE=1 selects the persistent double-buffered tap kernel for planar
-// inputs.  Off by default: on B200 it measured slower than independent CTAs
-// (config 3 layers 4.0 vs 2.35 ms, config 1 tap layers 5.6 vs 4.1 ms) because
-// the doubled tile buffer halves the resident CTAs per SM.
-static int tap_pipe_mode() {
-    static const int v = [] {
-        const char *e = std::getenv("SKC_TAP_PIPE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-// SKC_TAP_CLUSTER=1 enables the cluster HWC epilogue.  Opt-in: on config 1
-// the clustered last layer took 7.28 ms against 4.39 ms + 0.89 ms for the
-// planar layer + relayout pass (scalar DSMEM gathers and the two cluster
-// barriers cost more than the relayout's extra HBM pass).
-static bool tap_cluster_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_TAP_CLUSTER");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
-template <int KR, typename TO, int C>
-static int launch_tap_cl(const float *in, TO *out, int B, int H, int W, const LGeom &g, const TapList &tl,
-                         size_t smem, cudaStream_t s) {
-    auto kern = layer_tap_cl_kernel<KR, TO, C>;
-    static int attr = set_smem_attr(kern);
-    if (attr) return attr;
-    constexpr int TH = kTWY * 8 * KR;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
-    cfg.blockDim = dim3(kTWX * kTWY * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    SKC_CUDA(cudaLaunchKernelEx(&cfg, kern, in, out, g, tl));
-    SKC_LAUNCH_CHECK("layer_tap_cl_kernel");
-    return SKC_OK;
-}
-
-// SKC_TAP_SHFL=1: ninth window column by warp shuffle (see tap_rows).
-static bool tap_shfl_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_TAP_SHFL");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
 // Rows per thread of the tap tile for a layer of `ntaps` taps with the given
 // corner footprint (see tap_kr_override).
 static int tap_kr_for(int H, int W, int C, int boundary, int accumulate, int dx_min, int dx_max, int dy_min,
@@ -1114,47 +699,6 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
-    if constexpr (IN_PL && !OUT_PL) {
-        if (!accumulate && (C == 3 || C == 4) && tap_cluster_enabled() && smem <= (size_t)kMaxSmem) {
-            const int rc = C == 3 ? (KR == 7 ? launch_tap_cl<7, TO, 3>(pin, pout, B, H, W, g, tl, smem, s)
-                                             : launch_tap_cl<5, TO, 3>(pin, pout, B, H, W, g, tl, smem, s))
-                                  : (KR == 7 ? launch_tap_cl<7, TO, 4>(pin, pout, B, H, W, g, tl, smem, s)
-                                             : launch_tap_cl<5, TO, 4>(pin, pout, B, H, W, g, tl, smem, s));
-            return rc;
-        }
-    }
-    if constexpr (IN_PL) {
-        const int mode = tap_pipe_mode();
-        if ((mode == 1 || (mode < 0 && tl.n <= 12)) && 2 * smem <= (size_t)kMaxSmem) {
-            const int tiles_x = ceil_div(W, kTTW), tiles_y = ceil_div(H, TH);
-            const long long nt = (long long)tiles_x * tiles_y * B * C;
-            if (nt < (1LL << 31)) {
-                const int per_sm = std::max(1, std::min(4, (int)((size_t)kMaxSmem / (2 * smem))));
-                const int grid = (int)std::min<long long>(nt, 148LL * per_sm);
-                auto kern = KR == 7 ? layer_tap_pipe_kernel<7, TO, OUT_PL> : layer_tap_pipe_kernel<5, TO, OUT_PL>;
-                static int a5 = set_smem_attr(layer_tap_pipe_kernel<5, TO, OUT_PL>);
-                static int a7 = set_smem_attr(layer_tap_pipe_kernel<7, TO, OUT_PL>);
-                if (a5 || a7) return a5 ? a5 : a7;
-                kern<<<grid, kTWX * kTWY * 32, 2 * smem, s>>>(reinterpret_cast<const float *>(pin), pout, g, tl,
-                                                                tiles_x, tiles_y, (int)nt);
-                SKC_LAUNCH_CHECK("layer_tap_pipe_kernel");
-                return SKC_OK;
-            }
-        }
-    }
-    if constexpr (IN_PL) {
-        if (tap_shfl_enabled() && smem <= (size_t)kMaxSmem) {
-            auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL, true>
-                                : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL, true>;
-            static int sa5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL, true>);
-            static int sa7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL, true>);
-            if (sa5 || sa7) return sa5 ? sa5 : sa7;
-            dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
-            kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
-            SKC_LAUNCH_CHECK("layer_tap_kernel");
-            return SKC_OK;
-        }
-    }
     if (smem <= (size_t)kMaxSmem) {
         auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>;
         static int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
@@ -1172,36 +716,45 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     return SKC_OK;
 }
 
-// SKC_STENCIL_PIPE=1: persistent double-buffered stencil (tile loads overlap compute).
-static bool stencil_pipe_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_STENCIL_PIPE");
-        return e && e[0] == '1';
+// Packed-FP32 (FFMA2) stencil: default for planar inner layers with D >= 7
+// (config 1, D = 9: 2.18 ms against 2.59 ms); SKC_STENCIL_FFMA2=1 forces it
+// for every stencil, =0 disables it.
+static int stencil_ffma2_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_STENCIL_FFMA2");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
     return v;
+}
+
+template <int D, int SH>
+static int launch_stencil2_d(const void *in, void *out, int B, int C, const DenseList2 &dl, const LGeom &g,
+                             cudaStream_t s) {
+    auto kern = layer_stencil2_kernel<D, SH>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    dim3 grid(ceil_div(g.W, kDenTW) * C, ceil_div(g.H, kF2TH), B);
+    kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), g, dl);
+    SKC_LAUNCH_CHECK("layer_stencil2_kernel");
+    return SKC_OK;
+}
+
+static int launch_stencil2(const void *in, void *out, int B, int C, int D, const DenseList2 &dl, const LGeom &g,
+                           cudaStream_t s) {
+    const bool odd = dl.col_shift & 1;
+    switch (D) {
+        case 3: return odd ? launch_stencil2_d<3, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<3, 0>(in, out, B, C, dl, g, s);
+        case 5: return odd ? launch_stencil2_d<5, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<5, 0>(in, out, B, C, dl, g, s);
+        case 7: return odd ? launch_stencil2_d<7, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<7, 0>(in, out, B, C, dl, g, s);
+        default: return odd ? launch_stencil2_d<9, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<9, 0>(in, out, B, C, dl, g, s);
+    }
 }
 
 template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int C, const DenseList &dl,
                             const LGeom &g, cudaStream_t s) {
     const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
-    if constexpr (KR == kDenKR) {
-        if (stencil_pipe_enabled() && 2 * smem <= (size_t)kMaxSmem) {
-            const int tiles_x = ceil_div(W, kDenTW), tiles_y = ceil_div(H, kDenWY * 8 * KR);
-            const long long nt = (long long)tiles_x * tiles_y * B * C;
-            if (nt < (1LL << 31)) {
-                auto pk = layer_stencil_pipe_kernel<D, TI, TO, IN_PL, OUT_PL>;
-                static int pattr = set_smem_attr(pk);
-                if (pattr) return pattr;
-                const int per_sm = std::max(1, std::min(4, (int)((size_t)kMaxSmem / (2 * smem))));
-                const int grid = (int)std::min<long long>(nt, 148LL * per_sm);
-                pk<<<grid, kDenWX * kDenWY * 32, 2 * smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out),
-                                                                g, dl, tiles_x, tiles_y, (int)nt);
-                SKC_LAUNCH_CHECK("layer_stencil_pipe_kernel");
-                return SKC_OK;
-            }
-        }
-    }
     auto kern = layer_stencil_kernel<D, KR, TI, TO, IN_PL, OUT_PL>;
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
@@ -1209,102 +762,6 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
     kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);
     SKC_LAUNCH_CHECK("layer_stencil_kernel");
     return SKC_OK;
-}
-
-template <int D, typename TO, bool OUT_PL>
-static int launch_stencil_roll_d(const void *in, void *out, int B, int C, const RollList &rl, const LGeom &g,
-                                 cudaStream_t s) {
-    auto kern = layer_stencil_roll_kernel<D, TO, OUT_PL>;
-    static int attr = set_smem_attr(kern);
-    if (attr) return attr;
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
-    dim3 grid(ceil_div(g.W, kRlTW) * C, ceil_div(g.H, kRlTH), B);
-    kern<<<grid, kRlWX * kRlWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<TO *>(out), g, rl);
-    SKC_LAUNCH_CHECK("layer_stencil_roll_kernel");
-    return SKC_OK;
-}
-
-template <int D, typename TO, bool OUT_PL>
-static int launch_stencil_aloop_d(const void *in, void *out, int B, int C, const DenseList &dl, const LGeom &g,
-                                  cudaStream_t s) {
-    auto kern = layer_stencil_aloop_kernel<D, TO, OUT_PL>;
-    static int attr = set_smem_attr(kern);
-    if (attr) return attr;
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
-    dim3 grid(ceil_div(g.W, kAlTW) * C, ceil_div(g.H, kAlTH), B);
-    kern<<<grid, kAlWX * kAlWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<TO *>(out), g, dl);
-    SKC_LAUNCH_CHECK("layer_stencil_aloop_kernel");
-    return SKC_OK;
-}
-
-// SKC_STENCIL_ALOOP=1 selects the stencil-row loop for planar D >= 7
-// (config 1, D = 9: 2.597 ms vs 2.586 ms for the fully unrolled kernel once
-// the tile loader was fixed; kept as the smaller-code alternative).
-static bool aloop_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_STENCIL_ALOOP");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
-// SKC_STENCIL_ROLL=1 selects the row-rolled stencil for planar D >= 7 inputs
-// (measured slower than the unrolled one on config 1: 3.79 vs 2.78 ms).
-static bool roll_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_STENCIL_ROLL");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
-// SKC_STENCIL_HWC=1 selects the all-channel HWC-input stencil for chain heads
-// (measured slower than the per-channel one on config 1: 2.80 vs 2.09 ms).
-static bool stencil_hwc_enabled() {
-    static const bool v = [] {
-        const char *e = std::getenv("SKC_STENCIL_HWC");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
-
-// Rows per thread of the planar stencil: SKC_STENCIL_KR = 3 (odd pitch,
-// conflict-free LDS.32, a smaller unrolled body) or 5 (default).
-static int stencil_kr() {
-    static const int v = [] {
-        const char *e = std::getenv("SKC_STENCIL_KR");
-        return e && std::atoi(e) == 3 ? 3 : 5;
-    }();
-    return v;
-}
-
-template <int D, int C>
-static int launch_stencil_hwc_dc(const void *in, void *out, int B, const DenseList &dl, const LGeom &g, size_t smem,
-                                 cudaStream_t s) {
-    auto kern = layer_stencil_hwc_kernel<D, C>;
-    static int attr = set_smem_attr(kern);
-    if (attr) return attr;
-    dim3 grid(ceil_div(g.W, kHTW), ceil_div(g.H, kHTH), B);
-    kern<<<grid, kHWX * kHWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), g, dl);
-    SKC_LAUNCH_CHECK("layer_stencil_hwc_kernel");
-    return SKC_OK;
-}
-
-template <int C>
-static int launch_stencil_hwc_c(const void *in, void *out, int B, int D, const DenseList &dl, const LGeom &g,
-                                size_t smem, cudaStream_t s) {
-    switch (D) {
-        case 3: return launch_stencil_hwc_dc<3, C>(in, out, B, dl, g, smem, s);
-        case 5: return launch_stencil_hwc_dc<5, C>(in, out, B, dl, g, smem, s);
-        case 7: return launch_stencil_hwc_dc<7, C>(in, out, B, dl, g, smem, s);
-        default: return launch_stencil_hwc_dc<9, C>(in, out, B, dl, g, smem, s);
-    }
-}
-
-static int launch_stencil_hwc(const void *in, void *out, int B, int D, int C, const DenseList &dl, const LGeom &g,
-                              size_t smem, cudaStream_t s) {
-    return C == 3 ? launch_stencil_hwc_c<3>(in, out, B, D, dl, g, smem, s)
-                  : launch_stencil_hwc_c<1>(in, out, B, D, dl, g, smem, s);
 }
 
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
@@ -1323,56 +780,24 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
         }
     dl.D = D;
     for (int e = 0; e < kMaxDense * kMaxDense; ++e) dl.k[e] = e < D * D ? (float)k[e] : 0.f;
-    if constexpr (!IN_PL && OUT_PL && std::is_same<TI, float>::value) {
-        if ((C == 3 || C == 1) && stencil_hwc_enabled()) {
-            LGeom h = make_geom(H, W, C, boundary, 0, kHTW, kHTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
+    // planar inner layers: packed-FP32 stencil (default for D >= 7, forced by
+    // SKC_STENCIL_FFMA2=1, disabled by =0)
+    if constexpr (IN_PL && OUT_PL && std::is_same<TO, float>::value) {
+        const int f2mode = stencil_ffma2_mode();
+        if (f2mode == 1 || (f2mode < 0 && D >= 7)) {
+            LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kF2TH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
                                 pl.dy_min + D - 1);
-            h.pitch |= 1;   // odd pixel pitch: conflict-free strided windows
-            dl.col_shift = pl.dx_min - h.dx0;
-            const size_t smem = (size_t)h.rows * h.pitch * C * sizeof(float);
-            if (smem <= (size_t)kMaxSmem) {
-                *rc = launch_stencil_hwc(in, out, B, D, C, dl, h, smem, s);
-                return true;
-            }
-        }
-    }
-    if constexpr (IN_PL) {
-        if (D >= 7 && aloop_enabled() && !roll_enabled()) {
-            LGeom a = make_geom(H, W, C, boundary, 0, kAlTW, kAlTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
-                                pl.dy_min + D - 1);
-            dl.col_shift = pl.dx_min - a.dx0;
-            *rc = D == 7 ? launch_stencil_aloop_d<7, TO, OUT_PL>(in, out, B, C, dl, a, s)
-                         : launch_stencil_aloop_d<9, TO, OUT_PL>(in, out, B, C, dl, a, s);
-            return true;
-        }
-        if (D >= 7 && roll_enabled()) {
-            LGeom r = make_geom(H, W, C, boundary, 0, kRlTW, kRlTH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
-                                pl.dy_min + D - 1);
-            r.pitch |= 1;                                            // odd pitch: conflict-free LDS.32
-            r.rows = kRlTH - kRollKR + (D == 7 ? roll_rows_padded(7) : roll_rows_padded(9));
-            RollList rl;
-            std::memset(&rl, 0, sizeof(rl));
-            rl.D = D;
-            rl.col_shift = pl.dx_min - r.dx0;
-            for (int a = 0; a < D; ++a)
-                for (int bb = 0; bb < D; ++bb) rl.k[(a + kRollKR - 1) * D + bb] = (float)k[a * D + bb];
-            *rc = D == 7 ? launch_stencil_roll_d<7, TO, OUT_PL>(in, out, B, C, rl, r, s)
-                         : launch_stencil_roll_d<9, TO, OUT_PL>(in, out, B, C, rl, r, s);
-            return true;
-        }
-    }
-    if constexpr (IN_PL && std::is_same<TO, float>::value && OUT_PL) {
-        if (stencil_kr() == 3) {
-            LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenWY * 8 * 3, pl.dx_min, pl.dx_min + D - 1,
-                                pl.dy_min, pl.dy_min + D - 1);
-            g.pitch |= 1;
-            dl.col_shift = pl.dx_min - g.dx0;
-            switch (D) {
-                case 3: *rc = launch_stencil_d<3, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-                case 5: *rc = launch_stencil_d<5, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-                case 7: *rc = launch_stencil_d<7, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-                default: *rc = launch_stencil_d<9, 3, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
-            }
+            DenseList2 d2;
+            std::memset(&d2, 0, sizeof(d2));
+            d2.D = D;
+            d2.col_shift = pl.dx_min - g.dx0;
+            for (int a = 0; a <= D; ++a)
+                for (int bb = 0; bb < D; ++bb) {
+                    const float hi = a < D ? (float)k[a * D + bb] : 0.f;
+                    const float lo = a > 0 ? (float)k[(a - 1) * D + bb] : 0.f;
+                    d2.k2[a * D + bb] = make_float2(hi, lo);
+                }
+            *rc = launch_stencil2(in, out, B, C, D, d2, g, s);
             return true;
         }
     }
@@ -1605,12 +1030,11 @@ static bool tap_hwc_stage_enabled() {
     return v;
 }
 
-// Would a chain's last layer (planar fp32 in, HWC out) run a tap kernel that
-// writes HWC itself (staged epilogue, or the cluster one)?  Mirrors the
-// routing of layer_t -> try_stencil -> launch_taps.
+// Would a chain's last layer (planar fp32 in, HWC out) run the tap kernel,
+// which writes HWC itself through its staged epilogue?  Mirrors the routing
+// of layer_t -> try_stencil -> launch_taps.
 static bool last_layer_direct(int H, int W, int C, const double *taps, int S, int boundary) {
-    const bool cluster = tap_cluster_enabled() && (C == 3 || C == 4);
-    if ((!cluster && !tap_hwc_stage_enabled()) || S > kLMaxTaps) return false;
+    if (!tap_hwc_stage_enabled() || S > kLMaxTaps) return false;
     const Plan pl = plan_taps(taps, S);
     if (dense_allowed()) {
         const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
@@ -1629,7 +1053,7 @@ static bool last_layer_direct(int H, int W, int C, const double *taps, int S, in
 }
 
 // The chain's I/O passes (see chain_policy); by default the output relayout
-// is skipped when the last layer runs the cluster HWC epilogue.
+// is skipped when the last layer runs the tap kernel's staged HWC epilogue.
 static void chain_io(const double *taps, const int *layout, int L, long long total, int H, int W, int C,
                      int in_dtype, int boundary, bool *pre, bool *post) {
     const int pol = chain_policy(in_dtype);

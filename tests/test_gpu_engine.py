@@ -233,13 +233,11 @@ def test_dense_and_tap_paths_agree(skc, orc):
             assert normwise(dense_out, taps_out) < 2e-6
 
 
-def test_rolled_stencil_inner_layers(skc, orc):
-    """Inner (planar) layers with D = 5 / 7 / 9 footprints: the default fully
-    unrolled stencil and the opt-in variants (SKC_STENCIL_ROLL=1 row-rolled,
-    SKC_STENCIL_ALOOP=1 stencil-row loop, SKC_STENCIL_KR=3 odd pitch,
-    SKC_STENCIL_HWC=1 all-channel HWC chain head, SKC_STENCIL_PIPE=1
-    persistent double-buffered) all
-    match the oracle and each other on ragged sizes and both boundaries."""
+def test_stencil_variants_inner_layers(skc, orc):
+    """Inner (planar) layers with D = 3 / 5 / 7 / 9 footprints: the default
+    (packed-FP32 FFMA2 stencil for D >= 7, classic FFMA stencil below) and the
+    switches SKC_STENCIL_FFMA2=0 (classic everywhere) / =1 (FFMA2 everywhere)
+    all match the oracle and each other on ragged sizes and both boundaries."""
     import os
     import subprocess
     import sys
@@ -247,7 +245,7 @@ def test_rolled_stencil_inner_layers(skc, orc):
     from pathlib import Path
     rng = np.random.default_rng(77)
     layers = []
-    for reach, n in ((1.9, 16), (3.9, 32), (2.9, 24), (3.9, 40)):   # D = 5, 9, 7, 9
+    for reach, n in ((1.9, 16), (3.9, 32), (1.9, 16), (0.9, 12), (2.9, 24), (3.9, 40)):   # D = 5, 9, 5, 3, 7, 9
         off = rng.uniform(-reach, reach, (n, 2))
         w = rng.random(n)
         layers.append(skc.SparseLayer(off, w / w.sum()))
@@ -268,8 +266,7 @@ def test_rolled_stencil_inner_layers(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                for var in ({"SKC_STENCIL_ROLL": "1"}, {"SKC_STENCIL_ALOOP": "1"}, {"SKC_STENCIL_KR": "3"},
-                            {"SKC_STENCIL_HWC": "1"}, {"SKC_STENCIL_PIPE": "1"}):
+                for var in ({"SKC_STENCIL_FFMA2": "0"}, {"SKC_STENCIL_FFMA2": "1"}):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6, var
@@ -301,12 +298,11 @@ def test_chain_io_policies_agree(skc):
             assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
 
 
-def test_cluster_hwc_epilogue(skc, orc):
+def test_hwc_epilogue(skc, orc):
     """A chain whose last layer is a tap layer writes HWC straight from the
-    tap kernel (default: staged epilogue; SKC_TAP_CLUSTER=1: C-CTA cluster
-    with DSMEM) instead of planar + relayout (SKC_TAP_HWC_STAGE=0); all three
-    agree bit for bit and match the oracle, for C = 3 / 4, fp32 / fp16
-    storage, ragged sizes and both boundaries."""
+    tap kernel's staged epilogue instead of planar + relayout
+    (SKC_TAP_HWC_STAGE=0); both agree bit for bit and match the oracle, for
+    C = 3 / 4, fp32 / fp16 storage, ragged sizes and both boundaries."""
     import os
     import subprocess
     import sys
@@ -335,7 +331,7 @@ def test_cluster_hwc_epilogue(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                for var in ({"SKC_TAP_CLUSTER": "1"}, {"SKC_TAP_HWC_STAGE": "0"}, {"SKC_TAP_SHFL": "1"}):
+                for var in ({"SKC_TAP_HWC_STAGE": "0"},):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy")), var
