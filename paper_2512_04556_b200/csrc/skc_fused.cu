@@ -213,19 +213,12 @@ __global__ void __launch_bounds__(kF2Threads) fused2_kernel(const float *__restr
 int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_pl, int B, int H, int W,
              int C, cudaStream_t s);
 
-// Host: eligibility, plan and launch (relayout -> fused planar chain ->
-// relayout).  Returns -1 when the chain is not eligible.
-int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
-                const double *taps, const int *layout, int L, int boundary, cudaStream_t s, bool dry) {
-    // Opt-in (SKC_FUSED=1): on B200 the fused launch (1 CTA/SM at 186 KB of
-    // planes, 2x redundant halo work) measured slower than the unfused
-    // planar chain for config 3 (24.9 vs 15.9 ms for 32 frames).
-    static const bool enabled = [] {
-        const char *e = std::getenv("SKC_FUSED");
-        return e && e[0] == '1';
-    }();
-    if (!enabled || L < 2 || L > kF2MaxL || B > 65535) return -1;
-    F2Params q;
+// Plan one fused group of layers (taps/layout point at its first layer):
+// fills q, the plane pitch/rows and the shared-memory size.  Returns false
+// when the group is not eligible.
+static bool plan_fused(const double *taps, const int *layout, int L, int H, int W, int C, int boundary,
+                       F2Params &q, int &pitch, int &rows, size_t &smem) {
+    if (L < 1 || L > kF2MaxL) return false;
     std::memset(&q, 0, sizeof(q));
     q.H = H;
     q.W = W;
@@ -235,7 +228,7 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
     std::vector<int> dxmin(L), dxmax(L), dymin(L), dymax(L);
     const double *tp = taps;
     for (int l = 0; l < L; ++l) {
-        if (layout[l] > kF2MaxTaps) return -1;
+        if (layout[l] > kF2MaxTaps) return false;
         F2Layer &F = q.layer[l];
         F.n = layout[l];
         for (int i = 0; i < F.n; ++i) {
@@ -268,20 +261,20 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
     // every rectangle must contain the tile (footprints straddle the origin),
     // so clamped edge texels are always computed
     for (int l = 0; l <= L; ++l)
-        if (nx0[l] > 0 || ny0[l] > 0 || nx1[l] < kF2TW || ny1[l] < kF2TH) return -1;
+        if (nx0[l] > 0 || ny0[l] > 0 || nx1[l] < kF2TW || ny1[l] < kF2TH) return false;
     // keep the plane origin even so 8-byte loads and LDS.64 windows align
     q.hlx = -nx0[0] + ((-nx0[0]) & 1);
     q.hly = -ny0[0];
     q.in_w = nx1[0] + q.hlx;
     q.in_h = ny1[0] - ny0[0];
     const double redund = (double)(nx1[0] - nx0[0]) * q.in_h / (kF2TW * kF2TH);
-    if (redund > 4.0) return -1;
-    int pitch = q.in_w + 10;          // odd-tap windows read 9 columns past the block origin
+    if (redund > 4.0) return false;
+    pitch = q.in_w + 10;          // odd-tap windows read 9 columns past the block origin
     pitch = (pitch + 3) & ~3;
-    pitch += 2;                       // pitch = 2 mod 4
-    const int rows = q.in_h + kF2KR + 1;
-    const size_t smem = 2 * (size_t)rows * pitch * sizeof(float);
-    if (smem > (size_t)kMaxSmem) return -1;
+    pitch += 2;                   // pitch = 2 mod 4
+    rows = q.in_h + kF2KR + 1;
+    smem = 2 * (size_t)rows * pitch * sizeof(float);
+    if (smem > (size_t)kMaxSmem) return false;
     for (int l = 0; l < L; ++l) {
         F2Layer &F = q.layer[l];
         F.x0 = nx0[l + 1] + q.hlx;
@@ -302,30 +295,65 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
             }
         }
     }
+    return true;
+}
+
+// Layers per fused launch: SKC_FUSED_GROUP (default: the whole chain).
+static int fused_group() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_FUSED_GROUP");
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    return v;
+}
+
+// Host: eligibility, plan and launch (relayout -> fused planar groups ->
+// relayout).  Returns -1 when the chain is not eligible.
+int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C,
+                const double *taps, const int *layout, int L, int boundary, cudaStream_t s, bool dry) {
+    // Opt-in (SKC_FUSED=1): on B200 the fused launch (1 CTA/SM at 186 KB of
+    // planes, 2x redundant halo work) measured slower than the unfused
+    // planar chain for config 3 (24.9 vs 15.9 ms for 32 frames).
+    static const bool enabled = [] {
+        const char *e = std::getenv("SKC_FUSED");
+        return e && e[0] == '1';
+    }();
+    if (!enabled || L < 2 || B > 65535) return -1;
+    const int G = fused_group() ? fused_group() : L;
+    const int ng = (L + G - 1) / G;
+    std::vector<F2Params> qs(ng);
+    std::vector<int> pitches(ng), rowss(ng);
+    std::vector<size_t> smems(ng);
+    const double *tp = taps;
+    for (int gi = 0; gi < ng; ++gi) {
+        const int l0 = gi * G, nl = std::min(G, L - l0);
+        if (!plan_fused(tp, layout + l0, nl, H, W, C, boundary, qs[gi], pitches[gi], rowss[gi], smems[gi]))
+            return -1;
+        for (int l = l0; l < l0 + nl; ++l) tp += 3 * layout[l];
+    }
     if (dry) return SKC_OK;
 
-    // planar staging around the fused launch
+    // planar staging around the fused launches (ping-pong between groups)
     const size_t n = (size_t)B * H * W * C;
-    void *pin = nullptr, *pout = nullptr;
-    int rc = pool_alloc(&pin, n * sizeof(float), s);
+    void *buf[2] = {nullptr, nullptr};
+    int rc = pool_alloc(&buf[0], n * sizeof(float), s);
     if (rc) return rc;
-    if ((rc = pool_alloc(&pout, n * sizeof(float), s))) { pool_free(pin, s); return rc; }
-    rc = relayout(in, idt, false, pin, SKC_F32, true, B, H, W, C, s);
-    if (rc == SKC_OK) {
-        static cudaError_t attr =
-            cudaFuncSetAttribute(fused2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-        if (attr != cudaSuccess) {
-            rc = cuda_fail(attr, "cudaFuncSetAttribute(fused2)");
-        } else {
-            dim3 grid(ceil_div(W, kF2TW) * C, ceil_div(H, kF2TH), B);
-            fused2_kernel<<<grid, kF2Threads, smem, s>>>((const float *)pin, (float *)pout, q, pitch, rows);
-            cudaError_t e = cudaGetLastError();
-            if (e != cudaSuccess) rc = cuda_fail(e, "fused2_kernel");
-        }
+    if ((rc = pool_alloc(&buf[1], n * sizeof(float), s))) { pool_free(buf[0], s); return rc; }
+    rc = relayout(in, idt, false, buf[0], SKC_F32, true, B, H, W, C, s);
+    static cudaError_t attr =
+        cudaFuncSetAttribute(fused2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (rc == SKC_OK && attr != cudaSuccess) rc = cuda_fail(attr, "cudaFuncSetAttribute(fused2)");
+    int k = 0;
+    for (int gi = 0; gi < ng && rc == SKC_OK; ++gi, k ^= 1) {
+        dim3 grid(ceil_div(W, kF2TW) * C, ceil_div(H, kF2TH), B);
+        fused2_kernel<<<grid, kF2Threads, smems[gi], s>>>((const float *)buf[k], (float *)buf[k ^ 1], qs[gi],
+                                                          pitches[gi], rowss[gi]);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "fused2_kernel");
     }
-    if (rc == SKC_OK) rc = relayout(pout, SKC_F32, true, out, odt, false, B, H, W, C, s);
-    pool_free(pin, s);
-    pool_free(pout, s);
+    if (rc == SKC_OK) rc = relayout(buf[k], SKC_F32, true, out, odt, false, B, H, W, C, s);
+    pool_free(buf[0], s);
+    pool_free(buf[1], s);
     return rc;
 }
 

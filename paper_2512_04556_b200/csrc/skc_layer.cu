@@ -521,8 +521,11 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     store_block<KR, float, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, res);
 }
 
+// Register caps (4 CTAs per SM, 3 for D = 3 whose body otherwise hoists its
+// window loads into 80-104 registers and halves the resident CTAs of these
+// HBM-bound layers; at the 64-register cap it would spill).
 template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
-__global__ void __launch_bounds__(kDenWX *kDenWY * 32)
+__global__ void __launch_bounds__(kDenWX *kDenWY * 32, D == 3 ? 3 : 4)
     layer_stencil_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
                          const __grid_constant__ DenseList dl) {
     extern __shared__ __align__(16) float smem[];
