@@ -505,8 +505,17 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) {
                 const float2 kk = dl.k2[a * D + bb];
+                if (a == 0) {         // only row 2pp has a term (K[0][b]); scalar FFMA on that half
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[pp][j] = ffma2(kk, make_float2(w[j + bb], w[j + bb]), acc[pp][j]);
+                    for (int j = 0; j < 8; ++j) acc[pp][j].x = fmaf(kk.x, w[j + bb], acc[pp][j].x);
+                } else if (a == D) {  // only row 2pp+1 (K[D-1][b])
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[pp][j].y = fmaf(kk.y, w[j + bb], acc[pp][j].y);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        acc[pp][j] = ffma2(kk, make_float2(w[j + bb], w[j + bb]), acc[pp][j]);
+                }
             }
         }
     }
