@@ -73,13 +73,15 @@ int skc_layer_fwd(const void *in, int in_dtype, void *out, int out_dtype,
                   const double *taps, int S, int boundary, void *stream);
 
 /* memory layouts for skc_layer_fwd_ex: HWC interleaved (the reference's) or
- * planar CHW (the chain's internal fp32 intermediate layout) */
+ * planar CHW (the chain's internal intermediate layout: fp32, or fp16 in
+ * fp16-storage chains, see skc_chain_mid_dtype) */
 #define SKC_HWC 0
 #define SKC_CHW 1
 
 /*
  * skc_layer_fwd with explicit layouts: in/out each (B, H, W, C) HWC or
- * (B, C, H, W) planar.  Planar tensors must be fp32.  This is the per-layer
+ * (B, C, H, W) planar.  Planar tensors are fp32, or fp16 with fp16 on the
+ * other side too (at most skc_max_taps() taps).  This is the per-layer
  * step skc_chain_fwd runs (first layer HWC -> CHW, inner CHW -> CHW, last
  * CHW -> HWC), exposed so callers can drive/time layers individually.
  */
@@ -101,17 +103,33 @@ int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int
 
 /* Which kernel family skc_layer_fwd(_ex) runs for this layer with the default
  * switches: *kind = 0 tap tile (*param = rows per thread KR), 1 dense stencil
- * (*param = D), 2 direct gather.  Lets callers compute a launch's algorithmic
+ * (*param = D), 2 direct gather, 3 generated sparse stencil (*param = nonzero
+ * positions; planar-input layers, see skc_sparse_compile_check).  Lets callers compute a launch's algorithmic
  * shared-memory traffic (bench roofline). */
 int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary, int *kind, int *param);
 
-/* Layout/dtype conversion HWC <-> planar fp32 (the chain's bracketing passes). */
+/* Wide-footprint layers with planar input run a sparse stencil generated for
+ * the layer (weights as immediates) and compiled at run time with NVRTC
+ * (skc_sparse.cu).  This compiles the kernel the layer would run without a
+ * device: 0 = compiled, 1 = the layer does not take that path, SKC_ECUDA = the
+ * run-time compiler is missing or rejected it (skc_last_error). */
+int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int out_dtype, int out_layout);
+
+/* Dtype of skc_chain_fwd's planar intermediates for this chain: SKC_F16 when
+ * in and out are both fp16 ("fp16 storage, fp32 accumulation": every layer
+ * accumulates in fp32 and rounds once on store) and no layer exceeds
+ * skc_max_taps(), else SKC_F32 (SKC_HALF_MID=0 forces fp32).  Lets callers
+ * drive the chain's launches themselves.  Negative on bad arguments. */
+int skc_chain_mid_dtype(const int *layout, int L, int in_dtype, int out_dtype);
+
+/* Layout/dtype conversion HWC <-> planar (fp32, or fp16 <-> fp16): the chain's
+ * bracketing passes. */
 int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype,
                  int out_layout, int B, int H, int W, int C, void *stream);
 
 /*
  * A chain of L layers (engine.apply_complex, engine.py:173-178).  Intermediate
- * images stay fp32 in pool scratch; only `in` and `out` use the given dtypes.
+ * images stay in pool scratch, planar, in skc_chain_mid_dtype's dtype.
  *   taps   : HOST float64 (sum(layout), 3), layers concatenated in order
  *   layout : HOST int32 (L,) taps per layer
  */

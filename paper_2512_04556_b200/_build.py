@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libskc.so"
-SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_fused.cu", "skc_fit.cu"]
+SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_sparse.cu", "skc_fused.cu", "skc_fit.cu"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = [OBJ / (Path(s).stem + ".o") for s in SOURCES]
     if force or jobs or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

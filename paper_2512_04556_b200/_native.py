@@ -28,7 +28,7 @@ FIT_HDR = 8
 
 # Symbols declared in include/skc.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_layer_plan",
+    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check",
     "skc_chain_fwd",
     "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step",
@@ -78,6 +78,8 @@ def _declare(lib):
     lib.skc_relayout.argtypes = [_vp, _i, _i, _vp, _i, _i, _i, _i, _i, _i, _vp]
     lib.skc_chain_is_fused.argtypes = [_dp, _ip, _i, _i, _i, _i, _i]
     lib.skc_chain_relayouts.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i]
+    lib.skc_chain_mid_dtype.argtypes = [_ip, _i, _i, _i]
+    lib.skc_sparse_compile_check.argtypes = [_dp, _i, _i, _i, _i]
     lib.skc_layer_plan.argtypes = [_dp, _i, _i, _i, _i, _i, _ip, _ip]
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,

@@ -136,6 +136,34 @@ __device__ __forceinline__ bool tile_rows_any(unsigned sd, const float *sx, int 
     }
 }
 
+// Planar fp16 interior rows: each lane moves NCH half2 pairs of two rows per
+// iteration (2 * NCH independent 4-byte loads in flight), widened to fp32
+// with 8-byte shared stores.  (A cp.async variant staging the raw pairs
+// behind the fp32 tile measured slower on config 3: 1.5x shared memory per
+// CTA costs a resident CTA per SM; 19.1 vs 21.0 Gpix/s.)
+template <int NCH>
+__device__ __forceinline__ void half_rows(float *s, const __half *src, int lane, int np, int r0, int rows, int nw,
+                                          int spitch, int W) {
+    const int sstep = nw * spitch;
+    const long long gstep = (long long)nw * W;
+    for (int r = r0; r < rows; r += 2 * nw, s += 2 * sstep, src += 2 * gstep) {
+        const bool two = r + nw < rows;
+        __half2 v[2][NCH];
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) {
+            const bool in = u < NCH - 1 || lane + 32 * u < np;
+            if (in) v[0][u] = __ldg(reinterpret_cast<const __half2 *>(src + 64 * u));
+            if (in && two) v[1][u] = __ldg(reinterpret_cast<const __half2 *>(src + gstep + 64 * u));
+        }
+#pragma unroll
+        for (int u = 0; u < NCH; ++u) {
+            const bool in = u < NCH - 1 || lane + 32 * u < np;
+            if (in) *reinterpret_cast<float2 *>(s + 64 * u) = __half22float2(v[0][u]);
+            if (in && two) *reinterpret_cast<float2 *>(s + sstep + 64 * u) = __half22float2(v[1][u]);
+        }
+    }
+}
+
 // One channel plane of the halo tile into s[rows][pitch].  `frame` points at
 // the (H, W, C) HWC frame or the (C, H, W) planar frame.
 template <typename TI, bool PLANAR, bool WAIT = true>
@@ -144,7 +172,45 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const bool clamp = g.boundary == SKC_CLAMP;
     const int H = g.H, W = g.W, C = g.C;
-    if constexpr (PLANAR) {
+    if constexpr (PLANAR && sizeof(TI) == 2) {
+        // planar fp16 intermediates (fp16-storage chains): through registers
+        const __half *plane = reinterpret_cast<const __half *>(frame) + (long long)c * H * W;
+        const bool pairs_ok = (W & 1) == 0;  // gx0 is even: 4-byte aligned pairs
+        const int np = g.pitch >> 1;
+        if (pairs_ok && gx0 >= 0 && gx0 + g.pitch <= W && gy0 >= 0 && gy0 + g.rows <= H) {
+            float *sd = s + warp * g.pitch + 2 * lane;
+            const __half *sx = plane + (long long)(gy0 + warp) * W + gx0 + 2 * lane;
+            switch ((np + 31) >> 5) {
+                case 1: half_rows<1>(sd, sx, lane, np, warp, g.rows, nw, g.pitch, W); return;
+                case 2: half_rows<2>(sd, sx, lane, np, warp, g.rows, nw, g.pitch, W); return;
+                case 3: half_rows<3>(sd, sx, lane, np, warp, g.rows, nw, g.pitch, W); return;
+                case 4: half_rows<4>(sd, sx, lane, np, warp, g.rows, nw, g.pitch, W); return;
+                case 5: half_rows<5>(sd, sx, lane, np, warp, g.rows, nw, g.pitch, W); return;
+                default: break;
+            }
+        }
+        for (int r = warp; r < g.rows; r += nw) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const __half *src = plane + (long long)gy * W;
+            float *dst = s + r * g.pitch;
+            for (int p = lane; p < np; p += 32) {
+                const int col = 2 * p, gx = gx0 + col;
+                if (pairs_ok && rowin && gx >= 0 && gx + 1 < W) {
+                    *reinterpret_cast<float2 *>(dst + col) =
+                        __half22float2(__ldg(reinterpret_cast<const __half2 *>(src + gx)));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int x = gx + u;
+                        const bool ok = clamp || (rowin && x >= 0 && x < W);
+                        dst[col + u] = ok ? __half2float(__ldg(src + min(max(x, 0), W - 1))) : 0.f;
+                    }
+                }
+            }
+        }
+    } else if constexpr (PLANAR) {
         static_assert(sizeof(TI) == 4, "planar intermediates are fp32");
         const float *plane = reinterpret_cast<const float *>(frame) + (long long)c * H * W;
         const bool pairs_ok = (W & 1) == 0;  // 8-byte alignment of row starts
@@ -254,6 +320,12 @@ __device__ __forceinline__ void load_plane(float *s, const TI *__restrict__ fram
     }
 }
 
+// Shared memory of a layer kernel: the fp32 tile.
+template <typename TI, bool IN_PL>
+static size_t tile_smem(const LGeom &g) {
+    return (size_t)g.rows * g.pitch * sizeof(float);
+}
+
 // Store a KR x 8 block of one channel.
 template <int KR, typename TO, bool PLANAR>
 __device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom &g, int c, int gy0,
@@ -263,7 +335,24 @@ __device__ __forceinline__ void store_block(TO *__restrict__ frame, const LGeom 
     for (int r = 0; r < KR; ++r) {
         const int gy = gy0 + r;
         if (gy >= H) continue;
-        if constexpr (PLANAR) {
+        if constexpr (PLANAR && sizeof(TO) == 2) {
+            // planar fp16 intermediates: one 16-byte store of 8 halves per row
+            TO *p = frame + ((long long)c * H + gy) * W + gx0;
+            if (gx0 + 7 < W && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+                uint4 t;
+                unsigned *tw = reinterpret_cast<unsigned *>(&t);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const __half2 h = __floats2half2_rn(acc[r][2 * k], acc[r][2 * k + 1]);
+                    tw[k] = *reinterpret_cast<const unsigned *>(&h);
+                }
+                *reinterpret_cast<uint4 *>(p) = t;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (gx0 + j < W) IO<TO>::st(p + j, acc[r][j]);
+            }
+        } else if constexpr (PLANAR) {
             float *row = reinterpret_cast<float *>(frame) + ((long long)c * H + gy) * W;
             float *p = row + gx0;
             if (gx0 + 7 < W && ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && !g.accumulate) {
@@ -457,9 +546,9 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // Planar fp32 in and out (the chain's inner layers).  SH = col_shift & 1:
 // window rows are read with LDS.64 from the 8-byte-aligned column at or before
 // the window start.
-template <int D, int SH>
+template <int D, int SH, typename T>
 __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
-    layer_stencil2_kernel(const float *__restrict__ in, float *__restrict__ out, const LGeom g,
+    layer_stencil2_kernel(const T *__restrict__ in, T *__restrict__ out, const LGeom g,
                           const __grid_constant__ DenseList2 dl) {
     extern __shared__ __align__(16) float smem[];
     constexpr int KR = kF2KR, NP = KR / 2;
@@ -467,7 +556,7 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
     const int b = blockIdx.z, c = blockIdx.x % C;
     const long long fs = (long long)g.H * g.W * C;
     const int tx0 = (blockIdx.x / C) * kDenTW, ty0 = blockIdx.y * kF2TH;
-    load_plane<float, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    load_plane<T, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -527,7 +616,7 @@ __global__ void __launch_bounds__(kDenWX *kDenWY * 32)
             res[2 * pp][j] = acc[pp][j].x;
             res[2 * pp + 1][j] = acc[pp][j].y;
         }
-    store_block<KR, float, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, res);
+    store_block<KR, T, true>(out + b * fs, g, c, ty0 + row0, tx0 + col0, res);
 }
 
 // Register caps (4 CTAs per SM, 3 for D = 3 whose body otherwise hoists its
@@ -708,7 +797,7 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
             ++k;
         }
     }
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    const size_t smem = tile_smem<TI, IN_PL>(g);
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
     if (smem <= (size_t)kMaxSmem) {
@@ -739,34 +828,35 @@ static int stencil_ffma2_mode() {
     return v;
 }
 
-template <int D, int SH>
+template <int D, int SH, typename T>
 static int launch_stencil2_d(const void *in, void *out, int B, int C, const DenseList2 &dl, const LGeom &g,
                              cudaStream_t s) {
-    auto kern = layer_stencil2_kernel<D, SH>;
+    auto kern = layer_stencil2_kernel<D, SH, T>;
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    const size_t smem = tile_smem<T, true>(g);
     dim3 grid(ceil_div(g.W, kDenTW) * C, ceil_div(g.H, kF2TH), B);
-    kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), g, dl);
+    kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const T *>(in), static_cast<T *>(out), g, dl);
     SKC_LAUNCH_CHECK("layer_stencil2_kernel");
     return SKC_OK;
 }
 
+template <typename T>
 static int launch_stencil2(const void *in, void *out, int B, int C, int D, const DenseList2 &dl, const LGeom &g,
                            cudaStream_t s) {
     const bool odd = dl.col_shift & 1;
     switch (D) {
-        case 3: return odd ? launch_stencil2_d<3, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<3, 0>(in, out, B, C, dl, g, s);
-        case 5: return odd ? launch_stencil2_d<5, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<5, 0>(in, out, B, C, dl, g, s);
-        case 7: return odd ? launch_stencil2_d<7, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<7, 0>(in, out, B, C, dl, g, s);
-        default: return odd ? launch_stencil2_d<9, 1>(in, out, B, C, dl, g, s) : launch_stencil2_d<9, 0>(in, out, B, C, dl, g, s);
+        case 3: return odd ? launch_stencil2_d<3, 1, T>(in, out, B, C, dl, g, s) : launch_stencil2_d<3, 0, T>(in, out, B, C, dl, g, s);
+        case 5: return odd ? launch_stencil2_d<5, 1, T>(in, out, B, C, dl, g, s) : launch_stencil2_d<5, 0, T>(in, out, B, C, dl, g, s);
+        case 7: return odd ? launch_stencil2_d<7, 1, T>(in, out, B, C, dl, g, s) : launch_stencil2_d<7, 0, T>(in, out, B, C, dl, g, s);
+        default: return odd ? launch_stencil2_d<9, 1, T>(in, out, B, C, dl, g, s) : launch_stencil2_d<9, 0, T>(in, out, B, C, dl, g, s);
     }
 }
 
 template <int D, int KR, typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int C, const DenseList &dl,
                             const LGeom &g, cudaStream_t s) {
-    const size_t smem = (size_t)g.rows * g.pitch * sizeof(float);
+    const size_t smem = tile_smem<TI, IN_PL>(g);
     auto kern = layer_stencil_kernel<D, KR, TI, TO, IN_PL, OUT_PL>;
     static int attr = set_smem_attr(kern);
     if (attr) return attr;
@@ -794,7 +884,7 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
     for (int e = 0; e < kMaxDense * kMaxDense; ++e) dl.k[e] = e < D * D ? (float)k[e] : 0.f;
     // planar inner layers: packed-FP32 stencil (default for D >= 7, forced by
     // SKC_STENCIL_FFMA2=1, disabled by =0)
-    if constexpr (IN_PL && OUT_PL && std::is_same<TO, float>::value) {
+    if constexpr (IN_PL && OUT_PL && std::is_same<TI, TO>::value) {
         const int f2mode = stencil_ffma2_mode();
         if (f2mode == 1 || (f2mode < 0 && D >= 7)) {
             LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kF2TH, pl.dx_min, pl.dx_min + D - 1, pl.dy_min,
@@ -809,7 +899,7 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
                     const float lo = a > 0 ? (float)k[(a - 1) * D + bb] : 0.f;
                     d2.k2[a * D + bb] = make_float2(hi, lo);
                 }
-            *rc = launch_stencil2(in, out, B, C, D, d2, g, s);
+            *rc = launch_stencil2<TO>(in, out, B, C, D, d2, g, s);
             return true;
         }
     }
@@ -830,6 +920,12 @@ static int layer_t(const void *in, void *out, int B, int H, int W, int C, const 
                    int boundary, cudaStream_t s) {
     const Plan pl = plan_taps(taps, S);
     int rc = SKC_OK;
+    if constexpr (IN_PL) {  // planar input: generated sparse stencil when it is cheaper (skc_sparse.cu)
+        rc = sparse_layer(in, std::is_same<TI, float>::value, out, std::is_same<TO, float>::value, OUT_PL, B, H, W,
+                          C, taps, S, boundary, s);
+        if (rc != -1) return rc;
+        rc = SKC_OK;
+    }
     if (try_stencil<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, S, boundary, s, &rc)) return rc;
     if (S <= kLMaxTaps)
         return launch_taps<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, 0, S, boundary, 0, s);
@@ -845,10 +941,20 @@ static int layer_t(const void *in, void *out, int B, int H, int W, int C, const 
 }
 
 // Dispatch on (input dtype, output dtype, input planar, output planar).
+// Planar intermediates are fp32, or fp16 in chains whose storage is fp16 (see
+// chain_mid_dtype): the planar fp16 combinations compiled are HWC fp16 ->
+// planar fp16, planar fp16 -> planar fp16 and planar fp16 -> HWC fp16.
 int layer_dispatch(const void *in, int idt, bool in_pl, void *out, int odt, bool out_pl, int B, int H,
                    int W, int C, const double *taps, int S, int boundary, cudaStream_t s) {
-    if (in_pl && idt != SKC_F32) return fail(SKC_EBADARG, "planar intermediates are fp32");
-    if (out_pl && odt != SKC_F32) return fail(SKC_EBADARG, "planar intermediates are fp32");
+    const bool h_in = in_pl && idt == SKC_F16, h_out = out_pl && odt == SKC_F16;
+    if (h_in || h_out) {
+        if (idt != SKC_F16 || odt != SKC_F16)
+            return fail(SKC_EBADARG, "planar fp16 tensors pair with fp16 on the other side");
+        if (S > kLMaxTaps) return fail(SKC_EBADARG, "planar fp16 layers take at most skc_max_taps() taps");
+        if (in_pl && out_pl) return layer_t<__half, __half, true, true>(in, out, B, H, W, C, taps, S, boundary, s);
+        if (in_pl) return layer_t<__half, __half, true, false>(in, out, B, H, W, C, taps, S, boundary, s);
+        return layer_t<__half, __half, false, true>(in, out, B, H, W, C, taps, S, boundary, s);
+    }
     if (in_pl && out_pl) return layer_t<float, float, true, true>(in, out, B, H, W, C, taps, S, boundary, s);
     if (in_pl) {
         if (odt == SKC_F32) return layer_t<float, float, true, false>(in, out, B, H, W, C, taps, S, boundary, s);
@@ -1003,12 +1109,18 @@ int relayout(const void *in, int idt, bool in_pl, void *out, int odt, bool out_p
         case 3: relayout_kernel<3, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
         default: relayout_kernel<4, TI, TO, IP, OP><<<grid, 256, 0, s>>>((const TI *)in, (TO *)out, B, hw, vec); break; \
     }
-    if (!in_pl && out_pl) {
+    if (!in_pl && out_pl && odt == SKC_F16) {
+        if (idt != SKC_F16) return fail(SKC_EBADARG, "planar fp16 relayout takes fp16 HWC");
+        SKC_RL(__half, __half, false, true);
+    } else if (in_pl && !out_pl && idt == SKC_F16) {
+        if (odt != SKC_F16) return fail(SKC_EBADARG, "planar fp16 relayout writes fp16 HWC");
+        SKC_RL(__half, __half, true, false);
+    } else if (!in_pl && out_pl) {
         if (idt == SKC_F32) { SKC_RL(float, float, false, true); } else { SKC_RL(__half, float, false, true); }
     } else if (in_pl && !out_pl) {
         if (odt == SKC_F32) { SKC_RL(float, float, true, false); } else { SKC_RL(float, __half, true, false); }
     } else {
-        return fail(SKC_EBADARG, "relayout converts between HWC and planar fp32");
+        return fail(SKC_EBADARG, "relayout converts between HWC and planar");
     }
 #undef SKC_RL
     SKC_LAUNCH_CHECK("relayout_kernel");
@@ -1047,6 +1159,9 @@ static bool tap_hwc_stage_enabled() {
 // of layer_t -> try_stencil -> launch_taps.
 static bool last_layer_direct(int H, int W, int C, const double *taps, int S, int boundary) {
     if (!tap_hwc_stage_enabled() || S > kLMaxTaps) return false;
+    int np;
+    double wpo;
+    if (sparse_plan(taps, S, &np, &wpo)) return true;  // the sparse stencil has the same staged epilogue
     const Plan pl = plan_taps(taps, S);
     if (dense_allowed()) {
         const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
@@ -1075,6 +1190,24 @@ static void chain_io(const double *taps, const int *layout, int L, long long tot
         const double *lt = taps + 3 * (total - layout[L - 1]);
         if (last_layer_direct(H, W, C, lt, layout[L - 1], boundary)) *post = false;
     }
+}
+
+// Dtype of a chain's planar intermediates: fp16 when the chain's storage is
+// fp16 on both ends (config 3: "fp16 storage, fp32 accumulation"; each layer
+// still accumulates in fp32 and rounds once on store), else fp32.
+// SKC_HALF_MID=0 keeps fp32 intermediates for fp16 chains.
+static bool half_mid_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_HALF_MID");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+static int chain_mid_dtype(int in_dtype, int out_dtype, const int *layout, int L) {
+    if (!half_mid_enabled() || in_dtype != SKC_F16 || out_dtype != SKC_F16) return SKC_F32;
+    for (int l = 0; l < L; ++l)
+        if (layout[l] > kLMaxTaps) return SKC_F32;
+    return SKC_F16;
 }
 
 // HWC output layer with the long-layer fp16 fallback (fp32 temporary + convert).
@@ -1128,7 +1261,7 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
         return last_layer(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, B, H, W, C, taps, S, boundary, s);
     rc = layer_dispatch(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, true, B, H, W, C, taps, S,
                         boundary, s);
-    return rc == -1 ? fail(SKC_EBADARG, "planar output must be fp32") : rc;
+    return rc == -1 ? fail(SKC_EBADARG, "planar output of a long layer must be fp32") : rc;
 }
 
 int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out_dtype, int out_layout,
@@ -1136,8 +1269,6 @@ int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out
     int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, SKC_ZERO);
     if (rc) return rc;
     if (in_layout == out_layout) return fail(SKC_EBADARG, "relayout needs different layouts");
-    if ((in_layout == SKC_CHW && in_dtype != SKC_F32) || (out_layout == SKC_CHW && out_dtype != SKC_F32))
-        return fail(SKC_EBADARG, "planar tensors are fp32");
     return relayout(in, in_dtype, in_layout == SKC_CHW, out, out_dtype, out_layout == SKC_CHW, B, H, W, C,
                     (cudaStream_t)stream);
 }
@@ -1145,6 +1276,13 @@ int skc_relayout(const void *in, int in_dtype, int in_layout, void *out, int out
 int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary, int *kind, int *param) {
     if (!taps || S < 1 || H < 1 || W < 1 || C < 1 || !kind || !param) return fail(SKC_EBADARG, "bad layer arguments");
     const Plan pl = plan_taps(taps, S);
+    int np;
+    double wpo;
+    if (sparse_plan(taps, S, &np, &wpo)) {  // planar-input layers (the chain's inner and last layers)
+        *kind = 3;
+        *param = np;
+        return SKC_OK;
+    }
     if (dense_allowed()) {
         const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
         const int D = dense_size_for(std::max(sx, sy));
@@ -1188,6 +1326,11 @@ int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int
     return (pre ? 1 : 0) | (post ? 2 : 0);
 }
 
+int skc_chain_mid_dtype(const int *layout, int L, int in_dtype, int out_dtype) {
+    if (!layout || L < 1) return fail(SKC_EBADARG, "bad chain arguments");
+    return chain_mid_dtype(in_dtype, out_dtype, layout, L);
+}
+
 int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B, int H, int W,
                   int C, const double *taps, const int *layout, int L, int boundary, void *stream) {
     int rc = check_image_args(in, in_dtype, out, out_dtype, B, H, W, C, boundary);
@@ -1207,11 +1350,12 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
     bool pre, post;
     chain_io(taps, layout, L, total, H, W, C, in_dtype, boundary, &pre, &post);
+    const int mid = chain_mid_dtype(in_dtype, out_dtype, layout, L);
     const size_t n = (size_t)B * H * W * C;
     void *buf[2] = {nullptr, nullptr};
     const int nbuf = (L > 2 || post || pre) ? 2 : 1;
     for (int i = 0; i < nbuf; ++i) {
-        rc = pool_alloc(&buf[i], n * sizeof(float), s);
+        rc = pool_alloc(&buf[i], n * dtype_size(mid), s);
         if (rc) { for (int j = 0; j < i; ++j) pool_free(buf[j], s); return rc; }
     }
     const void *src = in;
@@ -1219,9 +1363,9 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     bool spl = false;
     int k = 0;  // next scratch buffer
     if (pre) {
-        rc = relayout(in, in_dtype, false, buf[0], SKC_F32, true, B, H, W, C, s);
+        rc = relayout(in, in_dtype, false, buf[0], mid, true, B, H, W, C, s);
         src = buf[0];
-        sdt = SKC_F32;
+        sdt = mid;
         spl = true;
         k = 1;
     }
@@ -1231,15 +1375,15 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
         if (last && !post) {
             rc = last_layer(src, sdt, spl, out, out_dtype, B, H, W, C, tp, layout[l], boundary, s);
         } else {
-            rc = layer_dispatch(src, sdt, spl, buf[k], SKC_F32, true, B, H, W, C, tp, layout[l], boundary, s);
+            rc = layer_dispatch(src, sdt, spl, buf[k], mid, true, B, H, W, C, tp, layout[l], boundary, s);
             src = buf[k];
-            sdt = SKC_F32;
+            sdt = mid;
             spl = true;
             k ^= 1;
         }
         tp += 3 * layout[l];
     }
-    if (rc == SKC_OK && post) rc = relayout(src, SKC_F32, true, out, out_dtype, false, B, H, W, C, s);
+    if (rc == SKC_OK && post) rc = relayout(src, sdt, true, out, out_dtype, false, B, H, W, C, s);
     for (int i = 0; i < nbuf; ++i) pool_free(buf[i], s);
     return rc;
 }

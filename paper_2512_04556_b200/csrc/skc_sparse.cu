@@ -1,0 +1,552 @@
+// skc_sparse.cu -- layer-specialised sparse stencils, generated and compiled at
+// run time with NVRTC (sm_100a).
+//
+// Reference: engine.apply_sparse_layer (engine.py:160-170) -> sample_shifted
+// (118-130) -> _accum_shift (106-115).  A uniform layer of S bilinear taps is
+// an integer stencil with at most 4S nonzero positions: the tap's 4 corners,
+// coincident corners merged in float64 and rounded once (the dense path's
+// rule, skc_layer.cu try_stencil).  For footprints wider than the 9 x 9 dense
+// kernels the tap kernel is shared-memory bound (~1.3 window words per
+// output per tap, SMEM 32 words/clk/SM against 128 FMA/clk/SM).  Knowing the
+// positions at compile time removes that bound: each thread slides down the
+// input rows of its KR x 8 output block once, loads only the columns the
+// stencil rows touching that input row need (LDS.128, conflict-free), and
+// issues one FFMA with an immediate weight per (position, output) -- no
+// per-tap window reloads, no zero work.  Config 1's radius-8 layer (32 taps ->
+// 102 positions in 15 x 17) reads ~10 words per output instead of ~41.
+//
+// The kernel source is emitted per layer (weights as hex-float immediates),
+// compiled once per process with NVRTC (dlopen'ed libnvrtc.so.12, no link-time
+// dependency), loaded with cudaLibraryLoadData and cached by source text.
+// SKC_SPARSE=0 disables the path; SKC_SPARSE=1 forces it for every eligible
+// layer regardless of the cost model; SKC_SPARSE_DUMP=<dir> writes the
+// generated sources.
+#include <dlfcn.h>
+#include <unistd.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "skc_tile.cuh"
+
+namespace skc {
+namespace {
+
+constexpr int kSpTW = 128;
+
+int env_int(const char *name, int dflt) {
+    const char *e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+// Rows per thread KR (odd: LDS.128 conflict-free with pitch = 4 mod 8; tile
+// 128 x 16 KR), barrier period in input rows (0 = none) and minimum resident
+// CTAs per SM of the generated kernel (SKC_SPARSE_KR / _SYNC / _MINB).
+int sp_kr() {
+    static const int v = [] { const int k = env_int("SKC_SPARSE_KR", 3); return (k == 1 || k == 3 || k == 5 || k == 7 || k == 9) ? k : 3; }();
+    return v;
+}
+int sp_sync() {
+    static const int v = env_int("SKC_SPARSE_SYNC", 0);
+    return v;
+}
+int sp_minb() {
+    static const int v = std::max(1, env_int("SKC_SPARSE_MINB", 2));
+    return v;
+}
+constexpr int kSpStagePitch = 132;        // staged HWC epilogue (as skc_layer.cu)
+constexpr int kSpMaxFfma = 4096;          // code-size guard: FFMAs per thread (instruction cache)
+
+struct SpPos {
+    int b;
+    float k;
+};
+
+struct SpPlan {
+    int KR = 7, TH = 112;
+    int dx_min = 0, dy_min = 0, Dx = 0, Dy = 0, npos = 0;
+    std::vector<std::vector<SpPos>> rows;  // rows[a]: nonzero (b, K) of stencil row a
+    int DX0 = 0, SH = 0, pitch = 0, nrows = 0, nw = 0;
+    double words_per_out = 0.0;            // LDS words per output (all loads / (8 * KR))
+    size_t smem = 0;
+};
+
+SpPlan make_plan(const double *taps, int S) {
+    SpPlan p;
+    p.KR = sp_kr();
+    p.TH = 16 * p.KR;
+    std::map<std::pair<int, int>, double> acc;  // (dy, dx) -> merged weight
+    for (int i = 0; i < S; ++i) {
+        const double ox = taps[3 * i], oy = taps[3 * i + 1], w = taps[3 * i + 2];
+        const double fx0 = std::floor(ox), fy0 = std::floor(oy);
+        const double fx = ox - fx0, fy = oy - fy0;
+        const int ix = (int)fx0, iy = (int)fy0;
+        acc[{iy, ix}] += w * (1.0 - fx) * (1.0 - fy);
+        acc[{iy, ix + 1}] += w * fx * (1.0 - fy);
+        acc[{iy + 1, ix}] += w * (1.0 - fx) * fy;
+        acc[{iy + 1, ix + 1}] += w * fx * fy;
+    }
+    int xmin = 1 << 30, xmax = -(1 << 30), ymin = 1 << 30, ymax = -(1 << 30);
+    for (const auto &kv : acc) {
+        if ((float)kv.second == 0.f) continue;
+        ymin = std::min(ymin, kv.first.first);
+        ymax = std::max(ymax, kv.first.first);
+        xmin = std::min(xmin, kv.first.second);
+        xmax = std::max(xmax, kv.first.second);
+    }
+    if (xmin > xmax) return p;  // all-zero layer: npos = 0
+    p.dx_min = xmin;
+    p.dy_min = ymin;
+    p.Dx = xmax - xmin + 1;
+    p.Dy = ymax - ymin + 1;
+    p.rows.assign(p.Dy, {});
+    for (const auto &kv : acc) {
+        const float k = (float)kv.second;
+        if (k == 0.f) continue;
+        p.rows[kv.first.first - ymin].push_back({kv.first.second - xmin, k});
+        ++p.npos;
+    }
+    // smem geometry: column 0 <-> global tx0 + DX0 (DX0 = dx_min floored to 4)
+    p.DX0 = xmin & ~3;
+    p.SH = xmin - p.DX0;
+    const int wmax = p.SH + p.Dx - 1 + 7;        // last window word of a thread
+    p.nw = (wmax / 4 + 1) * 4;
+    int pitch = 120 + p.nw;                        // last thread's col0 = 120
+    while (pitch % 8 != 4) ++pitch;
+    p.pitch = pitch;
+    p.nrows = p.TH + p.Dy - 1;
+    p.smem = (size_t)std::max(p.nrows * p.pitch, p.TH * kSpStagePitch) * sizeof(float);
+    // LDS words per output: per input row, the chunks the touching stencil rows need
+    long long words = 0;
+    for (int q = 0; q < p.KR + p.Dy - 1; ++q) {
+        int kmin = 1 << 30, kmax = -1;
+        for (int a = std::max(0, q - p.KR + 1); a <= std::min(p.Dy - 1, q); ++a)
+            for (const SpPos &e : p.rows[a]) {
+                kmin = std::min(kmin, p.SH + e.b);
+                kmax = std::max(kmax, p.SH + e.b + 7);
+            }
+        if (kmax >= 0) words += 4 * (kmax / 4 - kmin / 4 + 1);
+    }
+    p.words_per_out = (double)words / (8.0 * p.KR);
+    return p;
+}
+
+int sparse_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_SPARSE");
+        return e ? (e[0] == '0' ? 0 : (e[0] == '1' ? 1 : -1)) : -1;
+    }();
+    return v;
+}
+
+// Eligibility + cost model (per output and channel, in SM clocks): the tap
+// kernel at KR = 7 reads S * 72 / 56 words (32 words/clk) and issues 4S FFMAs
+// (128/clk), shared-memory bound; the sparse stencil issues npos FFMAs and
+// reads words_per_out words.  Taken when clearly cheaper (< 0.8x).
+// Footprints the dense kernels cover (D <= 9 with D^2 < 4S, skc_layer.cu
+// try_stencil) run sparse only when it skips enough zeros: npos < 0.8 D^2.
+bool eligible(const SpPlan &p, int S) {
+    const int mode = sparse_mode();
+    if (mode == 0 || p.npos == 0) return false;
+    if ((long long)p.npos * p.KR * 8 > kSpMaxFfma) return false;
+    if (p.smem > (size_t)kMaxSmem) return false;
+    if (mode == 1) return true;
+    const int D = dense_size_for(std::max(p.Dx, p.Dy));
+    if (D != 0 && D * D < 4 * S) return p.npos < 0.8 * D * D;
+    const double tap = S * (7 + 1) * 9.0 / (7 * 8.0) / 32.0;  // the tap kernel at KR = 7
+    const double sp = std::max(p.npos / 128.0, p.words_per_out / 32.0);
+    return sp < 0.8 * tap;
+}
+
+// ------------------------------------------------------------ generator ---
+const char *kSpPrelude = R"CUDA(
+typedef unsigned short half_t;
+__device__ __forceinline__ float h2f(unsigned h) { float f; asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"((unsigned short)h)); return f; }
+__device__ __forceinline__ half_t f2h(float f) { half_t h; asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
+__device__ __forceinline__ float ldx(const float *p) { return __ldg(p); }
+__device__ __forceinline__ float ldx(const half_t *p) { return h2f(__ldg(p)); }
+__device__ __forceinline__ void stx(float *p, float v) { *p = v; }
+__device__ __forceinline__ void stx(half_t *p, float v) { *p = f2h(v); }
+__device__ __forceinline__ void cp4(float *dst, const float *src, int n) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp16(float *dst, const float *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+}
+
+extern "C" __global__ void __launch_bounds__(256, MINB)
+skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W, int C, int clamp) {
+    extern __shared__ __align__(16) float smem[];
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const long long hw = (long long)H * W;
+    const int tx0 = (blockIdx.x / C) * 128, ty0 = blockIdx.y * TH;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {   // halo tile of channel plane c: rows [ty0 + DY0, +ROWS), cols [tx0 + DX0, +PITCH)
+        const TI *plane = in + ((long long)b * C + c) * hw;
+        const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
+        if (IN_F32 && (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W && gy0 >= 0 && gy0 + ROWS <= H) {
+            const float *src = (const float *)plane + (long long)(gy0 + warp) * W + gx0;
+            float *dst = smem + warp * PITCH;
+            for (int r = warp; r < ROWS; r += 8, src += 8LL * W, dst += 8 * PITCH)
+#pragma unroll
+                for (int u = 0; u < (PITCH / 4 + 31) / 32; ++u)
+                    if (lane + 32 * u < PITCH / 4) cp16(dst + 4 * (lane + 32 * u), src + 4 * (lane + 32 * u));
+        } else {
+            for (int r = warp; r < ROWS; r += 8) {
+                int gy = gy0 + r;
+                const bool rowin = clamp || (gy >= 0 && gy < H);
+                gy = min(max(gy, 0), H - 1);
+                const TI *src = plane + (long long)gy * W;
+                float *dst = smem + r * PITCH;
+                if (IN_F32) {
+                    for (int col = lane; col < PITCH; col += 32) {
+                        const int gx = gx0 + col;
+                        const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                        cp4(dst + col, (const float *)src + min(max(gx, 0), W - 1), ok ? 4 : 0);
+                    }
+                } else if (rowin && (W & 1) == 0 && gx0 >= 0 && gx0 + PITCH <= W) {
+                    const unsigned *s2 = (const unsigned *)(src + gx0);
+                    for (int p = lane; p < PITCH / 2; p += 32) {
+                        const unsigned v = __ldg(s2 + p);
+                        *(float2 *)(dst + 2 * p) = make_float2(h2f(v & 0xffffu), h2f(v >> 16));
+                    }
+                } else {
+                    for (int col = lane; col < PITCH; col += 32) {
+                        const int gx = gx0 + col;
+                        const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                        dst[col] = ok ? ldx(src + min(max(gx, 0), W - 1)) : 0.f;
+                    }
+                }
+            }
+        }
+        asm volatile("cp.async.wait_all;");
+    }
+    __syncthreads();
+    const int lx = lane & 3, ly = lane >> 2, wx = warp & 3, wy = warp >> 2;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    const float *base = smem + row0 * PITCH + col0;
+)CUDA";
+
+const char *kSpPlanarEpilogue = R"CUDA(
+    TO *o = out + ((long long)b * C + c) * hw;
+    const int gx = tx0 + col0;
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        const int gy = ty0 + row0 + i;
+        if (gy >= H) continue;
+        TO *p = o + (long long)gy * W + gx;
+        if (OUT_F32) {
+            if (gx + 7 < W && (W & 3) == 0) {
+                ((float4 *)p)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                ((float4 *)p)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+                continue;
+            }
+        } else if (gx + 7 < W && (W & 7) == 0) {
+            uint4 t;
+            t.x = (unsigned)f2h(acc[i][0]) | ((unsigned)f2h(acc[i][1]) << 16);
+            t.y = (unsigned)f2h(acc[i][2]) | ((unsigned)f2h(acc[i][3]) << 16);
+            t.z = (unsigned)f2h(acc[i][4]) | ((unsigned)f2h(acc[i][5]) << 16);
+            t.w = (unsigned)f2h(acc[i][6]) | ((unsigned)f2h(acc[i][7]) << 16);
+            *(uint4 *)p = t;
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (gx + j < W) stx(p + j, acc[i][j]);
+    }
+}
+)CUDA";
+
+const char *kSpHwcEpilogue = R"CUDA(
+    __syncthreads();  // every warp is done reading the input tile
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        float4 *d = (float4 *)(smem + (row0 + i) * 132 + col0);
+        d[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        d[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+    __syncthreads();
+    const int nx = min(128, W - tx0), nr = min(TH, H - ty0);
+    for (int r = warp; r < nr; r += 8) {
+        TO *dst = out + (((long long)b * H + ty0 + r) * W + tx0) * C + c;
+        const float *srow = smem + r * 132;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = lane + 32 * u;
+            if (x < nx) stx(dst + (long long)x * C, srow[x]);
+        }
+    }
+}
+)CUDA";
+
+std::string hexf(float v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%af", (double)v);
+    return buf;
+}
+
+std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl) {
+    std::ostringstream s;
+    s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
+      << "\n";
+    s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
+    s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n";
+    s << "#define MINB " << sp_minb() << "\n";
+    s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
+      << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
+    s << kSpPrelude;
+    // scalar accumulators a<i>_<j> and window words w<k> (not arrays: the front
+    // end's array scalarisation is ~10x slower on bodies of this size)
+    s << "    float";
+    for (int i = 0; i < p.KR; ++i)
+        for (int j = 0; j < 8; ++j) s << (i || j ? ", " : " ") << "a" << i << "_" << j << " = 0.f";
+    s << ";\n    float";
+    for (int k = 0; k < p.nw; ++k) s << (k ? ", " : " ") << "w" << k;
+    s << ";\n";
+    const int sync = sp_sync();
+    for (int q = 0; q < p.KR + p.Dy - 1; ++q) {
+        if (sync > 0 && q > 0 && q % sync == 0) s << "    __syncthreads();\n";
+        const int a_lo = std::max(0, q - p.KR + 1), a_hi = std::min(p.Dy - 1, q);
+        int kmin = 1 << 30, kmax = -1;
+        for (int a = a_lo; a <= a_hi; ++a)
+            for (const SpPos &e : p.rows[a]) {
+                kmin = std::min(kmin, p.SH + e.b);
+                kmax = std::max(kmax, p.SH + e.b + 7);
+            }
+        if (kmax < 0) continue;
+        s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
+        for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
+            s << "        { const float4 t = rp[" << ch << "]; w" << 4 * ch << " = t.x; w" << 4 * ch + 1
+              << " = t.y; w" << 4 * ch + 2 << " = t.z; w" << 4 * ch + 3 << " = t.w; }\n";
+        for (int a = a_lo; a <= a_hi; ++a) {
+            const int i = q - a;
+            for (const SpPos &e : p.rows[a]) {
+                const std::string k = hexf(e.k);
+                for (int j = 0; j < 8; ++j)
+                    s << "        a" << i << "_" << j << " = fmaf(" << k << ", w" << p.SH + e.b + j << ", a" << i << "_" << j
+                      << ");\n";
+            }
+        }
+        s << "    }\n";
+    }
+    s << "    float acc[KR][8];\n";
+ for (int i = 0; i < p.KR; ++i)
+        for (int j = 0; j < 8; ++j) s << "    acc[" << i << "][" << j << "] = a" << i << "_" << j << ";\n";
+    s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+    return s.str();
+}
+
+// ---------------------------------------------------------------- NVRTC ---
+struct Nvrtc {
+    bool ok = false;
+    std::string why;
+    nvrtcResult (*create)(nvrtcProgram *, const char *, const char *, int, const char *const *,
+                          const char *const *) = nullptr;
+    nvrtcResult (*compile)(nvrtcProgram, int, const char *const *) = nullptr;
+    nvrtcResult (*log_size)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*get_log)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*cubin_size)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*get_cubin)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*destroy)(nvrtcProgram *) = nullptr;
+};
+
+Nvrtc &nvrtc() {
+    static Nvrtc n = [] {
+        Nvrtc r;
+        void *h = nullptr;
+        for (const char *name : {"libnvrtc.so.12", "libnvrtc.so"})
+            if ((h = dlopen(name, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!h) {
+            r.why = std::string("dlopen libnvrtc: ") + dlerror();
+            return r;
+        }
+        r.create = (decltype(r.create))dlsym(h, "nvrtcCreateProgram");
+        r.compile = (decltype(r.compile))dlsym(h, "nvrtcCompileProgram");
+        r.log_size = (decltype(r.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+        r.get_log = (decltype(r.get_log))dlsym(h, "nvrtcGetProgramLog");
+        r.cubin_size = (decltype(r.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+        r.get_cubin = (decltype(r.get_cubin))dlsym(h, "nvrtcGetCUBIN");
+        r.destroy = (decltype(r.destroy))dlsym(h, "nvrtcDestroyProgram");
+        r.ok = r.create && r.compile && r.log_size && r.get_log && r.cubin_size && r.get_cubin && r.destroy;
+        if (!r.ok) r.why = "libnvrtc lacks an expected symbol";
+        return r;
+    }();
+    return n;
+}
+
+// Compile `src` to an sm_100a cubin; empty on failure (reason in *why).
+std::vector<char> compile_cubin(const std::string &src, std::string *why) {
+    if (const char *dir = std::getenv("SKC_SPARSE_DUMP")) {
+        static int seq = 0;
+        const std::string path = std::string(dir) + "/skc_sparse_" + std::to_string(seq++) + ".cu";
+        if (FILE *f = std::fopen(path.c_str(), "w")) {
+            std::fwrite(src.data(), 1, src.size(), f);
+            std::fclose(f);
+        }
+    }
+    Nvrtc &n = nvrtc();
+    if (!n.ok) {
+        *why = n.why;
+        return {};
+    }
+    nvrtcProgram prog;
+    if (n.create(&prog, src.c_str(), "skc_sparse.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+        *why = "nvrtcCreateProgram failed";
+        return {};
+    }
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
+    const nvrtcResult rc = n.compile(prog, 4, opts);
+    std::vector<char> cubin;
+    if (rc != NVRTC_SUCCESS) {
+        size_t ls = 0;
+        n.log_size(prog, &ls);
+        std::string log(ls, '\0');
+        if (ls) n.get_log(prog, &log[0]);
+        *why = "nvrtc compile failed: " + log;
+    } else {
+        size_t cs = 0;
+        n.cubin_size(prog, &cs);
+        cubin.resize(cs);
+        n.get_cubin(prog, cubin.data());
+    }
+    n.destroy(&prog);
+    return cubin;
+}
+
+// On-disk cubin cache (a cold cache only costs compile time): $SKC_CACHE_DIR,
+// else $XDG_CACHE_HOME/skc, else $HOME/.cache/skc; keyed by an FNV-1a hash
+// and the length of the generated source.
+std::string cache_path(const std::string &src) {
+    std::string dir;
+    if (const char *d = std::getenv("SKC_CACHE_DIR")) dir = d;
+    else if (const char *x = std::getenv("XDG_CACHE_HOME")) dir = std::string(x) + "/skc";
+    else if (const char *h = std::getenv("HOME")) dir = std::string(h) + "/.cache/skc";
+    else return "";
+    if (dir.empty() || dir == "0") return "";
+    unsigned long long hsh = 1469598103934665603ULL;
+    for (unsigned char ch : src) hsh = (hsh ^ ch) * 1099511628211ULL;
+    char name[96];
+    std::snprintf(name, sizeof name, "/sparse_sm100a_%016llx_%zu.cubin", hsh, src.size());
+    std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+    (void)!std::system(mk.c_str());
+    return dir + name;
+}
+
+std::vector<char> cached_cubin(const std::string &src, std::string *why) {
+    const std::string path = cache_path(src);
+    if (!path.empty()) {
+        if (FILE *f = std::fopen(path.c_str(), "rb")) {
+            std::vector<char> buf;
+            char tmp[65536];
+            size_t n;
+            while ((n = std::fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+            std::fclose(f);
+            if (!buf.empty()) return buf;
+        }
+    }
+    std::vector<char> cubin = compile_cubin(src, why);
+    if (!cubin.empty() && !path.empty()) {
+        const std::string tmpp = path + ".tmp" + std::to_string((long long)getpid());
+        if (FILE *f = std::fopen(tmpp.c_str(), "wb")) {
+            const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+            std::fclose(f);
+            if (ok) std::rename(tmpp.c_str(), path.c_str());
+            else std::remove(tmpp.c_str());
+        }
+    }
+    return cubin;
+}
+
+struct SpKernel {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    bool failed = false;
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, SpKernel> g_cache;
+
+// The compiled kernel for `src` (compiling on first use); nullptr when the
+// run-time compiler is unavailable or failed (the caller takes the tap path).
+cudaKernel_t get_kernel(const std::string &src, size_t smem) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_cache.find(src);
+    if (it != g_cache.end()) return it->second.failed ? nullptr : it->second.kern;
+    SpKernel k;
+    std::string why;
+    const std::vector<char> cubin = cached_cubin(src, &why);
+    if (cubin.empty() ||
+        cudaLibraryLoadData(&k.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&k.kern, k.lib, "skc_sparse_stencil") != cudaSuccess ||
+        cudaFuncSetAttribute((const void *)k.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        k.failed = true;
+        if (std::getenv("SKC_SPARSE_VERBOSE")) std::fprintf(stderr, "skc sparse stencil unavailable: %s\n", why.c_str());
+    }
+    g_cache.emplace(src, k);
+    return k.failed ? nullptr : k.kern;
+}
+
+}  // namespace
+
+// Plan query for skc_layer_plan: 1 and the position count / LDS words per
+// output when the layer would take the sparse path (cost model only; the
+// run-time compiler is not consulted).
+bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
+    const SpPlan p = make_plan(taps, S);
+    if (!eligible(p, S)) return false;
+    *npos = p.npos;
+    *words_per_out = p.words_per_out;
+    return true;
+}
+
+// One layer through a generated sparse stencil: planar input (fp32 or fp16),
+// planar or HWC output.  Returns -1 when the layer does not take this path
+// (ineligible, or no run-time compiler), else a status code.
+int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
+                 const double *taps, int S, int boundary, cudaStream_t s) {
+    const SpPlan p = make_plan(taps, S);
+    if (!eligible(p, S)) return -1;
+    const std::string src = generate(p, in_f32, out_f32, out_pl);
+    cudaKernel_t k = get_kernel(src, p.smem);
+    if (!k) return -1;
+    dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, p.TH), B);
+    int clamp = boundary == SKC_CLAMP ? 1 : 0;
+    void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};
+    const cudaError_t e = cudaLaunchKernel((const void *)k, grid, dim3(256), args, p.smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
+    return SKC_OK;
+}
+
+}  // namespace skc
+
+extern "C" {
+
+// Generate and compile (NVRTC, no device needed) the sparse stencil this layer
+// would run: 0 = compiled, 1 = the layer does not take the sparse path,
+// SKC_ECUDA = the run-time compiler is missing or rejected the source
+// (message in skc_last_error).
+int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int out_dtype, int out_layout) {
+    using namespace skc;
+    if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
+    const SpPlan p = make_plan(taps, S);
+    if (!eligible(p, S)) return 1;
+    std::string why;
+    const std::vector<char> cubin =
+        compile_cubin(generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW), &why);
+    return cubin.empty() ? fail(SKC_ECUDA, why) : SKC_OK;
+}
+
+}  // extern "C"

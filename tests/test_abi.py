@@ -50,3 +50,19 @@ def test_bad_arguments_fail_without_a_device():
     assert b"null" in lib.skc_last_error()
     rc = lib.skc_layer_fwd(ctypes.c_void_p(16), 0, ctypes.c_void_p(16), 0, 1, 4, 4, 7, nat.dbl(taps), 1, 0, None)
     assert rc == nat.SKC_EBADARG
+
+
+def test_sparse_stencil_compiles_without_a_device(tmp_path, monkeypatch):
+    """The generated sparse stencil of config 1's wide layers compiles with
+    NVRTC for sm_100a (no device needed), for every input/output variant."""
+    import numpy as np
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    lib = nat.load_library()
+    cpx = synth.c1_complex()
+    t = np.ascontiguousarray(cpx.layers[0].taps())
+    assert lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], nat.SKC_F32, nat.SKC_F32, nat.SKC_CHW) == 1
+    t = np.ascontiguousarray(cpx.layers[2].taps())
+    for args in ((nat.SKC_F32, nat.SKC_F32, nat.SKC_CHW), (nat.SKC_F16, nat.SKC_F16, nat.SKC_HWC)):
+        rc = lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], *args)
+        assert rc == 0, nat.last_error()

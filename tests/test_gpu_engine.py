@@ -237,7 +237,9 @@ def test_stencil_variants_inner_layers(skc, orc):
     """Inner (planar) layers with D = 3 / 5 / 7 / 9 footprints: the default
     (packed-FP32 FFMA2 stencil for D >= 7, classic FFMA stencil below) and the
     switches SKC_STENCIL_FFMA2=0 (classic everywhere) / =1 (FFMA2 everywhere)
-    all match the oracle and each other on ragged sizes and both boundaries."""
+    all match the oracle and each other on ragged sizes and both boundaries.
+    By default layers whose merged stencil skips enough zeros run the
+    generated sparse stencil instead; SKC_SPARSE=0 pins the dense kernels."""
     import os
     import subprocess
     import sys
@@ -266,7 +268,8 @@ def test_stencil_variants_inner_layers(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                for var in ({"SKC_STENCIL_FFMA2": "0"}, {"SKC_STENCIL_FFMA2": "1"}):
+                for var in ({"SKC_SPARSE": "0"}, {"SKC_STENCIL_FFMA2": "0", "SKC_SPARSE": "0"},
+                            {"SKC_STENCIL_FFMA2": "1", "SKC_SPARSE": "0"}):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert normwise(ours, np.load(f"{td}/u.npy")) < 2e-6, var
@@ -376,3 +379,138 @@ def test_fused_chain_matches_oracle_and_unfused(skc, orc):
                         outs.append(np.load(f"{td}/o{f}.npy").astype(np.float64))
                     assert normwise(outs[0], ref) < tol, (shape, mode, dt)
                     assert normwise(outs[0], outs[1]) < (1e-6 if dt == np.float32 else tol), (shape, mode)
+
+
+def test_half_intermediates(skc, orc):
+    """fp16-storage chains keep their planar intermediates in fp16
+    (skc_chain_mid_dtype; each layer accumulates in fp32 and rounds once on
+    store).  Checked against the oracle at the fp16 tolerance on ragged sizes,
+    odd widths (unpaired loads), both boundaries, the tap kernel, every
+    stencil kernel (c1's D5 head and D9 FFMA2 inner layer) and the staged HWC
+    epilogue; SKC_HALF_MID=0 (fp32 intermediates) must agree with it to the
+    same tolerance."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    lay = np.array([32, 32, 32, 32], dtype=np.int32)
+    assert nat.lib().skc_chain_mid_dtype(nat.ints(lay), 4, nat.SKC_F16, nat.SKC_F16) == nat.SKC_F16
+    assert nat.lib().skc_chain_mid_dtype(nat.ints(lay), 4, nat.SKC_F16, nat.SKC_F32) == nat.SKC_F32
+    assert nat.lib().skc_chain_mid_dtype(nat.ints(lay), 4, nat.SKC_F32, nat.SKC_F32) == nat.SKC_F32
+    long = np.array([8, 300], dtype=np.int32)
+    assert nat.lib().skc_chain_mid_dtype(nat.ints(long), 2, nat.SKC_F16, nat.SKC_F16) == nat.SKC_F32
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "x = np.load(sys.argv[1]); cpx = synth.c1_complex() if sys.argv[4] == 'c1' else synth.kawase_complex();"
+            "np.save(sys.argv[2], skc.apply_complex(x, cpx, boundary=sys.argv[3]))")
+    rng = np.random.default_rng(77)
+    with tempfile.TemporaryDirectory() as td:
+        for name, shape in (("kaw", (131, 263, 4)), ("kaw", (40, 37, 4)), ("c1", (150, 270, 3)),
+                            ("c1", (97, 129, 3)), ("kaw", (3, 2, 4))):
+            cpx = synth.c1_complex() if name == "c1" else synth.kawase_complex()
+            layers = [(l.offsets, l.weights) for l in cpx.layers]
+            x = rng.random(shape).astype(np.float16)
+            np.save(f"{td}/in.npy", x)
+            for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                ours = skc.apply_complex(x, cpx, boundary=mode)
+                assert ours.dtype == np.float16
+                ref = orc.apply_complex(x.astype(np.float64), layers, oid)
+                assert normwise(ours, ref) < TOL16, (name, shape, mode)
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/f.npy", mode, name], check=True,
+                               env=dict(os.environ, SKC_HALF_MID="0"), cwd=root)
+                f32mid = np.load(f"{td}/f.npy")
+                assert normwise(f32mid, ref) < TOL16
+                assert normwise(ours, f32mid.astype(np.float64)) < TOL16
+
+
+def test_planar_half_entry_points(skc):
+    """skc_layer_fwd_ex / skc_relayout accept planar fp16 only paired with fp16
+    and reject the mixed combinations with a status code."""
+    import torch
+    from paper_2512_04556_b200 import _native as nat
+    lib = nat.lib()
+    t = np.ascontiguousarray(np.array([[0.5, -0.25, 0.6], [-1.5, 1.0, 0.4]]))
+    x = torch.rand((2, 20, 30, 3), device="cuda").half()
+    pl = torch.empty((2, 3, 20, 30), device="cuda", dtype=torch.float16)
+    back = torch.empty_like(x)
+    s = nat.stream_ptr(torch.cuda.current_stream())
+    assert lib.skc_relayout(nat.ptr(x), nat.SKC_F16, nat.SKC_HWC, nat.ptr(pl), nat.SKC_F16, nat.SKC_CHW,
+                            2, 20, 30, 3, s) == 0
+    assert torch.equal(pl, x.permute(0, 3, 1, 2))
+    assert lib.skc_relayout(nat.ptr(pl), nat.SKC_F16, nat.SKC_CHW, nat.ptr(back), nat.SKC_F16, nat.SKC_HWC,
+                            2, 20, 30, 3, s) == 0
+    assert torch.equal(back, x)
+    o1 = torch.empty_like(pl)
+    assert lib.skc_layer_fwd_ex(nat.ptr(pl), nat.SKC_F16, nat.SKC_CHW, nat.ptr(o1), nat.SKC_F16, nat.SKC_CHW,
+                                2, 20, 30, 3, nat.dbl(t), 2, 0, s) == 0
+    o2 = torch.empty_like(x)
+    assert lib.skc_layer_fwd_ex(nat.ptr(x), nat.SKC_F16, nat.SKC_HWC, nat.ptr(o2), nat.SKC_F16, nat.SKC_HWC,
+                                2, 20, 30, 3, nat.dbl(t), 2, 0, s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2.permute(0, 3, 1, 2))
+    f32 = torch.empty((2, 3, 20, 30), device="cuda")
+    assert lib.skc_layer_fwd_ex(nat.ptr(pl), nat.SKC_F16, nat.SKC_CHW, nat.ptr(f32), nat.SKC_F32, nat.SKC_CHW,
+                                2, 20, 30, 3, nat.dbl(t), 2, 0, s) == nat.SKC_EBADARG
+    assert lib.skc_relayout(nat.ptr(x), nat.SKC_F16, nat.SKC_HWC, nat.ptr(f32), nat.SKC_F32, nat.SKC_CHW,
+                            2, 20, 30, 3, s) == 0
+
+
+def test_sparse_stencil_path(skc, orc):
+    """Wide-footprint planar layers run a sparse stencil generated for the
+    layer and compiled at run time (skc_layer_plan kind 3).  Chains whose
+    inner and last layers take it (planar and staged-HWC epilogues, fp32 and
+    fp16 storage, both boundaries, ragged and odd sizes) match the oracle, and
+    agree with the tap path (SKC_SPARSE=0) to the storage tolerance."""
+    import ctypes
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    rng = np.random.default_rng(404)
+    cpxs = [synth.c1_complex()]
+    for reach, n in ((6.0, 40), (12.0, 24), (15.5, 64)):
+        layers = [skc.SparseLayer(rng.uniform(-1.5, 1.5, (6, 2)), rng.random(6) + 0.1)]
+        off = rng.uniform(-reach, reach, (n, 2))
+        layers.append(skc.SparseLayer(off, rng.uniform(-0.2, 1.0, n)))
+        layers.append(skc.SparseLayer(-off[::-1] * 0.7, rng.random(n)))
+        cpxs.append(skc.KernelComplex(layers))
+    kinds = []
+    for cpx in cpxs:
+        for l in cpx.layers[1:]:
+            t = np.ascontiguousarray(l.taps())
+            kind, par = ctypes.c_int(), ctypes.c_int()
+            assert nat.lib().skc_layer_plan(nat.dbl(t), t.shape[0], 500, 500, 3, 0, ctypes.byref(kind),
+                                            ctypes.byref(par)) == 0
+            kinds.append(kind.value)
+    assert kinds.count(3) >= 4, kinds
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc;"
+            "d = np.load(sys.argv[1]); L = int(d['L']);"
+            "cpx = skc.KernelComplex([skc.SparseLayer(d[f'o{i}'], d[f'w{i}']) for i in range(L)]);"
+            "np.save(sys.argv[2], skc.apply_complex(d['img'], cpx, sys.argv[3]))")
+    with tempfile.TemporaryDirectory() as td:
+        for k, cpx in enumerate(cpxs):
+            layers = [(l.offsets, l.weights) for l in cpx.layers]
+            for (h, w, c, dt) in ((150, 300, 3, np.float32), (61, 131, 4, np.float16), (233, 97, 1, np.float32)):
+                img = rng.random((h, w, c)).astype(dt)
+                tol = TOL32 if dt == np.float32 else TOL16
+                for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                    ours = skc.apply_complex(img, cpx, boundary=mode)
+                    ref = orc.apply_complex(img.astype(np.float64), layers, oid)
+                    assert normwise(ours, ref) < tol, (k, h, w, c, mode)
+                    if mode == "clamp" and c != 1:
+                        continue
+                    np.savez(f"{td}/in.npz", img=img, L=len(layers),
+                             **{f"o{i}": o for i, (o, _) in enumerate(layers)},
+                             **{f"w{i}": ww for i, (_, ww) in enumerate(layers)})
+                    subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/t.npy", mode], check=True,
+                                   env=dict(os.environ, SKC_SPARSE="0"), cwd=root)
+                    assert normwise(ours, np.load(f"{td}/t.npy").astype(np.float64)) < tol
