@@ -59,8 +59,15 @@ int sp_sync() {
     static const int v = env_int("SKC_SPARSE_SYNC", 0);
     return v;
 }
+// Packed-FP32 body (default; SKC_SPARSE_F2=0 emits scalar FFMAs with
+// immediate weights): fma.rn.f32x2 on horizontal output pairs, the weight
+// broadcast as a (K, K) pair from a __constant__ table (uniform registers).
+int sp_f2() {
+    static const int v = env_int("SKC_SPARSE_F2", 1);
+    return v;
+}
 int sp_minb() {
-    static const int v = std::max(1, env_int("SKC_SPARSE_MINB", 2));
+    static const int v = std::max(1, env_int("SKC_SPARSE_MINB", 3));
     return v;
 }
 constexpr int kSpStagePitch = 132;        // staged HWC epilogue (as skc_layer.cu)
@@ -302,10 +309,89 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl) {
       << "\n";
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n";
-    s << "#define MINB " << sp_minb() << "\n";
+    s << "#define MINB " << sp_minb() << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
+    const bool f2 = sp_f2() != 0;
+    if (f2) {
+        // (K, K) pairs for fma.rn.f32x2, in position order of the body below
+        s << "__constant__ float2 KW[" << std::max(1, p.npos) << "] = {";
+        int n = 0;
+        for (int a = 0; a < p.Dy; ++a)
+            for (const SpPos &e : p.rows[a]) s << (n++ ? ", " : "") << "{" << hexf(e.k) << ", " << hexf(e.k) << "}";
+        s << "};\n";
+        s << "__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {\n"
+             "    unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a), rb = *reinterpret_cast<unsigned long long *>(&b),\n"
+             "        rc = *reinterpret_cast<unsigned long long *>(&c), rd;\n"
+             "    asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(rd) : \"l\"(ra), \"l\"(rb), \"l\"(rc));\n"
+             "    return *reinterpret_cast<float2 *>(&rd);\n}\n";
+    }
     s << kSpPrelude;
+    if (f2) {
+        // Window words as aligned pairs wp<m> = (w[2m], w[2m+1]).  A position at
+        // window column c0 feeds output j from w[c0 + j]: for even c0 the output
+        // pairs (2m, 2m+1) meet aligned window pairs; for odd c0 the pairs
+        // (2m+1, 2m+2) do, with outputs 0 and 7 as scalar FFMAs -- two
+        // accumulator sets (e: even-paired, o: odd-paired + 2 scalars), summed
+        // in the epilogue.  No register moves to re-pair the window.
+        std::vector<int> first(p.Dy + 1, 0);  // index of row a's first position in KW
+        for (int a = 0; a < p.Dy; ++a) first[a + 1] = first[a] + (int)p.rows[a].size();
+        s << "    float2";
+        for (int i = 0; i < p.KR; ++i)
+            for (int j = 0; j < 4; ++j) s << (i || j ? ", " : " ") << "e" << i << "_" << j << " = make_float2(0.f, 0.f)";
+        for (int i = 0; i < p.KR; ++i)
+            for (int j = 0; j < 3; ++j) s << ", o" << i << "_" << j << " = make_float2(0.f, 0.f)";
+        s << ";\n    float";
+        for (int i = 0; i < p.KR; ++i) s << (i ? ", " : " ") << "s" << i << "_0 = 0.f, s" << i << "_7 = 0.f";
+        s << ";\n    float2";
+        for (int m = 0; m < p.nw / 2; ++m) s << (m ? ", " : " ") << "wp" << m;
+        s << ";\n";
+        for (int q = 0; q < p.KR + p.Dy - 1; ++q) {
+            const int a_lo = std::max(0, q - p.KR + 1), a_hi = std::min(p.Dy - 1, q);
+            int kmin = 1 << 30, kmax = -1;
+            for (int a = a_lo; a <= a_hi; ++a)
+                for (const SpPos &e : p.rows[a]) {
+                    kmin = std::min(kmin, p.SH + e.b);
+                    kmax = std::max(kmax, p.SH + e.b + 7);
+                }
+            if (kmax < 0) continue;
+            s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
+            for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
+                s << "        { const float4 t = rp[" << ch << "]; wp" << 2 * ch << " = make_float2(t.x, t.y); wp"
+                  << 2 * ch + 1 << " = make_float2(t.z, t.w); }\n";
+            for (int a = a_lo; a <= a_hi; ++a) {
+                const int i = q - a;
+                for (size_t e = 0; e < p.rows[a].size(); ++e) {
+                    const int c0 = p.SH + p.rows[a][e].b;
+                    const std::string kw = "KW[" + std::to_string(first[a] + (int)e) + "]";
+                    if (c0 % 2 == 0) {
+                        for (int j = 0; j < 4; ++j)
+                            s << "        e" << i << "_" << j << " = ffma2(" << kw << ", wp" << c0 / 2 + j << ", e" << i << "_"
+                              << j << ");\n";
+                    } else {
+                        s << "        s" << i << "_0 = fmaf(" << kw << ".x, wp" << (c0 - 1) / 2 << ".y, s" << i << "_0);\n";
+                        for (int j = 0; j < 3; ++j)
+                            s << "        o" << i << "_" << j << " = ffma2(" << kw << ", wp" << (c0 + 1) / 2 + j << ", o" << i
+                              << "_" << j << ");\n";
+                        s << "        s" << i << "_7 = fmaf(" << kw << ".x, wp" << (c0 + 7) / 2 << ".x, s" << i << "_7);\n";
+                    }
+                }
+            }
+            s << "    }\n";
+        }
+        s << "    float acc[KR][8];\n";
+        for (int i = 0; i < p.KR; ++i) {
+            for (int j = 0; j < 4; ++j)
+                s << "    acc[" << i << "][" << 2 * j << "] = e" << i << "_" << j << ".x; acc[" << i << "][" << 2 * j + 1
+                  << "] = e" << i << "_" << j << ".y;\n";
+            s << "    acc[" << i << "][0] += s" << i << "_0; acc[" << i << "][7] += s" << i << "_7;\n";
+            for (int j = 0; j < 3; ++j)
+                s << "    acc[" << i << "][" << 2 * j + 1 << "] += o" << i << "_" << j << ".x; acc[" << i << "][" << 2 * j + 2
+                  << "] += o" << i << "_" << j << ".y;\n";
+        }
+        s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+        return s.str();
+    }
     // scalar accumulators a<i>_<j> and window words w<k> (not arrays: the front
     // end's array scalarisation is ~10x slower on bodies of this size)
     s << "    float";
@@ -499,17 +585,53 @@ cudaKernel_t get_kernel(const std::string &src, size_t smem) {
     return k.failed ? nullptr : k.kern;
 }
 
+// Per-layer memo (host cost per launch is a hash lookup, not a plan and a
+// 300 KB source string): keyed by the tap bytes, the variant and the knobs.
+struct SpLaunch {
+    bool eligible = false;
+    int npos = 0, TH = 0;
+    double words_per_out = 0.0;
+    size_t smem = 0;
+    cudaKernel_t kern = nullptr;  // null: the run-time compiler failed
+};
+std::mutex g_memo_mu;
+std::unordered_map<std::string, SpLaunch> g_memo;
+
+std::string memo_key(const double *taps, int S, int variant) {
+    std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
+    const int knobs[6] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2()};
+    k.append((const char *)knobs, sizeof knobs);
+    return k;
+}
+
 }  // namespace
 
 // Plan query for skc_layer_plan: 1 and the position count / LDS words per
 // output when the layer would take the sparse path (cost model only; the
 // run-time compiler is not consulted).
 bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
+    const std::string key = memo_key(taps, S, -1);
+    {
+        std::lock_guard<std::mutex> lock(g_memo_mu);
+        auto it = g_memo.find(key);
+        if (it != g_memo.end()) {
+            *npos = it->second.npos;
+            *words_per_out = it->second.words_per_out;
+            return it->second.eligible;
+        }
+    }
     const SpPlan p = make_plan(taps, S);
-    if (!eligible(p, S)) return false;
+    SpLaunch l;
+    l.eligible = eligible(p, S);
+    l.npos = p.npos;
+    l.words_per_out = p.words_per_out;
+    {
+        std::lock_guard<std::mutex> lock(g_memo_mu);
+        g_memo.emplace(key, l);
+    }
     *npos = p.npos;
     *words_per_out = p.words_per_out;
-    return true;
+    return l.eligible;
 }
 
 // One layer through a generated sparse stencil: planar input (fp32 or fp16),
@@ -517,15 +639,33 @@ bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
 // (ineligible, or no run-time compiler), else a status code.
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
                  const double *taps, int S, int boundary, cudaStream_t s) {
-    const SpPlan p = make_plan(taps, S);
-    if (!eligible(p, S)) return -1;
-    const std::string src = generate(p, in_f32, out_f32, out_pl);
-    cudaKernel_t k = get_kernel(src, p.smem);
-    if (!k) return -1;
-    dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, p.TH), B);
+    const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0));
+    SpLaunch l;
+    bool found = false;
+    {
+        std::lock_guard<std::mutex> lock(g_memo_mu);
+        auto it = g_memo.find(key);
+        if (it != g_memo.end()) {
+            l = it->second;
+            found = true;
+        }
+    }
+    if (!found) {
+        const SpPlan p = make_plan(taps, S);
+        l.eligible = eligible(p, S);
+        l.npos = p.npos;
+        l.TH = p.TH;
+        l.words_per_out = p.words_per_out;
+        l.smem = p.smem;
+        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl), p.smem);
+        std::lock_guard<std::mutex> lock(g_memo_mu);
+        g_memo[key] = l;
+    }
+    if (!l.eligible || !l.kern) return -1;
+    dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, l.TH), B);
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};
-    const cudaError_t e = cudaLaunchKernel((const void *)k, grid, dim3(256), args, p.smem, s);
+    const cudaError_t e = cudaLaunchKernel((const void *)l.kern, grid, dim3(256), args, l.smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
 }

@@ -276,7 +276,9 @@ def test_stencil_variants_inner_layers(skc, orc):
 
 
 def test_chain_io_policies_agree(skc):
-    """SKC_CHAIN_IO 0/1/2 (direct HWC I/O vs relayout passes) give identical chains."""
+    """SKC_CHAIN_IO 0/1/2 (direct HWC I/O vs relayout passes) give identical
+    chains with the fixed-kernel routing (SKC_SPARSE=0), and agree to fp32
+    rounding when planar first layers may take the generated sparse stencil."""
     import os
     import subprocess
     import sys
@@ -292,13 +294,21 @@ def test_chain_io_policies_agree(skc):
         for img in (rng.random((97, 130, 3)).astype(np.float32), rng.random((61, 77, 4)).astype(np.float16),
                     rng.random((300, 700, 4)).astype(np.float16), rng.random((333, 517, 3)).astype(np.float32)):
             np.save(f"{td}/in.npy", img)
-            outs = []
-            for pol in ("0", "1", "2"):
-                env = dict(os.environ, SKC_CHAIN_IO=pol)
-                subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/o{pol}.npy"], check=True,
-                               env=env, cwd=root)
-                outs.append(np.load(f"{td}/o{pol}.npy"))
-            assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+            for sparse in ("0", "auto"):
+                outs = []
+                for pol in ("0", "1", "2"):
+                    env = dict(os.environ, SKC_CHAIN_IO=pol, SKC_SPARSE=sparse)
+                    subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/o{pol}.npy"], check=True,
+                                   env=env, cwd=root)
+                    outs.append(np.load(f"{td}/o{pol}.npy"))
+                if sparse == "0":
+                    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+                else:
+                    # policy 0's first layer reads HWC (dense kernel), 1 and 2 may
+                    # run it as a generated sparse stencil: same weights, other
+                    # summation order
+                    tol = 2e-6 if img.dtype == np.float32 else 2e-3
+                    assert normwise(outs[0], outs[1]) < tol and normwise(outs[1], outs[2]) < tol
 
 
 def test_hwc_epilogue(skc, orc):
@@ -464,7 +474,8 @@ def test_sparse_stencil_path(skc, orc):
     layer and compiled at run time (skc_layer_plan kind 3).  Chains whose
     inner and last layers take it (planar and staged-HWC epilogues, fp32 and
     fp16 storage, both boundaries, ragged and odd sizes) match the oracle, and
-    agree with the tap path (SKC_SPARSE=0) to the storage tolerance."""
+    agree with the tap path (SKC_SPARSE=0) and the scalar-FFMA body
+    (SKC_SPARSE_F2=0) to the storage tolerance."""
     import ctypes
     import os
     import subprocess
@@ -511,6 +522,7 @@ def test_sparse_stencil_path(skc, orc):
                     np.savez(f"{td}/in.npz", img=img, L=len(layers),
                              **{f"o{i}": o for i, (o, _) in enumerate(layers)},
                              **{f"w{i}": ww for i, (_, ww) in enumerate(layers)})
-                    subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/t.npy", mode], check=True,
-                                   env=dict(os.environ, SKC_SPARSE="0"), cwd=root)
-                    assert normwise(ours, np.load(f"{td}/t.npy").astype(np.float64)) < tol
+                    for var in ({"SKC_SPARSE": "0"}, {"SKC_SPARSE_F2": "0"}):   # tap path; scalar-FFMA body
+                        subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/t.npy", mode], check=True,
+                                       env=dict(os.environ, **var), cwd=root)
+                        assert normwise(ours, np.load(f"{td}/t.npy").astype(np.float64)) < tol, var
