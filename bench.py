@@ -255,7 +255,7 @@ class Chain:
                         self.launch_fma.append(4 * t.shape[0] * npx)
                 elif kind.value == 3:    # generated sparse stencil: one FFMA per nonzero position
                     self.smem_bytes.append(0)
-                    self.smem_kind.append(f"sparse stencil, {par.value} positions (FFMA immediates, LDS.128)")
+                    self.smem_kind.append(f"sparse stencil, {par.value} positions (generated; FFMA2 body, LDS.128)")
                     self.launch_fma.append(par.value * npx)
                 else:
                     self.smem_bytes.append(0)
@@ -275,7 +275,7 @@ class Chain:
                        "frames_per_gpu": self.nf,
                        "l2": "inputs larger than L2, no flush" if npx * esz > 126e6 else "L2 flushed between steps"}
         self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if npx * esz <= 126e6 else None
-        self.kernel = "fused_chain_kernel" if self.fused else "layer kernels (dense stencil + tap tile)"
+        self.kernel = "fused_chain_kernel" if self.fused else "layer kernels (dense stencil / generated sparse stencil / tap tile, see roofline.fp32_pipe.kernel)"
 
     def step(self, stream, events=None):
         from paper_2512_04556_b200 import _native as nat

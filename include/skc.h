@@ -108,12 +108,14 @@ int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int
  * shared-memory traffic (bench roofline). */
 int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary, int *kind, int *param);
 
-/* Wide-footprint layers with planar input run a sparse stencil generated for
- * the layer (weights as immediates) and compiled at run time with NVRTC
- * (skc_sparse.cu).  This compiles the kernel the layer would run without a
- * device: 0 = compiled, 1 = the layer does not take that path, SKC_ECUDA = the
- * run-time compiler is missing or rejected it (skc_last_error). */
-int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int out_dtype, int out_layout);
+/* Layers with planar input (and, with SKC_SPARSE_HWC=1, HWC input) run a
+ * sparse stencil generated for the layer (its merged positions unrolled, the
+ * weights in a constant table) and compiled at run time with NVRTC
+ * (skc_sparse.cu) when the cost model prefers it.  This compiles the kernel
+ * such a layer would run, without a device: 0 = compiled, 1 = the layer does
+ * not take that path, SKC_ECUDA = the run-time compiler is missing or rejected
+ * it (skc_last_error).  Layouts are SKC_HWC / SKC_CHW. */
+int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_layout, int out_dtype, int out_layout);
 
 /* Dtype of skc_chain_fwd's planar intermediates for this chain: SKC_F16 when
  * in and out are both fp16 ("fp16 storage, fp32 accumulation": every layer

@@ -79,7 +79,7 @@ def _declare(lib):
     lib.skc_chain_is_fused.argtypes = [_dp, _ip, _i, _i, _i, _i, _i]
     lib.skc_chain_relayouts.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i]
     lib.skc_chain_mid_dtype.argtypes = [_ip, _i, _i, _i]
-    lib.skc_sparse_compile_check.argtypes = [_dp, _i, _i, _i, _i]
+    lib.skc_sparse_compile_check.argtypes = [_dp, _i, _i, _i, _i, _i]
     lib.skc_layer_plan.argtypes = [_dp, _i, _i, _i, _i, _i, _ip, _ip]
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,

@@ -204,35 +204,54 @@ __global__ void __launch_bounds__(TR * 64)
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[k][c] = 0.f;
     }
+    // One (tap, pixel): lerp the tap between the bracket's basis entries
+    // (_fastpath.py:109-111), split the offset into floor and fraction and
+    // gather the 2 x 2 corners of all C channels.
+    auto tap_px = [&](const float4 a, const float4 d, int k) {
+        const float t = tt[k];
+        const float ox = fmaf(t, d.x, a.x);
+        const float oy = fmaf(t, d.y, a.y);
+        const float w = fmaf(t, d.z, a.z);
+        const float bx = __fadd_rd(ox, kMagic), by = __fadd_rd(oy, kMagic);  // kMagic + floor(o)
+        const float fx = ox - (bx - kMagic), fy = oy - (by - kMagic);
+        const float wb = w * fy, wa = w - wb;
+        const float c10 = wa * fx, c00 = wa - c10, c11 = wb * fx, c01 = wb - c11;
+        int iy = __float_as_int(by) - kMagicBits, ix = __float_as_int(bx) - kMagicBits;
+        // opaque to the optimiser: otherwise the magic bias is re-associated into
+        // a separate add in front of every shared load (no room in the LDS offset)
+        asm("" : "+r"(iy), "+r"(ix));
+        const float *sp = tile + (pb[k] + iy * rs + ix * PS);
+        const float *sq = sp + rs;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float v = acc[k][c];
+            v = fmaf(c00, sp[c], v);
+            v = fmaf(c10, sp[PS + c], v);
+            v = fmaf(c01, sq[c], v);
+            v = fmaf(c11, sq[PS + c], v);
+            acc[k][c] = v;
+        }
+    };
+    // Smooth size maps put a thread's 8 pixels (one column, TR rows apart) in
+    // the same bracket almost everywhere: then one table read per tap serves
+    // all 8 (the per-pixel reads were ~2 of ~17 shared wavefronts per
+    // warp-tap-pixel).  Warp-uniform choice, so no divergence between paths.
+    bool same = true;
+#pragma unroll
+    for (int k = 1; k < kSvPx; ++k) same &= e0[k] == e0[0];
+    if (__all_sync(0xffffffffu, same)) {
+        const float4 *row = stab + e0[0];
 #pragma unroll 1
-    for (int i = 0; i < q.n; ++i) {
+        for (int i = 0; i < q.n; ++i) {
+            const float4 a = row[2 * i], d = row[2 * i + 1];
 #pragma unroll
-        for (int k = 0; k < kSvPx; ++k) {
-            const float4 a = stab[e0[k] + 2 * i];
-            const float4 d = stab[e0[k] + 2 * i + 1];
-            const float t = tt[k];
-            const float ox = fmaf(t, d.x, a.x);  // _fastpath.py:109-111
-            const float oy = fmaf(t, d.y, a.y);
-            const float w = fmaf(t, d.z, a.z);
-            const float bx = __fadd_rd(ox, kMagic), by = __fadd_rd(oy, kMagic);  // kMagic + floor(o)
-            const float fx = ox - (bx - kMagic), fy = oy - (by - kMagic);
-            const float wb = w * fy, wa = w - wb;
-            const float c10 = wa * fx, c00 = wa - c10, c11 = wb * fx, c01 = wb - c11;
-            int iy = __float_as_int(by) - kMagicBits, ix = __float_as_int(bx) - kMagicBits;
-            // opaque to the optimiser: otherwise the magic bias is re-associated into
-            // a separate add in front of every shared load (no room in the LDS offset)
-            asm("" : "+r"(iy), "+r"(ix));
-            const float *sp = tile + (pb[k] + iy * rs + ix * PS);
-            const float *sq = sp + rs;
+            for (int k = 0; k < kSvPx; ++k) tap_px(a, d, k);
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < q.n; ++i) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float v = acc[k][c];
-                v = fmaf(c00, sp[c], v);
-                v = fmaf(c10, sp[PS + c], v);
-                v = fmaf(c01, sq[c], v);
-                v = fmaf(c11, sq[PS + c], v);
-                acc[k][c] = v;
-            }
+            for (int k = 0; k < kSvPx; ++k) tap_px(stab[e0[k] + 2 * i], stab[e0[k] + 2 * i + 1], k);
         }
     }
 #pragma unroll

@@ -760,10 +760,13 @@ static int tap_kr_override() {
 // Rows per thread of the tap tile for a layer of `ntaps` taps with the given
 // corner footprint (see tap_kr_override).
 static int tap_kr_for(int H, int W, int C, int boundary, int accumulate, int dx_min, int dx_max, int dy_min,
-                      int dy_max, int ntaps) {
+                      int dy_max, int ntaps, bool hwc_out = false) {
     const int KR = tap_kr_override();
-    if (KR == 5 || KR == 7) return KR;
-    if (ntaps <= 16) return 5;  // memory-bound layers: smaller tiles, more CTAs in flight (config 3: 2.05 vs 2.17 ms)
+    if (KR == 3 || KR == 5 || KR == 7) return KR;
+    // latency-bound small layers: smaller tiles, more CTAs in flight (config 3's
+    // planar 4-tap layers: KR 3 -> 1.59 ms, 5 -> 1.83, 7 -> ~2.2); the staged HWC
+    // epilogue prefers the taller tile (2.44 vs 2.59 ms at KR 3)
+    if (ntaps <= 16) return hwc_out ? 5 : 3;
     const LGeom g7 = make_geom(H, W, C, boundary, accumulate, kTTW, kTWY * 8 * 7, dx_min, dx_max, dy_min, dy_max);
     return ((size_t)g7.rows * g7.pitch * sizeof(float) * 2 <= (size_t)kMaxSmem) ? 7 : 5;
 }
@@ -778,7 +781,7 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
         dy_min = std::min(dy_min, pl.iy[i]);
         dy_max = std::max(dy_max, pl.iy[i] + 1);
     }
-    const int KR = tap_kr_for(H, W, C, boundary, accumulate, dx_min, dx_max, dy_min, dy_max, t1 - t0);
+    const int KR = tap_kr_for(H, W, C, boundary, accumulate, dx_min, dx_max, dy_min, dy_max, t1 - t0, IN_PL && !OUT_PL);
     const int TH = kTWY * 8 * KR;
     LGeom g = make_geom(H, W, C, boundary, accumulate, kTTW, TH, dx_min, dx_max, dy_min, dy_max);
     TapList tl;
@@ -801,10 +804,12 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
     if (smem <= (size_t)kMaxSmem) {
-        auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>;
+        auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>
+                            : (KR == 5 ? layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
+        static int attr3 = set_smem_attr(layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
         static int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
         static int attr7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>);
-        if (attr5 || attr7) return attr5 ? attr5 : attr7;
+        if (attr3 || attr5 || attr7) return attr3 ? attr3 : (attr5 ? attr5 : attr7);
         dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
         kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
         SKC_LAUNCH_CHECK("layer_tap_kernel");
@@ -866,10 +871,24 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
     return SKC_OK;
 }
 
+static bool odd_head_pitch() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_HEAD_ODD_PITCH");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 template <typename TI, typename TO, bool IN_PL, bool OUT_PL>
 static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, const Plan &pl, int S,
                         int boundary, cudaStream_t s, int *rc) {
     if (!dense_allowed()) return false;
+    // planar fp16 inputs of small layers are load-latency bound: the KR = 3 tap
+    // tile beats the dense kernel's fewer FMAs (config 3's D3 layer: 1.59 vs
+    // 2.05 ms; with fp32 planar input the dense D3 wins, 1.68 vs 1.82 ms)
+    if constexpr (IN_PL && sizeof(TI) == 2) {
+        if (S <= 16) return false;
+    }
     const int sx = pl.dx_max - pl.dx_min + 1, sy = pl.dy_max - pl.dy_min + 1;
     const int D = dense_size_for(std::max(sx, sy));
     if (D == 0 || D * D >= 4 * S) return false;
@@ -905,6 +924,13 @@ static bool try_stencil(const void *in, void *out, int B, int H, int W, int C, c
     }
     LGeom g = make_geom(H, W, C, boundary, 0, kDenTW, kDenTH, pl.dx_min, pl.dx_min + D - 1,
                         pl.dy_min, pl.dy_min + D - 1);
+    // HWC inputs stage with 4-byte copies, so the pitch may be odd: then the
+    // window rows' LDS.32 of the 4 x 8 lane layout (rows KR * pitch apart)
+    // hit 32 distinct banks (config 1's D5 head: 51% of its shared-load
+    // wavefronts were 2-way conflicts at pitch = 2 mod 4)
+    if constexpr (!IN_PL) {
+        if (odd_head_pitch() && (g.pitch & 1) == 0) g.pitch += 1;
+    }
     dl.col_shift = pl.dx_min - g.dx0;
     switch (D) {
         case 3: *rc = launch_stencil_d<3, kDenKR, TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, dl, g, s); break;
@@ -920,12 +946,11 @@ static int layer_t(const void *in, void *out, int B, int H, int W, int C, const 
                    int boundary, cudaStream_t s) {
     const Plan pl = plan_taps(taps, S);
     int rc = SKC_OK;
-    if constexpr (IN_PL) {  // planar input: generated sparse stencil when it is cheaper (skc_sparse.cu)
-        rc = sparse_layer(in, std::is_same<TI, float>::value, out, std::is_same<TO, float>::value, OUT_PL, B, H, W,
-                          C, taps, S, boundary, s);
-        if (rc != -1) return rc;
-        rc = SKC_OK;
-    }
+    // generated sparse stencil when it is cheaper (skc_sparse.cu); HWC inputs opt-in (SKC_SPARSE_HWC)
+    rc = sparse_layer(in, std::is_same<TI, float>::value, out, std::is_same<TO, float>::value, OUT_PL, B, H, W, C,
+                      taps, S, boundary, s, !IN_PL);
+    if (rc != -1) return rc;
+    rc = SKC_OK;
     if (try_stencil<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, S, boundary, s, &rc)) return rc;
     if (S <= kLMaxTaps)
         return launch_taps<TI, TO, IN_PL, OUT_PL>(in, out, B, H, W, C, pl, 0, S, boundary, 0, s);

@@ -66,6 +66,12 @@ int sp_f2() {
     static const int v = env_int("SKC_SPARSE_F2", 1);
     return v;
 }
+// SKC_SPARSE_HWC=1: HWC-input layers (a chain's head) may take the sparse
+// path too (channel-strided tile loads, like the dense / tap kernels).
+int sp_hwc() {
+    static const int v = env_int("SKC_SPARSE_HWC", 0);
+    return v;
+}
 int sp_minb() {
     static const int v = std::max(1, env_int("SKC_SPARSE_MINB", 3));
     return v;
@@ -199,6 +205,28 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     const long long hw = (long long)H * W;
     const int tx0 = (blockIdx.x / C) * 128, ty0 = blockIdx.y * TH;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if IN_HWC
+    {   // channel c of the HWC halo tile: 4-byte copies at element stride C
+        const TI *frame = in + (long long)b * hw * C;
+        const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
+        for (int r = warp; r < ROWS; r += 8) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const TI *src = frame + (long long)gy * W * C + c;
+            float *dst = smem + r * PITCH;
+            const bool inner = rowin && gx0 >= 0 && gx0 + PITCH <= W;
+            for (int col = lane; col < PITCH; col += 32) {
+                const int gx = gx0 + col;
+                const bool ok = inner || clamp || (rowin && gx >= 0 && gx < W);
+                const long long e = (long long)(inner ? gx : min(max(gx, 0), W - 1)) * C;
+                if (IN_F32) cp4(dst + col, (const float *)src + e, ok ? 4 : 0);
+                else dst[col] = ok ? ldx(src + e) : 0.f;
+            }
+        }
+        asm volatile("cp.async.wait_all;");
+    }
+#else
     {   // halo tile of channel plane c: rows [ty0 + DY0, +ROWS), cols [tx0 + DX0, +PITCH)
         const TI *plane = in + ((long long)b * C + c) * hw;
         const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
@@ -239,6 +267,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
         }
         asm volatile("cp.async.wait_all;");
     }
+#endif
     __syncthreads();
     const int lx = lane & 3, ly = lane >> 2, wx = warp & 3, wy = warp >> 2;
     const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
@@ -303,12 +332,13 @@ std::string hexf(float v) {
     return buf;
 }
 
-std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl) {
+std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false) {
     std::ostringstream s;
     s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
       << "\n";
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
-    s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n";
+    s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
+      << (in_hwc ? 1 : 0) << "\n";
     s << "#define MINB " << sp_minb() << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
@@ -599,7 +629,7 @@ std::unordered_map<std::string, SpLaunch> g_memo;
 
 std::string memo_key(const double *taps, int S, int variant) {
     std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
-    const int knobs[6] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2()};
+    const int knobs[7] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc()};
     k.append((const char *)knobs, sizeof knobs);
     return k;
 }
@@ -638,8 +668,10 @@ bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
 // planar or HWC output.  Returns -1 when the layer does not take this path
 // (ineligible, or no run-time compiler), else a status code.
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
-                 const double *taps, int S, int boundary, cudaStream_t s) {
-    const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0));
+                 const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
+    if (in_hwc && sp_hwc() == 0) return -1;
+    const std::string key =
+        memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) | (in_hwc ? 8 : 0));
     SpLaunch l;
     bool found = false;
     {
@@ -657,7 +689,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
         l.TH = p.TH;
         l.words_per_out = p.words_per_out;
         l.smem = p.smem;
-        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl), p.smem);
+        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl, in_hwc), p.smem);
         std::lock_guard<std::mutex> lock(g_memo_mu);
         g_memo[key] = l;
     }
@@ -678,14 +710,15 @@ extern "C" {
 // would run: 0 = compiled, 1 = the layer does not take the sparse path,
 // SKC_ECUDA = the run-time compiler is missing or rejected the source
 // (message in skc_last_error).
-int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int out_dtype, int out_layout) {
+int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_layout, int out_dtype, int out_layout) {
     using namespace skc;
     if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
     const SpPlan p = make_plan(taps, S);
     if (!eligible(p, S)) return 1;
     std::string why;
     const std::vector<char> cubin =
-        compile_cubin(generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW), &why);
+        compile_cubin(generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW, in_layout == SKC_HWC),
+                      &why);
     return cubin.empty() ? fail(SKC_ECUDA, why) : SKC_OK;
 }
 

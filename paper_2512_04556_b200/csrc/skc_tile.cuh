@@ -120,7 +120,7 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
 // Layer-specialised sparse stencils compiled at run time (skc_sparse.cu):
 // planar input, planar or HWC output; -1 = not taken.
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
-                 const double *taps, int S, int boundary, cudaStream_t s);
+                 const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc = false);
 bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out);
 
 // Argument checks shared by the image entry points (skc_layer.cu).

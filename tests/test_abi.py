@@ -61,8 +61,9 @@ def test_sparse_stencil_compiles_without_a_device(tmp_path, monkeypatch):
     lib = nat.load_library()
     cpx = synth.c1_complex()
     t = np.ascontiguousarray(cpx.layers[0].taps())
-    assert lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], nat.SKC_F32, nat.SKC_F32, nat.SKC_CHW) == 1
+    assert lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], nat.SKC_F32, nat.SKC_CHW, nat.SKC_F32, nat.SKC_CHW) == 1
     t = np.ascontiguousarray(cpx.layers[2].taps())
-    for args in ((nat.SKC_F32, nat.SKC_F32, nat.SKC_CHW), (nat.SKC_F16, nat.SKC_F16, nat.SKC_HWC)):
+    for args in ((nat.SKC_F32, nat.SKC_CHW, nat.SKC_F32, nat.SKC_CHW), (nat.SKC_F16, nat.SKC_CHW, nat.SKC_F16, nat.SKC_HWC),
+                 (nat.SKC_F32, nat.SKC_HWC, nat.SKC_F32, nat.SKC_CHW)):
         rc = lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], *args)
         assert rc == 0, nat.last_error()
