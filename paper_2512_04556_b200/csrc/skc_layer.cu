@@ -136,31 +136,33 @@ __device__ __forceinline__ bool tile_rows_any(unsigned sd, const float *sx, int 
     }
 }
 
-// Planar fp16 interior rows: each lane moves NCH half2 pairs of two rows per
-// iteration (2 * NCH independent 4-byte loads in flight), widened to fp32
+// Planar fp16 interior rows: each lane moves NCH half2 pairs of four rows per
+// iteration (4 * NCH independent 4-byte loads in flight), widened to fp32
 // with 8-byte shared stores.  (A cp.async variant staging the raw pairs
 // behind the fp32 tile measured slower on config 3: 1.5x shared memory per
 // CTA costs a resident CTA per SM; 19.1 vs 21.0 Gpix/s.)
 template <int NCH>
 __device__ __forceinline__ void half_rows(float *s, const __half *src, int lane, int np, int r0, int rows, int nw,
                                           int spitch, int W) {
+    constexpr int RU = 4;  // rows per iteration: RU * NCH independent loads in flight per lane
     const int sstep = nw * spitch;
     const long long gstep = (long long)nw * W;
-    for (int r = r0; r < rows; r += 2 * nw, s += 2 * sstep, src += 2 * gstep) {
-        const bool two = r + nw < rows;
-        __half2 v[2][NCH];
+    for (int r = r0; r < rows; r += RU * nw, s += RU * sstep, src += RU * gstep) {
+        __half2 v[RU][NCH];
 #pragma unroll
-        for (int u = 0; u < NCH; ++u) {
-            const bool in = u < NCH - 1 || lane + 32 * u < np;
-            if (in) v[0][u] = __ldg(reinterpret_cast<const __half2 *>(src + 64 * u));
-            if (in && two) v[1][u] = __ldg(reinterpret_cast<const __half2 *>(src + gstep + 64 * u));
-        }
+        for (int q = 0; q < RU; ++q)
 #pragma unroll
-        for (int u = 0; u < NCH; ++u) {
-            const bool in = u < NCH - 1 || lane + 32 * u < np;
-            if (in) *reinterpret_cast<float2 *>(s + 64 * u) = __half22float2(v[0][u]);
-            if (in && two) *reinterpret_cast<float2 *>(s + sstep + 64 * u) = __half22float2(v[1][u]);
-        }
+            for (int u = 0; u < NCH; ++u) {
+                const bool in = (u < NCH - 1 || lane + 32 * u < np) && r + q * nw < rows;
+                if (in) v[q][u] = __ldg(reinterpret_cast<const __half2 *>(src + q * gstep + 64 * u));
+            }
+#pragma unroll
+        for (int q = 0; q < RU; ++q)
+#pragma unroll
+            for (int u = 0; u < NCH; ++u) {
+                const bool in = (u < NCH - 1 || lane + 32 * u < np) && r + q * nw < rows;
+                if (in) *reinterpret_cast<float2 *>(s + q * sstep + 64 * u) = __half22float2(v[q][u]);
+            }
     }
 }
 

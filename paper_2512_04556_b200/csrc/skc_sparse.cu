@@ -72,6 +72,12 @@ int sp_hwc() {
     static const int v = env_int("SKC_SPARSE_HWC", 0);
     return v;
 }
+// Warps along y per CTA (SKC_SPARSE_WY, 2 or 4; 4 along x): taller tiles
+// amortise the vertical halo of wide layers.
+int sp_wy() {
+    static const int v = [] { const int w = env_int("SKC_SPARSE_WY", 2); return w == 4 ? 4 : 2; }();
+    return v;
+}
 int sp_minb() {
     static const int v = std::max(1, env_int("SKC_SPARSE_MINB", 3));
     return v;
@@ -85,7 +91,7 @@ struct SpPos {
 };
 
 struct SpPlan {
-    int KR = 7, TH = 112;
+    int KR = 7, TH = 112, WY = 2;  // rows per thread, tile height, warps along y (4 along x)
     int dx_min = 0, dy_min = 0, Dx = 0, Dy = 0, npos = 0;
     std::vector<std::vector<SpPos>> rows;  // rows[a]: nonzero (b, K) of stencil row a
     int DX0 = 0, SH = 0, pitch = 0, nrows = 0, nw = 0;
@@ -96,7 +102,8 @@ struct SpPlan {
 SpPlan make_plan(const double *taps, int S) {
     SpPlan p;
     p.KR = sp_kr();
-    p.TH = 16 * p.KR;
+    p.WY = sp_wy();
+    p.TH = 8 * p.KR * p.WY;
     std::map<std::pair<int, int>, double> acc;  // (dy, dx) -> merged weight
     for (int i = 0; i < S; ++i) {
         const double ox = taps[3 * i], oy = taps[3 * i + 1], w = taps[3 * i + 2];
@@ -131,7 +138,7 @@ SpPlan make_plan(const double *taps, int S) {
     // smem geometry: column 0 <-> global tx0 + DX0 (DX0 = dx_min floored to 4)
     p.DX0 = xmin & ~3;
     p.SH = xmin - p.DX0;
-    const int wmax = p.SH + p.Dx - 1 + 7;        // last window word of a thread
+    const int wmax = p.SH + p.Dx - 1 + (sp_f2() == 2 ? 8 : 7);  // last window word of a thread
     p.nw = (wmax / 4 + 1) * 4;
     int pitch = 120 + p.nw;                        // last thread's col0 = 120
     while (pitch % 8 != 4) ++pitch;
@@ -198,7 +205,7 @@ __device__ __forceinline__ void cp16(float *dst, const float *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
 }
 
-extern "C" __global__ void __launch_bounds__(256, MINB)
+extern "C" __global__ void __launch_bounds__(NWARP * 32, MINB)
 skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W, int C, int clamp) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.z, c = blockIdx.x % C;
@@ -209,7 +216,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     {   // channel c of the HWC halo tile: 4-byte copies at element stride C
         const TI *frame = in + (long long)b * hw * C;
         const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
-        for (int r = warp; r < ROWS; r += 8) {
+        for (int r = warp; r < ROWS; r += NWARP) {
             int gy = gy0 + r;
             const bool rowin = clamp || (gy >= 0 && gy < H);
             gy = min(max(gy, 0), H - 1);
@@ -233,12 +240,12 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
         if (IN_F32 && (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W && gy0 >= 0 && gy0 + ROWS <= H) {
             const float *src = (const float *)plane + (long long)(gy0 + warp) * W + gx0;
             float *dst = smem + warp * PITCH;
-            for (int r = warp; r < ROWS; r += 8, src += 8LL * W, dst += 8 * PITCH)
+            for (int r = warp; r < ROWS; r += NWARP, src += (long long)NWARP * W, dst += NWARP * PITCH)
 #pragma unroll
                 for (int u = 0; u < (PITCH / 4 + 31) / 32; ++u)
                     if (lane + 32 * u < PITCH / 4) cp16(dst + 4 * (lane + 32 * u), src + 4 * (lane + 32 * u));
         } else {
-            for (int r = warp; r < ROWS; r += 8) {
+            for (int r = warp; r < ROWS; r += NWARP) {
                 int gy = gy0 + r;
                 const bool rowin = clamp || (gy >= 0 && gy < H);
                 gy = min(max(gy, 0), H - 1);
@@ -314,7 +321,7 @@ const char *kSpHwcEpilogue = R"CUDA(
     }
     __syncthreads();
     const int nx = min(128, W - tx0), nr = min(TH, H - ty0);
-    for (int r = warp; r < nr; r += 8) {
+    for (int r = warp; r < nr; r += NWARP) {
         TO *dst = out + (((long long)b * H + ty0 + r) * W + tx0) * C + c;
         const float *srow = smem + r * 132;
 #pragma unroll
@@ -340,6 +347,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
       << (in_hwc ? 1 : 0) << "\n";
     s << "#define MINB " << sp_minb() << "\n#define F2MODE " << sp_f2() << "\n";
+    s << "#define NWARP " << 4 * p.WY << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
     const bool f2 = sp_f2() != 0;
@@ -369,8 +377,9 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
         s << "    float2";
         for (int i = 0; i < p.KR; ++i)
             for (int j = 0; j < 4; ++j) s << (i || j ? ", " : " ") << "e" << i << "_" << j << " = make_float2(0.f, 0.f)";
+        const bool xchg = sp_f2() == 2;  // odd positions: 4 pairs (1,2)..(7,8), output 8 to the right neighbour
         for (int i = 0; i < p.KR; ++i)
-            for (int j = 0; j < 3; ++j) s << ", o" << i << "_" << j << " = make_float2(0.f, 0.f)";
+            for (int j = 0; j < (xchg ? 4 : 3); ++j) s << ", o" << i << "_" << j << " = make_float2(0.f, 0.f)";
         s << ";\n    float";
         for (int i = 0; i < p.KR; ++i) s << (i ? ", " : " ") << "s" << i << "_0 = 0.f, s" << i << "_7 = 0.f";
         s << ";\n    float2";
@@ -382,13 +391,14 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
             for (int a = a_lo; a <= a_hi; ++a)
                 for (const SpPos &e : p.rows[a]) {
                     kmin = std::min(kmin, p.SH + e.b);
-                    kmax = std::max(kmax, p.SH + e.b + 7);
+                    kmax = std::max(kmax, p.SH + e.b + (xchg && (p.SH + e.b) % 2 ? 8 : 7));
                 }
             if (kmax < 0) continue;
             s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
             for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
                 s << "        { const float4 t = rp[" << ch << "]; wp" << 2 * ch << " = make_float2(t.x, t.y); wp"
                   << 2 * ch + 1 << " = make_float2(t.z, t.w); }\n";
+            std::ostringstream first_col;  // exchange mode: output 0 of the tile's first column block
             for (int a = a_lo; a <= a_hi; ++a) {
                 const int i = q - a;
                 for (size_t e = 0; e < p.rows[a].size(); ++e) {
@@ -398,6 +408,12 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                         for (int j = 0; j < 4; ++j)
                             s << "        e" << i << "_" << j << " = ffma2(" << kw << ", wp" << c0 / 2 + j << ", e" << i << "_"
                               << j << ");\n";
+                    } else if (xchg) {
+                        first_col << "            s" << i << "_0 = fmaf(" << kw << ".x, wp" << (c0 - 1) / 2 << ".y, s" << i
+                                  << "_0);\n";
+                        for (int j = 0; j < 4; ++j)
+                            s << "        o" << i << "_" << j << " = ffma2(" << kw << ", wp" << (c0 + 1) / 2 + j << ", o" << i
+                              << "_" << j << ");\n";
                     } else {
                         s << "        s" << i << "_0 = fmaf(" << kw << ".x, wp" << (c0 - 1) / 2 << ".y, s" << i << "_0);\n";
                         for (int j = 0; j < 3; ++j)
@@ -407,14 +423,31 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                     }
                 }
             }
+            if (!first_col.str().empty()) s << "        if (wx == 0) {\n" << first_col.str() << "        }\n";
             s << "    }\n";
         }
         s << "    float acc[KR][8];\n";
+        if (xchg) {
+            // output 8 of each column block is output 0 of the block to its right:
+            // exchange through the dead tile (16 column blocks per tile row); the
+            // tile's first block keeps its own scalar sums s<i>_0
+            s << "    __syncthreads();\n";
+            for (int i = 0; i < p.KR; ++i)
+                s << "    smem[(row0 + " << i << ") * 16 + (col0 >> 3)] = o" << i << "_3.y;\n";
+            s << "    __syncthreads();\n";
+            for (int i = 0; i < p.KR; ++i)
+                s << "    const float x" << i << " = col0 > 0 ? smem[(row0 + " << i << ") * 16 + (col0 >> 3) - 1] : s" << i
+                  << "_0;\n";
+        }
         for (int i = 0; i < p.KR; ++i) {
             for (int j = 0; j < 4; ++j)
                 s << "    acc[" << i << "][" << 2 * j << "] = e" << i << "_" << j << ".x; acc[" << i << "][" << 2 * j + 1
                   << "] = e" << i << "_" << j << ".y;\n";
-            s << "    acc[" << i << "][0] += s" << i << "_0; acc[" << i << "][7] += s" << i << "_7;\n";
+            if (xchg) {
+                s << "    acc[" << i << "][0] += x" << i << "; acc[" << i << "][7] += o" << i << "_3.x;\n";
+            } else {
+                s << "    acc[" << i << "][0] += s" << i << "_0; acc[" << i << "][7] += s" << i << "_7;\n";
+            }
             for (int j = 0; j < 3; ++j)
                 s << "    acc[" << i << "][" << 2 * j + 1 << "] += o" << i << "_" << j << ".x; acc[" << i << "][" << 2 * j + 2
                   << "] += o" << i << "_" << j << ".y;\n";
@@ -629,7 +662,7 @@ std::unordered_map<std::string, SpLaunch> g_memo;
 
 std::string memo_key(const double *taps, int S, int variant) {
     std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
-    const int knobs[7] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc()};
+    const int knobs[8] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc(), sp_wy()};
     k.append((const char *)knobs, sizeof knobs);
     return k;
 }
@@ -697,7 +730,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, l.TH), B);
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};
-    const cudaError_t e = cudaLaunchKernel((const void *)l.kern, grid, dim3(256), args, l.smem, s);
+    const cudaError_t e = cudaLaunchKernel((const void *)l.kern, grid, dim3(128 * sp_wy()), args, l.smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
 }
