@@ -208,11 +208,49 @@ __device__ __forceinline__ void cp16(float *dst, const float *src) {
 extern "C" __global__ void __launch_bounds__(NWARP * 32, MINB)
 skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W, int C, int clamp) {
     extern __shared__ __align__(16) float smem[];
-    const int b = blockIdx.z, c = blockIdx.x % C;
     const long long hw = (long long)H * W;
-    const int tx0 = (blockIdx.x / C) * 128, ty0 = blockIdx.y * TH;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#if IN_HWC
+#if ALLC
+    // all channels per CTA (HWC chain head): coalesced 16-byte row loads of the
+    // interleaved tile, deinterleaved into CC planes; the body runs once per plane
+    const int b = blockIdx.z;
+    const int tx0 = blockIdx.x * 128, ty0 = blockIdx.y * TH;
+    {
+        const float *frame = (const float *)in + (long long)b * hw * CC;
+        const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
+        for (int r = warp; r < ROWS; r += NWARP) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const float *src = frame + (long long)gy * W * CC;
+            float *dst = smem + r * PITCH;
+            if (rowin && (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W) {
+                const float4 *s4 = (const float4 *)(src + (long long)gx0 * CC);
+#pragma unroll 4
+                for (int k = lane; k < PITCH * CC / 4; k += 32) {
+                    const float4 v = __ldg(s4 + k);
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int e = 4 * k + t, px = e / CC, ch = e - px * CC;
+                        dst[ch * (ROWS * PITCH) + px] = vv[t];
+                    }
+                }
+            } else {
+                for (int e = lane; e < PITCH * CC; e += 32) {
+                    const int px = e / CC, ch = e - px * CC, gx = gx0 + px;
+                    const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                    dst[ch * (ROWS * PITCH) + px] = ok ? __ldg(src + (long long)min(max(gx, 0), W - 1) * CC + ch) : 0.f;
+                }
+            }
+        }
+    }
+#else
+    const int b = blockIdx.z, c = blockIdx.x % C;
+    const int tx0 = (blockIdx.x / C) * 128, ty0 = blockIdx.y * TH;
+#endif
+#if ALLC
+#elif IN_HWC
     {   // channel c of the HWC halo tile: 4-byte copies at element stride C
         const TI *frame = in + (long long)b * hw * C;
         const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
@@ -278,7 +316,13 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     __syncthreads();
     const int lx = lane & 3, ly = lane >> 2, wx = warp & 3, wy = warp >> 2;
     const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+#if ALLC
+#pragma unroll 1
+    for (int c = 0; c < CC; ++c) {
+    const float *base = smem + c * (ROWS * PITCH) + row0 * PITCH + col0;
+#else
     const float *base = smem + row0 * PITCH + col0;
+#endif
 )CUDA";
 
 const char *kSpPlanarEpilogue = R"CUDA(
@@ -308,7 +352,6 @@ const char *kSpPlanarEpilogue = R"CUDA(
         for (int j = 0; j < 8; ++j)
             if (gx + j < W) stx(p + j, acc[i][j]);
     }
-}
 )CUDA";
 
 const char *kSpHwcEpilogue = R"CUDA(
@@ -330,7 +373,6 @@ const char *kSpHwcEpilogue = R"CUDA(
             if (x < nx) stx(dst + (long long)x * C, srow[x]);
         }
     }
-}
 )CUDA";
 
 std::string hexf(float v) {
@@ -339,14 +381,15 @@ std::string hexf(float v) {
     return buf;
 }
 
-std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false) {
+std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0) {
     std::ostringstream s;
+    s << "#define ALLC " << (allc ? 1 : 0) << "\n#define CC " << std::max(1, allc) << "\n";
     s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
       << "\n";
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
       << (in_hwc ? 1 : 0) << "\n";
-    s << "#define MINB " << sp_minb() << "\n#define F2MODE " << sp_f2() << "\n";
+    s << "#define MINB " << (allc ? std::min(2, sp_minb()) : sp_minb()) << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
@@ -453,6 +496,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                   << "] += o" << i << "_" << j << ".y;\n";
         }
         s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+        s << (allc ? "    }\n}\n" : "}\n");
         return s.str();
     }
     // scalar accumulators a<i>_<j> and window words w<k> (not arrays: the front
@@ -493,6 +537,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
  for (int i = 0; i < p.KR; ++i)
         for (int j = 0; j < 8; ++j) s << "    acc[" << i << "][" << j << "] = a" << i << "_" << j << ";\n";
     s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+    s << (allc ? "    }\n}\n" : "}\n");
     return s.str();
 }
 
@@ -703,8 +748,10 @@ bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
     if (in_hwc && sp_hwc() == 0) return -1;
-    const std::string key =
-        memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) | (in_hwc ? 8 : 0));
+    // SKC_SPARSE_HWC=2: an fp32 HWC head writing planar runs all channels per CTA
+    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 && out_pl && sp_f2() != 2) ? C : 0;
+    const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
+                                                  (in_hwc ? 8 : 0) | (allc << 4));
     SpLaunch l;
     bool found = false;
     {
@@ -716,18 +763,22 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
         }
     }
     if (!found) {
-        const SpPlan p = make_plan(taps, S);
+        SpPlan p = make_plan(taps, S);
         l.eligible = eligible(p, S);
+        if (allc) {  // forced for the experiment: no cost model; C planes of shared memory
+            p.smem = (size_t)std::max(allc * p.nrows * p.pitch, p.TH * kSpStagePitch) * sizeof(float);
+            l.eligible = p.npos > 0 && (long long)p.npos * p.KR * 8 <= kSpMaxFfma && p.smem <= (size_t)kMaxSmem;
+        }
         l.npos = p.npos;
         l.TH = p.TH;
         l.words_per_out = p.words_per_out;
         l.smem = p.smem;
-        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl, in_hwc), p.smem);
+        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl, in_hwc, allc), p.smem);
         std::lock_guard<std::mutex> lock(g_memo_mu);
         g_memo[key] = l;
     }
     if (!l.eligible || !l.kern) return -1;
-    dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, l.TH), B);
+    dim3 grid(ceil_div(W, kSpTW) * (allc ? 1 : C), ceil_div(H, l.TH), B);
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};
     const cudaError_t e = cudaLaunchKernel((const void *)l.kern, grid, dim3(128 * sp_wy()), args, l.smem, s);
@@ -747,11 +798,12 @@ int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_lay
     using namespace skc;
     if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
     const SpPlan p = make_plan(taps, S);
-    if (!eligible(p, S)) return 1;
+    // the all-channel head variant (SKC_SPARSE_HWC=2) is checked for C = 3
+    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == SKC_F32 && out_layout == SKC_CHW) ? 3 : 0;
+    if (!allc && !eligible(p, S)) return 1;
     std::string why;
-    const std::vector<char> cubin =
-        compile_cubin(generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW, in_layout == SKC_HWC),
-                      &why);
+    const std::vector<char> cubin = compile_cubin(
+        generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW, in_layout == SKC_HWC, allc), &why);
     return cubin.empty() ? fail(SKC_ECUDA, why) : SKC_OK;
 }
 
