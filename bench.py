@@ -238,6 +238,21 @@ class Chain:
                     self.smem_bytes.append(npx * (5 + d - 1) * (8 + d - 1) * 4 / 40)
                     self.smem_kind.append(f"dense stencil D={d} (LDS.32)")
                     self.launch_fma.append(d * d * npx)
+                elif kind.value in (1, 3) and item == 0 and not self.pre and self.storage == torch.float32:
+                    # fp32 HWC chain head of a stencil-type layer: the all-channel generated
+                    # stencil (skc_sparse.cu); nonzero merged corner positions counted here
+                    ix, iy = np.floor(t[:, 0]), np.floor(t[:, 1])
+                    fx, fy, w = t[:, 0] - ix, t[:, 1] - iy, t[:, 2]
+                    acc = {}
+                    for cx, cy, cw in ((0, 0, w * (1 - fx) * (1 - fy)), (1, 0, w * fx * (1 - fy)),
+                                       (0, 1, w * (1 - fx) * fy), (1, 1, w * fx * fy)):
+                        for k in range(t.shape[0]):
+                            key = (int(iy[k]) + cy, int(ix[k]) + cx)
+                            acc[key] = acc.get(key, 0.0) + cw[k]
+                    npos = sum(1 for v in acc.values() if np.float32(v) != 0)
+                    self.smem_bytes.append(0)
+                    self.smem_kind.append(f"all-channel sparse head, {npos} positions (generated)")
+                    self.launch_fma.append(npos * npx)
                 elif kind.value == 3 and item == 0 and not self.pre:
                     # HWC-input first layer: the sparse stencil takes planar input, so the
                     # dense / tap kernel runs (dense when D^2 < 4S, as skc_layer.cu routes)

@@ -66,10 +66,14 @@ int sp_f2() {
     static const int v = env_int("SKC_SPARSE_F2", 1);
     return v;
 }
-// SKC_SPARSE_HWC=1: HWC-input layers (a chain's head) may take the sparse
-// path too (channel-strided tile loads, like the dense / tap kernels).
+// HWC-input layers (a chain's head): SKC_SPARSE_HWC=2 (default) runs an
+// fp32 head that writes planar as an all-channel sparse stencil (the
+// interleaved tile lands with coalesced cp.async; config 1's D5 head 1.60 ->
+// 1.25 ms) when the layer would run a dense or sparse stencil and two CTAs
+// fit per SM; 1 = per-channel CTAs with strided loads (measured slower);
+// 0 = the dense / tap kernels.
 int sp_hwc() {
-    static const int v = env_int("SKC_SPARSE_HWC", 0);
+    static const int v = env_int("SKC_SPARSE_HWC", 2);
     return v;
 }
 // Warps along y per CTA (SKC_SPARSE_WY, 2 or 4; 4 along x): taller tiles
@@ -211,8 +215,10 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     const long long hw = (long long)H * W;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if ALLC
-    // all channels per CTA (HWC chain head): coalesced 16-byte row loads of the
-    // interleaved tile, deinterleaved into CC planes; the body runs once per plane
+    // all channels per CTA (HWC chain head): the interleaved halo tile lands
+    // with coalesced 4-byte cp.async (RS = PITCH * CC + 1 words per row: odd, so
+    // the body's stride-CC window loads of the 4 x 8 lane layout are
+    // conflict-free); the body then runs once per channel on that tile
     const int b = blockIdx.z;
     const int tx0 = blockIdx.x * 128, ty0 = blockIdx.y * TH;
     {
@@ -223,27 +229,20 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
             const bool rowin = clamp || (gy >= 0 && gy < H);
             gy = min(max(gy, 0), H - 1);
             const float *src = frame + (long long)gy * W * CC;
-            float *dst = smem + r * PITCH;
-            if (rowin && (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W) {
-                const float4 *s4 = (const float4 *)(src + (long long)gx0 * CC);
+            float *dst = smem + r * RS;
+            if (rowin && gx0 >= 0 && gx0 + PITCH <= W) {
+                const float *s1 = src + (long long)gx0 * CC;
 #pragma unroll 4
-                for (int k = lane; k < PITCH * CC / 4; k += 32) {
-                    const float4 v = __ldg(s4 + k);
-                    const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int e = 4 * k + t, px = e / CC, ch = e - px * CC;
-                        dst[ch * (ROWS * PITCH) + px] = vv[t];
-                    }
-                }
+                for (int e = lane; e < PITCH * CC; e += 32) cp4(dst + e, s1 + e, 4);
             } else {
                 for (int e = lane; e < PITCH * CC; e += 32) {
                     const int px = e / CC, ch = e - px * CC, gx = gx0 + px;
                     const bool ok = clamp || (rowin && gx >= 0 && gx < W);
-                    dst[ch * (ROWS * PITCH) + px] = ok ? __ldg(src + (long long)min(max(gx, 0), W - 1) * CC + ch) : 0.f;
+                    cp4(dst + e, src + (long long)min(max(gx, 0), W - 1) * CC + ch, ok ? 4 : 0);
                 }
             }
         }
+        asm volatile("cp.async.wait_all;");
     }
 #else
     const int b = blockIdx.z, c = blockIdx.x % C;
@@ -319,7 +318,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
 #if ALLC
 #pragma unroll 1
     for (int c = 0; c < CC; ++c) {
-    const float *base = smem + c * (ROWS * PITCH) + row0 * PITCH + col0;
+    const float *base = smem + row0 * RS + col0 * CC + c;
 #else
     const float *base = smem + row0 * PITCH + col0;
 #endif
@@ -383,7 +382,8 @@ std::string hexf(float v) {
 
 std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0) {
     std::ostringstream s;
-    s << "#define ALLC " << (allc ? 1 : 0) << "\n#define CC " << std::max(1, allc) << "\n";
+    s << "#define ALLC " << (allc ? 1 : 0) << "\n#define CC " << std::max(1, allc) << "\n#define RS "
+      << p.pitch * std::max(1, allc) + 1 << "\n";
     s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
       << "\n";
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
@@ -437,10 +437,16 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                     kmax = std::max(kmax, p.SH + e.b + (xchg && (p.SH + e.b) % 2 ? 8 : 7));
                 }
             if (kmax < 0) continue;
-            s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
-            for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
-                s << "        { const float4 t = rp[" << ch << "]; wp" << 2 * ch << " = make_float2(t.x, t.y); wp"
-                  << 2 * ch + 1 << " = make_float2(t.z, t.w); }\n";
+            if (allc) {
+                s << "    {\n        const float *rp = base + " << q << " * RS;\n";
+                for (int m = kmin / 2; m <= kmax / 2; ++m)
+                    s << "        wp" << m << " = make_float2(rp[" << 2 * m << " * CC], rp[" << 2 * m + 1 << " * CC]);\n";
+            } else {
+                s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
+                for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
+                    s << "        { const float4 t = rp[" << ch << "]; wp" << 2 * ch << " = make_float2(t.x, t.y); wp"
+                      << 2 * ch + 1 << " = make_float2(t.z, t.w); }\n";
+            }
             std::ostringstream first_col;  // exchange mode: output 0 of the tile's first column block
             for (int a = a_lo; a <= a_hi; ++a) {
                 const int i = q - a;
@@ -747,9 +753,10 @@ bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
 // (ineligible, or no run-time compiler), else a status code.
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
-    if (in_hwc && sp_hwc() == 0) return -1;
-    // SKC_SPARSE_HWC=2: an fp32 HWC head writing planar runs all channels per CTA
-    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 && out_pl && sp_f2() != 2) ? C : 0;
+    // HWC input: the all-channel head (fp32 in, planar out), or with
+    // SKC_SPARSE_HWC=1 the per-channel variant; otherwise the dense / tap kernels
+    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 && out_pl && sp_f2() == 1) ? C : 0;
+    if (in_hwc && !allc && sp_hwc() != 1) return -1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4));
     SpLaunch l;
@@ -765,9 +772,12 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (!found) {
         SpPlan p = make_plan(taps, S);
         l.eligible = eligible(p, S);
-        if (allc) {  // forced for the experiment: no cost model; C planes of shared memory
-            p.smem = (size_t)std::max(allc * p.nrows * p.pitch, p.TH * kSpStagePitch) * sizeof(float);
-            l.eligible = p.npos > 0 && (long long)p.npos * p.KR * 8 <= kSpMaxFfma && p.smem <= (size_t)kMaxSmem;
+        if (allc) {  // C interleaved channels of shared memory; stencil-type layers, two CTAs per SM
+            p.smem = (size_t)std::max(p.nrows * (allc * p.pitch + 1), p.TH * kSpStagePitch) * sizeof(float);
+            const int D = dense_size_for(std::max(p.Dx, p.Dy));
+            const bool stencil_like = l.eligible || (D != 0 && D * D < 4 * S);
+            l.eligible = sparse_mode() != 0 && stencil_like && p.npos > 0 &&
+                         (long long)p.npos * p.KR * 8 <= kSpMaxFfma && 2 * p.smem <= (size_t)kMaxSmem;
         }
         l.npos = p.npos;
         l.TH = p.TH;
@@ -799,7 +809,7 @@ int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_lay
     if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
     const SpPlan p = make_plan(taps, S);
     // the all-channel head variant (SKC_SPARSE_HWC=2) is checked for C = 3
-    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == SKC_F32 && out_layout == SKC_CHW) ? 3 : 0;
+    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == SKC_F32 && out_layout == SKC_CHW && sp_f2() == 1) ? 3 : 0;
     if (!allc && !eligible(p, S)) return 1;
     std::string why;
     const std::vector<char> cubin = compile_cubin(

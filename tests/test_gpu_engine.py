@@ -474,8 +474,10 @@ def test_sparse_stencil_path(skc, orc):
     layer and compiled at run time (skc_layer_plan kind 3).  Chains whose
     inner and last layers take it (planar and staged-HWC epilogues, fp32 and
     fp16 storage, both boundaries, ragged and odd sizes) match the oracle, and
-    agree with the tap path (SKC_SPARSE=0) and the scalar-FFMA body
-    (SKC_SPARSE_F2=0) to the storage tolerance."""
+    agree with the tap path (SKC_SPARSE=0), the scalar-FFMA body
+    (SKC_SPARSE_F2=0) and the per-channel HWC head (SKC_SPARSE_HWC=0; by
+    default an fp32 chain head runs all channels per CTA) to the storage
+    tolerance."""
     import ctypes
     import os
     import subprocess
@@ -522,7 +524,8 @@ def test_sparse_stencil_path(skc, orc):
                     np.savez(f"{td}/in.npz", img=img, L=len(layers),
                              **{f"o{i}": o for i, (o, _) in enumerate(layers)},
                              **{f"w{i}": ww for i, (_, ww) in enumerate(layers)})
-                    for var in ({"SKC_SPARSE": "0"}, {"SKC_SPARSE_F2": "0"}):   # tap path; scalar-FFMA body
+                    # tap / dense path; scalar-FFMA body; per-channel kernels for the HWC head
+                    for var in ({"SKC_SPARSE": "0"}, {"SKC_SPARSE_F2": "0"}, {"SKC_SPARSE_HWC": "0"}):
                         subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/t.npy", mode], check=True,
                                        env=dict(os.environ, **var), cwd=root)
                         assert normwise(ours, np.load(f"{td}/t.npy").astype(np.float64)) < tol, var

@@ -250,3 +250,39 @@ def test_build_basis_and_json_roundtrip(skc, tmp_path):
     for fa, fb in zip(basis.filters, back.filters):
         for la, lb in zip(fa.layers, fb.layers):
             assert np.array_equal(la.offsets, lb.offsets) and np.array_equal(la.weights, lb.weights)
+
+
+def test_sv_pixel_pairs_on_smooth_maps(skc, orc):
+    """On smooth size maps (config 2's recipe) most warps take the
+    bracket-uniform path, which runs pixel pairs in packed FP32 (FFMA2 /
+    FADD2.RM); it matches the oracle and the scalar path (SKC_SV_PAIRS=0) to
+    fp32 rounding, for C = 1 / 3 / 4 and both boundaries."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    from paper_2512_04556_b200 import synth
+    from paper_2512_04556_b200.svfilter import stacked_params
+    basis = synth.c2_basis()
+    root = str(Path(__file__).parent.parent)
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "d = np.load(sys.argv[1]);"
+            "np.save(sys.argv[2], skc.sv_filter(d['img'], synth.c2_basis(), d['pmap'], boundary=sys.argv[3]))")
+    rng = np.random.default_rng(23)
+    with tempfile.TemporaryDirectory() as td:
+        for (h, w, c) in ((300, 257, 3), (181, 222, 4), (140, 333, 1)):
+            img = rng.random((h, w, c)).astype(np.float32)
+            if c == 1:
+                img = img[..., 0]
+            pmap = synth.c2_pmap(h, w, seed=5, blobs=4)
+            for mode, oid in (("zero", orc.ZERO), ("clamp", orc.CLAMP)):
+                ours = np.asarray(skc.sv_filter(img, basis, pmap, boundary=mode))
+                ref = orc.sv_filter(img.astype(np.float64), pmap, basis.params, stacked_params(basis),
+                                    basis.layout, oid)
+                assert normwise(ours, ref) < TOL32, (h, w, c, mode)
+                np.savez(f"{td}/in.npz", img=img, pmap=pmap)
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/o.npy", mode], check=True,
+                               env=dict(os.environ, SKC_SV_PAIRS="0"), cwd=root)
+                assert normwise(ours, np.load(f"{td}/o.npy")) < 2e-6
