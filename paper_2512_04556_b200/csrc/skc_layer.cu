@@ -1208,11 +1208,19 @@ static bool last_layer_direct(int H, int W, int C, const double *taps, int S, in
 
 // The chain's I/O passes (see chain_policy); by default the output relayout
 // is skipped when the last layer runs the tap kernel's staged HWC epilogue.
+static int chain_mid_dtype(int in_dtype, int out_dtype, const int *layout, int L);
+
 static void chain_io(const double *taps, const int *layout, int L, long long total, int H, int W, int C,
-                     int in_dtype, int boundary, bool *pre, bool *post) {
+                     int in_dtype, int boundary, bool *pre, bool *post, int out_dtype = -1) {
+    if (out_dtype < 0) out_dtype = in_dtype;
     const int pol = chain_policy(in_dtype);
     *pre = pol == 1;
     *post = pol == 1 || pol == 2;
+    // an fp16 head that runs as the all-channel generated stencil reads the
+    // HWC input itself (coalesced), so the input relayout pass goes
+    if (*pre && chain_policy_env() < 0 && in_dtype == SKC_F16 &&
+        chain_mid_dtype(in_dtype, out_dtype, layout, L) == SKC_F16 && sparse_head_allc(taps, layout[0], C, false))
+        *pre = false;
     if (*post && chain_policy_env() < 0) {
         const double *lt = taps + 3 * (total - layout[L - 1]);
         if (last_layer_direct(H, W, C, lt, layout[L - 1], boundary)) *post = false;
@@ -1376,7 +1384,7 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     rc = SKC_OK;
     // intermediates: fp32 planar (B, C, H, W), ping-pong; see chain_policy()
     bool pre, post;
-    chain_io(taps, layout, L, total, H, W, C, in_dtype, boundary, &pre, &post);
+    chain_io(taps, layout, L, total, H, W, C, in_dtype, boundary, &pre, &post, out_dtype);
     const int mid = chain_mid_dtype(in_dtype, out_dtype, layout, L);
     const size_t n = (size_t)B * H * W * C;
     void *buf[2] = {nullptr, nullptr};

@@ -221,6 +221,33 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     // conflict-free); the body then runs once per channel on that tile
     const int b = blockIdx.z;
     const int tx0 = blockIdx.x * 128, ty0 = blockIdx.y * TH;
+#if !IN_F32
+    {   // fp16 head: the raw interleaved halves land with 4-byte cp.async (RSH
+        // halves per row, even); the body widens each window word it reads
+        const half_t *frame = (const half_t *)in + (long long)b * hw * CC;
+        const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
+        half_t *sh = (half_t *)smem;
+        for (int r = warp; r < ROWS; r += NWARP) {
+            int gy = gy0 + r;
+            const bool rowin = clamp || (gy >= 0 && gy < H);
+            gy = min(max(gy, 0), H - 1);
+            const half_t *src = frame + (long long)gy * W * CC;
+            half_t *dst = sh + r * RSH;
+            if (rowin && ((W * CC) & 1) == 0 && gx0 >= 0 && gx0 + PITCH <= W) {
+                const float *s1 = (const float *)(src + (long long)gx0 * CC);
+#pragma unroll 4
+                for (int e = lane; e < PITCH * CC / 2; e += 32) cp4((float *)dst + e, s1 + e, 4);
+            } else {
+                for (int e = lane; e < PITCH * CC; e += 32) {
+                    const int px = e / CC, ch = e - px * CC, gx = gx0 + px;
+                    const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                    dst[e] = ok ? __ldg(src + (long long)min(max(gx, 0), W - 1) * CC + ch) : (half_t)0;
+                }
+            }
+        }
+        asm volatile("cp.async.wait_all;");
+    }
+#else
     {
         const float *frame = (const float *)in + (long long)b * hw * CC;
         const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
@@ -244,6 +271,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
         }
         asm volatile("cp.async.wait_all;");
     }
+#endif
 #else
     const int b = blockIdx.z, c = blockIdx.x % C;
     const int tx0 = (blockIdx.x / C) * 128, ty0 = blockIdx.y * TH;
@@ -296,6 +324,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
                     }
                 } else if (rowin && (W & 1) == 0 && gx0 >= 0 && gx0 + PITCH <= W) {
                     const unsigned *s2 = (const unsigned *)(src + gx0);
+#pragma unroll 4
                     for (int p = lane; p < PITCH / 2; p += 32) {
                         const unsigned v = __ldg(s2 + p);
                         *(float2 *)(dst + 2 * p) = make_float2(h2f(v & 0xffffu), h2f(v >> 16));
@@ -318,7 +347,11 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
 #if ALLC
 #pragma unroll 1
     for (int c = 0; c < CC; ++c) {
+#if IN_F32
     const float *base = smem + row0 * RS + col0 * CC + c;
+#else
+    const half_t *base = (const half_t *)smem + row0 * RSH + col0 * CC + c;
+#endif
 #else
     const float *base = smem + row0 * PITCH + col0;
 #endif
@@ -383,7 +416,7 @@ std::string hexf(float v) {
 std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0) {
     std::ostringstream s;
     s << "#define ALLC " << (allc ? 1 : 0) << "\n#define CC " << std::max(1, allc) << "\n#define RS "
-      << p.pitch * std::max(1, allc) + 1 << "\n";
+      << p.pitch * std::max(1, allc) + 1 << "\n#define RSH " << p.pitch * std::max(1, allc) + 2 << "\n";
     s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
       << "\n";
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
@@ -437,10 +470,15 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                     kmax = std::max(kmax, p.SH + e.b + (xchg && (p.SH + e.b) % 2 ? 8 : 7));
                 }
             if (kmax < 0) continue;
-            if (allc) {
+            if (allc && in_f32) {
                 s << "    {\n        const float *rp = base + " << q << " * RS;\n";
                 for (int m = kmin / 2; m <= kmax / 2; ++m)
                     s << "        wp" << m << " = make_float2(rp[" << 2 * m << " * CC], rp[" << 2 * m + 1 << " * CC]);\n";
+            } else if (allc) {
+                s << "    {\n        const half_t *rp = base + " << q << " * RSH;\n";
+                for (int m = kmin / 2; m <= kmax / 2; ++m)
+                    s << "        wp" << m << " = make_float2(h2f(rp[" << 2 * m << " * CC]), h2f(rp[" << 2 * m + 1
+                      << " * CC]));\n";
             } else {
                 s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
                 for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
@@ -699,6 +737,16 @@ cudaKernel_t get_kernel(const std::string &src, size_t smem) {
     return k.failed ? nullptr : k.kern;
 }
 
+// All-channel head eligibility (and its shared memory in p.smem): C
+// interleaved channels staged per CTA, stencil-type layers, two CTAs per SM.
+bool allc_ok(SpPlan &p, int S, int C, bool in_f32) {
+    p.smem = in_f32 ? (size_t)p.nrows * (C * p.pitch + 1) * sizeof(float) : (size_t)p.nrows * (C * p.pitch + 2) * 2;
+    const int D = dense_size_for(std::max(p.Dx, p.Dy));
+    const bool stencil_like = eligible(p, S) || (D != 0 && D * D < 4 * S);
+    return sparse_mode() != 0 && sp_hwc() == 2 && sp_f2() == 1 && stencil_like && p.npos > 0 &&
+           (long long)p.npos * p.KR * 8 <= kSpMaxFfma && 2 * p.smem <= (size_t)kMaxSmem;
+}
+
 // Per-layer memo (host cost per launch is a hash lookup, not a plan and a
 // 300 KB source string): keyed by the tap bytes, the variant and the knobs.
 struct SpLaunch {
@@ -748,6 +796,14 @@ bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
     return l.eligible;
 }
 
+// Would an HWC head (fp32 or fp16 storage, planar output of the same dtype)
+// run as the all-channel generated stencil?  skc_chain_fwd then skips its
+// input relayout pass.
+bool sparse_head_allc(const double *taps, int S, int C, bool f32) {
+    SpPlan p = make_plan(taps, S);
+    return allc_ok(p, S, C, f32);
+}
+
 // One layer through a generated sparse stencil: planar input (fp32 or fp16),
 // planar or HWC output.  Returns -1 when the layer does not take this path
 // (ineligible, or no run-time compiler), else a status code.
@@ -755,7 +811,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
     // HWC input: the all-channel head (fp32 in, planar out), or with
     // SKC_SPARSE_HWC=1 the per-channel variant; otherwise the dense / tap kernels
-    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 && out_pl && sp_f2() == 1) ? C : 0;
+    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 == out_f32 && out_pl && sp_f2() == 1) ? C : 0;
     if (in_hwc && !allc && sp_hwc() != 1) return -1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4));
@@ -772,13 +828,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (!found) {
         SpPlan p = make_plan(taps, S);
         l.eligible = eligible(p, S);
-        if (allc) {  // C interleaved channels of shared memory; stencil-type layers, two CTAs per SM
-            p.smem = (size_t)std::max(p.nrows * (allc * p.pitch + 1), p.TH * kSpStagePitch) * sizeof(float);
-            const int D = dense_size_for(std::max(p.Dx, p.Dy));
-            const bool stencil_like = l.eligible || (D != 0 && D * D < 4 * S);
-            l.eligible = sparse_mode() != 0 && stencil_like && p.npos > 0 &&
-                         (long long)p.npos * p.KR * 8 <= kSpMaxFfma && 2 * p.smem <= (size_t)kMaxSmem;
-        }
+        if (allc) l.eligible = allc_ok(p, S, allc, in_f32);
         l.npos = p.npos;
         l.TH = p.TH;
         l.words_per_out = p.words_per_out;
@@ -809,7 +859,8 @@ int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_lay
     if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
     const SpPlan p = make_plan(taps, S);
     // the all-channel head variant (SKC_SPARSE_HWC=2) is checked for C = 3
-    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == SKC_F32 && out_layout == SKC_CHW && sp_f2() == 1) ? 3 : 0;
+    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == out_dtype && out_layout == SKC_CHW && sp_f2() == 1)
+                         ? (in_dtype == SKC_F32 ? 3 : 4) : 0;
     if (!allc && !eligible(p, S)) return 1;
     std::string why;
     const std::vector<char> cubin = compile_cubin(

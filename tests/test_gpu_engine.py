@@ -461,7 +461,10 @@ def test_planar_half_entry_points(skc):
     assert lib.skc_layer_fwd_ex(nat.ptr(x), nat.SKC_F16, nat.SKC_HWC, nat.ptr(o2), nat.SKC_F16, nat.SKC_HWC,
                                 2, 20, 30, 3, nat.dbl(t), 2, 0, s) == 0
     torch.cuda.synchronize()
-    assert torch.equal(o1, o2.permute(0, 3, 1, 2))
+    # same kernel family on both layouts by default (bit-equal); forced kernel
+    # switches may route the planar call elsewhere, so allow fp16 rounding
+    d = (o1.float() - o2.permute(0, 3, 1, 2).float()).abs().max().item()
+    assert d <= 2e-3 * o2.float().abs().max().item()
     f32 = torch.empty((2, 3, 20, 30), device="cuda")
     assert lib.skc_layer_fwd_ex(nat.ptr(pl), nat.SKC_F16, nat.SKC_CHW, nat.ptr(f32), nat.SKC_F32, nat.SKC_CHW,
                                 2, 20, 30, 3, nat.dbl(t), 2, 0, s) == nat.SKC_EBADARG
