@@ -755,6 +755,7 @@ struct SpLaunch {
     double words_per_out = 0.0;
     size_t smem = 0;
     cudaKernel_t kern = nullptr;  // null: the run-time compiler failed
+    unsigned long long devmask = 0;  // devices whose shared-memory opt-in is set
 };
 std::mutex g_memo_mu;
 std::unordered_map<std::string, SpLaunch> g_memo;
@@ -838,6 +839,16 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
         g_memo[key] = l;
     }
     if (!l.eligible || !l.kern) return -1;
+    {   // the shared-memory opt-in is per device: set it once for each device used
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && dev < 64 && !(l.devmask >> dev & 1ULL)) {
+            const cudaError_t ae = cudaFuncSetAttribute((const void *)l.kern,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l.smem);
+            if (ae != cudaSuccess) return cuda_fail(ae, "cudaFuncSetAttribute(skc_sparse_stencil)");
+            std::lock_guard<std::mutex> lock(g_memo_mu);
+            g_memo[key].devmask |= 1ULL << dev;
+        }
+    }
     dim3 grid(ceil_div(W, kSpTW) * (allc ? 1 : C), ceil_div(H, l.TH), B);
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};

@@ -67,3 +67,9 @@ def test_sparse_stencil_compiles_without_a_device(tmp_path, monkeypatch):
                  (nat.SKC_F32, nat.SKC_HWC, nat.SKC_F32, nat.SKC_CHW)):
         rc = lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], *args)
         assert rc == 0, nat.last_error()
+    # all-channel chain heads (HWC in, planar out): config 1's fp32 D5 head and
+    # config 3's fp16 Kawase head (dense-size layers the generator takes as heads)
+    for layer, dt in ((cpx.layers[0], nat.SKC_F32), (synth.kawase_complex().layers[0], nat.SKC_F16)):
+        t = np.ascontiguousarray(layer.taps())
+        rc = lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], dt, nat.SKC_HWC, dt, nat.SKC_CHW)
+        assert rc == 0, nat.last_error()
