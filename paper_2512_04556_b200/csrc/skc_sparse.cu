@@ -55,6 +55,10 @@ int sp_kr() {
     static const int v = [] { const int k = env_int("SKC_SPARSE_KR", 3); return (k == 1 || k == 3 || k == 5 || k == 7 || k == 9) ? k : 3; }();
     return v;
 }
+int sp_kr_wide() {
+    static const int v = [] { const int k = env_int("SKC_SPARSE_KR_WIDE", sp_kr()); return (k == 3 || k == 5 || k == 7) ? k : sp_kr(); }();
+    return v;
+}
 int sp_sync() {
     static const int v = env_int("SKC_SPARSE_SYNC", 0);
     return v;
@@ -80,6 +84,13 @@ int sp_hwc() {
 // amortise the vertical halo of wide layers.
 int sp_wy() {
     static const int v = [] { const int w = env_int("SKC_SPARSE_WY", 2); return w == 4 ? 4 : 2; }();
+    return v;
+}
+// Interior fp32 planar tiles fill with one bulk (TMA) copy per row
+// (SKC_SPARSE_TMA=1; measured no faster: config 1 25.6 vs 25.8 Gpix/s) or
+// per-lane 16-byte cp.async (=0, default).
+int sp_tma() {
+    static const int v = env_int("SKC_SPARSE_TMA", 0);
     return v;
 }
 int sp_minb() {
@@ -132,6 +143,12 @@ SpPlan make_plan(const double *taps, int S) {
     p.dy_min = ymin;
     p.Dx = xmax - xmin + 1;
     p.Dy = ymax - ymin + 1;
+    // tall footprints re-read fewer window rows per output at a larger KR
+    // ((KR + Dy - 1) / KR rows per output row); SKC_SPARSE_KR_WIDE for Dy >= 24
+    if (p.Dy >= 24) {
+        p.KR = sp_kr_wide();
+        p.TH = 8 * p.KR * p.WY;
+    }
     p.rows.assign(p.Dy, {});
     for (const auto &kv : acc) {
         const float k = (float)kv.second;
@@ -181,7 +198,7 @@ int sparse_mode() {
 bool eligible(const SpPlan &p, int S) {
     const int mode = sparse_mode();
     if (mode == 0 || p.npos == 0) return false;
-    if ((long long)p.npos * p.KR * 8 > kSpMaxFfma) return false;
+    if ((long long)p.npos * p.KR * (sp_f2() ? 5 : 8) > kSpMaxFfma) return false;
     if (p.smem > (size_t)kMaxSmem) return false;
     if (mode == 1) return true;
     const int D = dense_size_for(std::max(p.Dx, p.Dy));
@@ -302,7 +319,35 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     {   // halo tile of channel plane c: rows [ty0 + DY0, +ROWS), cols [tx0 + DX0, +PITCH)
         const TI *plane = in + ((long long)b * C + c) * hw;
         const int gx0 = tx0 + DX0, gy0 = ty0 + DY0;
-        if (IN_F32 && (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W && gy0 >= 0 && gy0 + ROWS <= H) {
+        const bool interior = (W & 3) == 0 && gx0 >= 0 && gx0 + PITCH <= W && gy0 >= 0 && gy0 + ROWS <= H;
+#if USE_TMA
+        if (IN_F32 && interior) {
+            // interior tile: one bulk (TMA) copy per row, completion counted in
+            // bytes on an mbarrier -- the fill bypasses the LSU (no per-lane
+            // LDGSTS, none of its shared-store wavefronts)
+            __shared__ __align__(8) unsigned long long mbar;
+            const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+            if (threadIdx.x == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+                asm volatile("fence.mbarrier_init.release.cluster;");
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(ROWS * PITCH * 4));
+            if (lane == 0) {
+                const float *src = (const float *)plane + (long long)(gy0 + warp) * W + gx0;
+                unsigned dst = (unsigned)__cvta_generic_to_shared(smem + warp * PITCH);
+                for (int r = warp; r < ROWS; r += NWARP, src += (long long)NWARP * W, dst += NWARP * PITCH * 4)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(dst), "l"(src), "r"(PITCH * 4), "r"(mb) : "memory");
+            }
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(mb) : "memory");
+        } else
+#endif
+        if (IN_F32 && interior) {
             const float *src = (const float *)plane + (long long)(gy0 + warp) * W + gx0;
             float *dst = smem + warp * PITCH;
             for (int r = warp; r < ROWS; r += NWARP, src += (long long)NWARP * W, dst += NWARP * PITCH)
@@ -354,6 +399,7 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
 #endif
 #else
     const float *base = smem + row0 * PITCH + col0;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(base);
 #endif
 )CUDA";
 
@@ -423,6 +469,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
       << (in_hwc ? 1 : 0) << "\n";
     s << "#define MINB " << (allc ? std::min(2, sp_minb()) : sp_minb()) << "\n#define F2MODE " << sp_f2() << "\n";
+    s << "#define USE_TMA " << sp_tma() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
@@ -480,10 +527,14 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                     s << "        wp" << m << " = make_float2(h2f(rp[" << 2 * m << " * CC]), h2f(rp[" << 2 * m + 1
                       << " * CC]));\n";
             } else {
-                s << "    {\n        const float4 *rp = (const float4 *)(base + " << q << " * PITCH);\n";
+                // full-width LDS.128 through inline PTX: a chunk whose words are only
+                // partly used would otherwise be narrowed to LDS.32/64, which the 4 x 8
+                // lane layout turns into 4-way bank conflicts (ncu source page, config 1)
+                s << "    {\n";
                 for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
-                    s << "        { const float4 t = rp[" << ch << "]; wp" << 2 * ch << " = make_float2(t.x, t.y); wp"
-                      << 2 * ch + 1 << " = make_float2(t.z, t.w); }\n";
+                    s << "        asm(\"ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4+" << 4 * (q * p.pitch + 4 * ch)
+                      << "];\" : \"=f\"(wp" << 2 * ch << ".x), \"=f\"(wp" << 2 * ch << ".y), \"=f\"(wp" << 2 * ch + 1
+                      << ".x), \"=f\"(wp" << 2 * ch + 1 << ".y) : \"r\"(sbase));\n";
             }
             std::ostringstream first_col;  // exchange mode: output 0 of the tile's first column block
             for (int a = a_lo; a <= a_hi; ++a) {
@@ -762,7 +813,8 @@ std::unordered_map<std::string, SpLaunch> g_memo;
 
 std::string memo_key(const double *taps, int S, int variant) {
     std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
-    const int knobs[8] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc(), sp_wy()};
+    const int knobs[10] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc(), sp_wy(), sp_tma(),
+                           sp_kr_wide()};
     k.append((const char *)knobs, sizeof knobs);
     return k;
 }
