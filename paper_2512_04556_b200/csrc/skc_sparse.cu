@@ -56,7 +56,7 @@ int sp_kr() {
     return v;
 }
 int sp_kr_wide() {
-    static const int v = [] { const int k = env_int("SKC_SPARSE_KR_WIDE", sp_kr()); return (k == 3 || k == 5 || k == 7) ? k : sp_kr(); }();
+    static const int v = [] { const int k = env_int("SKC_SPARSE_KR_WIDE", 5); return (k == 3 || k == 5 || k == 7) ? k : 5; }();
     return v;
 }
 int sp_sync() {
@@ -144,7 +144,8 @@ SpPlan make_plan(const double *taps, int S) {
     p.Dx = xmax - xmin + 1;
     p.Dy = ymax - ymin + 1;
     // tall footprints re-read fewer window rows per output at a larger KR
-    // ((KR + Dy - 1) / KR rows per output row); SKC_SPARSE_KR_WIDE for Dy >= 24
+    // ((KR + Dy - 1) / KR rows per output row): SKC_SPARSE_KR_WIDE (default 5)
+    // for Dy >= 24
     if (p.Dy >= 24) {
         p.KR = sp_kr_wide();
         p.TH = 8 * p.KR * p.WY;
@@ -468,7 +469,10 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "#define TI " << (in_f32 ? "float" : "half_t") << "\n#define TO " << (out_f32 ? "float" : "half_t") << "\n";
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
       << (in_hwc ? 1 : 0) << "\n";
-    s << "#define MINB " << (allc ? std::min(2, sp_minb()) : sp_minb()) << "\n#define F2MODE " << sp_f2() << "\n";
+    // resident CTAs per SM: 3 at KR = 3 (<= 85 registers), 2 for all-channel heads
+    // and KR >= 5 bodies (config 1's tall layer: 3.15 vs 3.23 ms at KR 5 / 2 CTAs)
+    const int minb = (allc || p.KR >= 5) ? std::min(2, sp_minb()) : sp_minb();
+    s << "#define MINB " << minb << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define USE_TMA " << sp_tma() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
