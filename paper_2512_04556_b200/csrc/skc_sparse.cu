@@ -22,6 +22,7 @@
 // layer regardless of the cost model; SKC_SPARSE_DUMP=<dir> writes the
 // generated sources.
 #include <dlfcn.h>
+#include <sys/stat.h>
 #include <unistd.h>
 #include <nvrtc.h>
 
@@ -731,8 +732,8 @@ std::string cache_path(const std::string &src) {
     for (unsigned char ch : src) hsh = (hsh ^ ch) * 1099511628211ULL;
     char name[96];
     std::snprintf(name, sizeof name, "/sparse_sm100a_%016llx_%zu.cubin", hsh, src.size());
-    std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
-    (void)!std::system(mk.c_str());
+    for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p without a shell
+        if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0755);
     return dir + name;
 }
 
