@@ -30,6 +30,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "skc_tile.cuh"
 
 namespace skc {
@@ -492,6 +494,132 @@ __global__ void __launch_bounds__(kTWX *kTWY * 32)
     store_block<KR, TO, OUT_PL>(out + b * fs, g, c, ty0 + row0, tx0 + col0, acc);
 }
 
+// Cluster-of-C HWC epilogue (opt-in, SKC_TAP_CLUSTER=1): the C channel CTAs
+// of a tile form one thread-block cluster.  Each stages its finished channel
+// tile in its dead input tile, then -- after a cluster barrier -- writes every
+// C-th tile row for *all* channels: each lane reads 4 pixels of every channel
+// from the sibling CTAs' shared memory (DSMEM, 16-byte loads) and stores the
+// interleaved pixels contiguously (fp16 C = 4: 32 bytes per lane), instead of
+// C CTAs each scattering 2- or 4-byte stores at stride C.
+template <typename TO, int CC>
+__device__ __forceinline__ void store_hwc_pixels(TO *dst, const float (&v)[4][CC], int n) {
+    if constexpr (sizeof(TO) == 2 && CC == 4) {
+        if (n == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            uint4 t[2];
+            unsigned *tw = reinterpret_cast<unsigned *>(t);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const __half2 a = __floats2half2_rn(v[p][0], v[p][1]), b = __floats2half2_rn(v[p][2], v[p][3]);
+                tw[2 * p] = *reinterpret_cast<const unsigned *>(&a);
+                tw[2 * p + 1] = *reinterpret_cast<const unsigned *>(&b);
+            }
+            reinterpret_cast<uint4 *>(dst)[0] = t[0];
+            reinterpret_cast<uint4 *>(dst)[1] = t[1];
+            return;
+        }
+    }
+    if constexpr (sizeof(TO) == 4 && (CC == 4 || CC == 2)) {
+        if (n == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            float4 *d4 = reinterpret_cast<float4 *>(dst);
+            const float *f = &v[0][0];
+#pragma unroll
+            for (int q = 0; q < CC; ++q) d4[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+            return;
+        }
+    }
+    for (int p = 0; p < n; ++p)
+#pragma unroll
+        for (int c = 0; c < CC; ++c) IO<TO>::st(dst + p * CC + c, v[p][c]);
+}
+
+template <int KR, typename TI, typename TO, int CC>
+__global__ void __launch_bounds__(kTWX *kTWY * 32)
+    layer_tap_cluster_kernel(const TI *__restrict__ in, TO *__restrict__ out, const LGeom g,
+                             const __grid_constant__ TapList tl) {
+    extern __shared__ __align__(16) float smem[];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int b = blockIdx.z, c = (int)cluster.block_rank();  // cluster (CC,1,1) over the channel-fastest grid
+    const long long fs = (long long)g.H * g.W * CC;
+    constexpr int TH = kTWY * 8 * KR;
+    const int tx0 = (blockIdx.x / CC) * kTTW, ty0 = blockIdx.y * TH;
+    load_plane<TI, true>(smem, in + b * fs, g, c, tx0 + g.dx0, ty0 + g.dy0);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp % kTWX, wy = warp / kTWX;
+    const int col0 = wx * 32 + lx * 8;
+    const int row0 = wy * 8 * KR + ly * KR;
+    const float *base = smem + row0 * g.pitch + col0;
+    float acc[KR][8];
+#pragma unroll
+    for (int r = 0; r < KR; ++r)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+#pragma unroll 1
+    for (int i = 0; i < tl.n_even; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], false);
+#pragma unroll 1
+    for (int i = tl.n_even; i < tl.n; ++i) tap_rows<KR>(acc, base + tl.off[i], g.pitch, tl.cw[i], true);
+    __syncthreads();  // every warp is done reading the input tile
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+        float4 *d = reinterpret_cast<float4 *>(smem + (row0 + r) * kStagePitch + col0);
+        d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
+    }
+    cluster.sync();  // all C channel tiles staged
+    const float *sib[CC];
+#pragma unroll
+    for (int q = 0; q < CC; ++q) sib[q] = cluster.map_shared_rank(smem, q);
+    const int nx = min(128, g.W - tx0), nr = min(TH, g.H - ty0);
+    const int nw = blockDim.x >> 5;
+    for (int r = c + CC * warp; r < nr; r += CC * nw) {
+        const int x = 4 * lane;
+        if (x >= nx) continue;
+        float v[4][CC];
+#pragma unroll
+        for (int q = 0; q < CC; ++q) {
+            const float4 t = *reinterpret_cast<const float4 *>(sib[q] + r * kStagePitch + x);
+            v[0][q] = t.x;
+            v[1][q] = t.y;
+            v[2][q] = t.z;
+            v[3][q] = t.w;
+        }
+        store_hwc_pixels<TO, CC>(out + ((long long)b * g.H * g.W + (long long)(ty0 + r) * g.W + tx0 + x) * CC, v,
+                                 min(4, nx - x));
+    }
+    cluster.sync();  // keep this CTA's staged tile alive until the siblings are done
+}
+
+static bool tap_cluster_enabled() {
+    static const bool v = [] {
+        const char *e = std::getenv("SKC_TAP_CLUSTER");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+template <int KR, typename TI, typename TO, int CC>
+static int launch_tap_cluster(const TI *in, TO *out, int B, int H, int W, const LGeom &g, const TapList &tl,
+                              size_t smem, cudaStream_t s) {
+    auto kern = layer_tap_cluster_kernel<KR, TI, TO, CC>;
+    static int attr = set_smem_attr(kern);
+    if (attr) return attr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ceil_div(W, kTTW) * CC, ceil_div(H, kTWY * 8 * KR), B);
+    cfg.blockDim = dim3(kTWX * kTWY * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SKC_CUDA(cudaLaunchKernelEx(&cfg, kern, in, out, g, tl));
+    return SKC_OK;
+}
+
 // ------------------------------------------------------------- dense path ---
 constexpr int kDenKR = 5, kDenWX = 4, kDenWY = 2;  // 256 threads, tile 128 x 80
 constexpr int kDenTW = kDenWX * 32, kDenTH = kDenWY * 8 * kDenKR;
@@ -805,6 +933,14 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     const size_t smem = tile_smem<TI, IN_PL>(g);
     const TI *pin = static_cast<const TI *>(in);
     TO *pout = static_cast<TO *>(out);
+    if constexpr (IN_PL && !OUT_PL) {
+        if (tap_cluster_enabled() && !accumulate && (C == 3 || C == 4) && KR == 5 &&
+            std::max(smem, (size_t)kTWY * 8 * 5 * kStagePitch * sizeof(float)) <= (size_t)kMaxSmem) {
+            const size_t sm = std::max(smem, (size_t)kTWY * 8 * 5 * kStagePitch * sizeof(float));
+            return C == 4 ? launch_tap_cluster<5, TI, TO, 4>(static_cast<const TI *>(in), static_cast<TO *>(out), B, H, W, g, tl, sm, s)
+                          : launch_tap_cluster<5, TI, TO, 3>(static_cast<const TI *>(in), static_cast<TO *>(out), B, H, W, g, tl, sm, s);
+        }
+    }
     if (smem <= (size_t)kMaxSmem) {
         auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>
                             : (KR == 5 ? layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
