@@ -314,7 +314,8 @@ def test_chain_io_policies_agree(skc):
 def test_hwc_epilogue(skc, orc):
     """A chain whose last layer is a tap layer writes HWC straight from the
     tap kernel's staged epilogue instead of planar + relayout
-    (SKC_TAP_HWC_STAGE=0); both agree bit for bit and match the oracle, for
+    (SKC_TAP_HWC_STAGE=0) or the cluster-of-C epilogue (SKC_TAP_CLUSTER=1);
+    all agree bit for bit and match the oracle, for
     C = 3 / 4, fp32 / fp16 storage, ragged sizes and both boundaries."""
     import os
     import subprocess
@@ -344,7 +345,7 @@ def test_hwc_epilogue(skc, orc):
                 np.savez(f"{td}/in.npz", img=img, L=len(layers),
                          **{f"o{i}": l.offsets for i, l in enumerate(layers)},
                          **{f"w{i}": l.weights for i, l in enumerate(layers)})
-                for var in ({"SKC_TAP_HWC_STAGE": "0"},):
+                for var in ({"SKC_TAP_HWC_STAGE": "0"}, {"SKC_TAP_CLUSTER": "1"}):
                     subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/u.npy", mode], check=True,
                                    env=dict(os.environ, **var), cwd=root)
                     assert np.array_equal(np.asarray(ours), np.load(f"{td}/u.npy")), var
