@@ -471,8 +471,11 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "#define IN_F32 " << (in_f32 ? 1 : 0) << "\n#define OUT_F32 " << (out_f32 ? 1 : 0) << "\n#define IN_HWC "
       << (in_hwc ? 1 : 0) << "\n";
     // resident CTAs per SM: 3 at KR = 3 (<= 85 registers), 2 for all-channel heads
-    // and KR >= 5 bodies (config 1's tall layer: 3.15 vs 3.23 ms at KR 5 / 2 CTAs)
-    const int minb = (allc || p.KR >= 5) ? std::min(2, sp_minb()) : sp_minb();
+    // and KR >= 5 bodies (config 1's tall layer: 3.15 vs 3.23 ms at KR 5 / 2 CTAs),
+    // and 4 for small, narrow KR = 3 bodies (64 registers: config 1's 58-position
+    // 9 x 9 layer 1.58 -> 1.47 ms; 5 CTAs spill)
+    int minb = (allc || p.KR >= 5) ? std::min(2, sp_minb()) : sp_minb();
+    if (!allc && sp_f2() == 1 && p.KR < 5 && p.npos <= 64 && p.nw <= 20) minb = env_int("SKC_SPARSE_MINB_SMALL", 4);
     s << "#define MINB " << minb << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define USE_TMA " << sp_tma() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
@@ -818,8 +821,8 @@ std::unordered_map<std::string, SpLaunch> g_memo;
 
 std::string memo_key(const double *taps, int S, int variant) {
     std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
-    const int knobs[10] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc(), sp_wy(), sp_tma(),
-                           sp_kr_wide()};
+    const int knobs[11] = {variant, sparse_mode(), sp_kr(), sp_sync(), sp_minb(), sp_f2(), sp_hwc(), sp_wy(), sp_tma(),
+                           sp_kr_wide(), env_int("SKC_SPARSE_MINB_SMALL", 0)};
     k.append((const char *)knobs, sizeof knobs);
     return k;
 }
