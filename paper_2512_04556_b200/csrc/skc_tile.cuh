@@ -107,7 +107,7 @@ __device__ __forceinline__ void store_px<float>(float *p, float v, int accumulat
 }
 
 
-// Dense-stencil path (skc_dense.cu): a layer whose merged corner footprint
+// Dense-stencil path (skc_layer.cu): a layer whose merged corner footprint
 // fits a D x D window (D <= 9) and costs fewer FMAs than 4 per tap.
 constexpr int kMaxDense = 9;
 int dense_size_for(int span);  // smallest compiled D >= span, or 0
