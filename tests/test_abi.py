@@ -73,3 +73,35 @@ def test_sparse_stencil_compiles_without_a_device(tmp_path, monkeypatch):
         t = np.ascontiguousarray(layer.taps())
         rc = lib.skc_sparse_compile_check(nat.dbl(t), t.shape[0], dt, nat.SKC_HWC, dt, nat.SKC_CHW)
         assert rc == 0, nat.last_error()
+
+
+def test_layer_routing_of_the_benchmark_complexes():
+    """skc_layer_plan (no device needed) routes config 1's wide layers to the
+    generated sparse stencil (kind 3, merged position counts 58 / 102 / 116),
+    its 5 x 5 head to the dense kernel (kind 1, D = 5: on HWC input it runs as
+    the all-channel generated head), and config 3's 4-tap Kawase layers to
+    the tap kernel (kind 0)."""
+    import ctypes
+    import numpy as np
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    lib = nat.load_library()
+
+    def plan(layer, c):
+        t = np.ascontiguousarray(layer.taps())
+        k, p = ctypes.c_int(), ctypes.c_int()
+        assert lib.skc_layer_plan(nat.dbl(t), t.shape[0], 2665, 1264, c, 0, ctypes.byref(k), ctypes.byref(p)) == 0
+        return k.value, p.value
+
+    assert [plan(l, 3) for l in synth.c1_complex().layers] == [(1, 5), (3, 58), (3, 102), (3, 116)]
+    kaw = [plan(l, 4) for l in synth.kawase_complex().layers]
+    assert kaw[0] == (1, 3) and all(k == 0 for k, _ in kaw[1:])
+    t = np.ascontiguousarray(synth.c1_complex().taps())
+    lay = np.ascontiguousarray(synth.c1_complex().layout, dtype=np.int32)
+    # fp32 chain: no input relayout (the head reads HWC), no output relayout (staged epilogue)
+    assert lib.skc_chain_relayouts(nat.dbl(t), nat.ints(lay), 4, 2665, 1264, 3, nat.SKC_F32, 0) == 0
+    tk = np.ascontiguousarray(synth.kawase_complex().taps())
+    lk = np.ascontiguousarray(synth.kawase_complex().layout, dtype=np.int32)
+    # fp16 Kawase chain: the all-channel fp16 head replaces the input relayout pass
+    assert lib.skc_chain_relayouts(nat.dbl(tk), nat.ints(lk), 6, 2160, 3840, 4, nat.SKC_F16, 0) == 0
+    assert lib.skc_chain_mid_dtype(nat.ints(lk), 6, nat.SKC_F16, nat.SKC_F16) == nat.SKC_F16
