@@ -15,8 +15,9 @@
  *   - images are HWC interleaved (the reference's (H, W, C) layout,
  *     engine.py:133-136), batched as (B, H, W, C), contiguous;
  *   - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
- *     default stream), re-entrant, and keeps no global mutable state; scratch
- *     comes from the device's stream-ordered memory pool;
+ *     default stream), re-entrant; scratch comes from a private per-device
+ *     stream-ordered memory pool (skc_release_scratch), the only process
+ *     state the library keeps besides its generated-kernel cache;
  *   - the return value is a status code; no C++ exception crosses the ABI;
  *     skc_last_error() returns a thread-local message for the last failure.
  */
@@ -57,6 +58,13 @@ extern "C" {
 
 int skc_version(void);
 const char *skc_last_error(void);
+
+/* Scratch (chain ping-pong planes, fit arenas) comes from a private
+ * stream-ordered memory pool per device that keeps freed blocks cached
+ * between calls; this returns every cached block to the driver (call after
+ * synchronising the streams that used the library).  No reference
+ * counterpart: numpy frees its temporaries itself. */
+int skc_release_scratch(void);
 
 /* Upper bound on taps per layer accepted by the filter entry points. */
 int skc_max_taps(void);
@@ -110,12 +118,21 @@ int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary,
 
 /* Layers with planar input (and, with SKC_SPARSE_HWC=1, HWC input) run a
  * sparse stencil generated for the layer (its merged positions unrolled, the
- * weights in a constant table) and compiled at run time with NVRTC
+ * weights a kernel parameter) and compiled at run time with NVRTC
  * (skc_sparse.cu) when the cost model prefers it.  This compiles the kernel
  * such a layer would run, without a device: 0 = compiled, 1 = the layer does
  * not take that path, SKC_ECUDA = the run-time compiler is missing or rejected
  * it (skc_last_error).  Layouts are SKC_HWC / SKC_CHW. */
 int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_layout, int out_dtype, int out_layout);
+
+/* Generated stencils compile in the background by default: a layer whose
+ * kernel is not ready yet runs on the tap / dense kernels (same result to
+ * fp32 rounding, so the first calls on a new position pattern can differ from
+ * later ones in the last bits).  mode 1 = compile synchronously on first use
+ * (every call of a layer runs the same kernel; also SKC_JIT=sync), 0 = async
+ * (default).  skc_jit_wait blocks until every pending compile finished. */
+int skc_set_jit_mode(int mode);
+int skc_jit_wait(void);
 
 /* Dtype of skc_chain_fwd's planar intermediates for this chain: SKC_F16 when
  * in and out are both fp16 ("fp16 storage, fp32 accumulation": every layer

@@ -7,7 +7,7 @@ signatures and errors, with the arithmetic in hand-written CUDA kernels
 `_fastpath.HAVE_NUMBA` switch; there is no CPU fallback.
 """
 
-from ._native import HAVE_CUDA, NativeError, NativeUnavailable
+from ._native import NativeError, NativeUnavailable, release_scratch
 from .engine import (
     EngineError,
     KernelComplex,
@@ -72,4 +72,13 @@ from .svfilter import (
     synthesize_filter,
 )
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
+
+
+def __getattr__(name):
+    # the reference's _fastpath.HAVE_NUMBA role; evaluated lazily so that
+    # `import paper_2512_04556_b200` never loads libskc.so by itself
+    if name == "HAVE_CUDA":
+        from . import _native
+        return _native.have_cuda()
+    raise AttributeError(name)

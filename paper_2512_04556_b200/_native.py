@@ -28,7 +28,7 @@ FIT_HDR = 8
 
 # Symbols declared in include/skc.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "skc_version", "skc_last_error", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check",
+    "skc_version", "skc_last_error", "skc_release_scratch", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check", "skc_set_jit_mode", "skc_jit_wait",
     "skc_chain_fwd",
     "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step",
@@ -80,6 +80,8 @@ def _declare(lib):
     lib.skc_chain_relayouts.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i]
     lib.skc_chain_mid_dtype.argtypes = [_ip, _i, _i, _i]
     lib.skc_sparse_compile_check.argtypes = [_dp, _i, _i, _i, _i, _i]
+    lib.skc_set_jit_mode.argtypes = [_i]
+    lib.skc_jit_wait.argtypes = []
     lib.skc_layer_plan.argtypes = [_dp, _i, _i, _i, _i, _i, _ip, _ip]
     lib.skc_chain_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _i, _dp, _ip, _i, _i, _vp]
     lib.skc_sv_fwd.argtypes = [_vp, _i, _vp, _i, _i, _i, _i, _vp, _dp, _i, _dp, _i, _ip, _i, _i,
@@ -94,7 +96,7 @@ def _declare(lib):
                                 _vp]
     lib.skc_adam_step.argtypes = [_vp, _vp, _vp, _vp, _ip, _i, _i, ctypes.POINTER(FitCfg),
                                   ctypes.c_float, _vp, _vp]
-    for name in EXPORTS[3:]:
+    for name in EXPORTS[2:]:
         getattr(lib, name).restype = _i
 
 
@@ -136,7 +138,12 @@ def have_cuda() -> bool:
     return _device_ok()
 
 
-HAVE_CUDA = have_cuda()
+def __getattr__(name):
+    # HAVE_CUDA is resolved on first access, not at import: importing the
+    # package (e.g. for its synthetic-input recipes) must not map libskc.so
+    if name == "HAVE_CUDA":
+        return have_cuda()
+    raise AttributeError(name)
 
 
 def lib():
@@ -177,3 +184,22 @@ def ptr(t):
 def fit_cfg(steps, lr_start, lr_end, beta1, beta2, eps, weight_norm, kws, loss_kind, loss_eps):
     return FitCfg(int(steps), float(lr_start), float(lr_end), float(beta1), float(beta2), float(eps),
                   WN_IDS[weight_norm], int(bool(kws)), LOSS_IDS[loss_kind], float(loss_eps))
+
+
+def release_scratch() -> None:
+    """Return the library's cached scratch blocks to the driver (skc_release_scratch)."""
+    import torch
+    torch.cuda.synchronize()
+    check(load_library().skc_release_scratch(), "release_scratch")
+
+
+def set_jit_mode(sync: bool) -> None:
+    """Generated-stencil compiles: True = synchronous on first use (every call
+    of a layer runs the same kernel), False = background (default; the tap /
+    dense kernels serve a layer until its kernel is ready)."""
+    check(load_library().skc_set_jit_mode(1 if sync else 0), "set_jit_mode")
+
+
+def jit_wait() -> None:
+    """Block until every background stencil compile has finished."""
+    check(load_library().skc_jit_wait(), "jit_wait")

@@ -30,11 +30,15 @@ int cuda_fail(cudaError_t e, const char *what);
     } while (0)
 
 // ------------------------------------------------- stream-ordered scratch ---
-// Scratch comes from the device's default memory pool (cudaMallocAsync);
-// the pool keeps freed blocks cached so steady-state calls do not hit the
-// driver allocator.
+// Scratch comes from a private per-device pool (skc_api.cu); the pool keeps
+// freed blocks cached so steady-state calls do not hit the driver allocator.
 int pool_alloc(void **p, size_t bytes, cudaStream_t s);
 void pool_free(void *p, cudaStream_t s);
+int release_scratch();
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device
+// (remembered per function and device; a failure is reported, not cached).
+int smem_optin(const void *fn, int bytes);
 
 // ----------------------------------------------------- dtype conversions ---
 template <typename T> struct IO;

@@ -400,11 +400,7 @@ static int launch_sv_tile(const void *in, void *out, const float *pmap, const fl
             (size_t)2 * nrow * q.n * sizeof(float4) + (size_t)SvPix<C>::PS * q.rows * q.pitch * 4;
         if (smem > (size_t)kMaxSmem) return -1;
         auto kern = sv_tile_il_kernel<C, TR, TI, TO>;
-        static bool il_attr = false;
-        if (!il_attr) {
-            SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-            il_attr = true;
-        }
+        if (int rc_ = smem_optin((const void *)kern, kMaxSmem)) return rc_;
         dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, TR * kSvPx));
         kern<<<grid, TR * 64, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), pmap, table, q);
         SKC_LAUNCH_CHECK("sv_tile_il_kernel");
@@ -413,11 +409,7 @@ static int launch_sv_tile(const void *in, void *out, const float *pmap, const fl
     const size_t smem = (size_t)2 * nrow * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
     if (smem > (size_t)kMaxSmem) return -1;
     auto kern = sv_tile_kernel<C, TR, TI, TO>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-        attr_set = true;
-    }
+    if (int rc_ = smem_optin((const void *)kern, kMaxSmem)) return rc_;
     dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, TR * kSvPx));
     kern<<<grid, TR * 64, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), pmap, table, q);
     SKC_LAUNCH_CHECK("sv_tile_kernel");
@@ -540,11 +532,7 @@ static int launch_sv_grid_c(const void *in, void *out, const float2 *pmap2, cons
     const size_t smem = (size_t)q.Mu * q.Mv * q.n * sizeof(float4) + (size_t)C * q.rows * q.pitch * 4;
     if (smem > (size_t)kMaxSmem) return fail(SKC_EBADARG, "grid SV basis/halo too large for shared memory");
     auto kern = sv_grid_kernel<C, float, float>;
-    static bool attr = false;
-    if (!attr) {
-        SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-        attr = true;
-    }
+    if (int rc_ = smem_optin((const void *)kern, kMaxSmem)) return rc_;
     dim3 grid(ceil_div(q.W, kSvTW), ceil_div(q.H, 4 * kSvPx));
     kern<<<grid, 256, smem, s>>>(static_cast<const float *>(in), static_cast<float *>(out), pmap2, table, q);
     SKC_LAUNCH_CHECK("sv_grid_kernel");

@@ -73,6 +73,7 @@ struct FitParams {
     float *ir_out;         // MODE_IR: (B, canvas, canvas)
     double *energy_out;    // MODE_ENERGY: (B,)
     int tgt_shared;        // MODE_ENERGY: every complex uses target 0
+    const int *idx;        // MODE_FIT relaunch: CTA i runs target idx[i] (null = i)
 };
 
 struct FitSmem {
@@ -581,10 +582,12 @@ __global__ void __launch_bounds__(kFitThreads, 2) fit_kernel(const __grid_consta
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FitSmem &S = *reinterpret_cast<FitSmem *>(smem_raw);
     float *arena = reinterpret_cast<float *>(smem_raw + (sizeof(FitSmem) + 15) / 16 * 16);
-    const int b = blockIdx.x;
+    const int b = p.idx ? p.idx[blockIdx.x] : blockIdx.x;
     const int blk = p.L * p.nmax * 3;
     int *status = p.status + 4 * b;
-    float *gslots = p.scratch + (size_t)b * p.L * p.cap * p.cap;
+    // overflow slots are per launched CTA: a relaunch of parked targets only
+    // sizes scratch for those
+    float *gslots = p.scratch + (size_t)blockIdx.x * p.L * p.cap * p.cap;
 
     if (p.mode != MODE_FIT) {
         // backward()/synthesize_ir(): parameters come in as effective weights
@@ -914,28 +917,23 @@ static int fill_params(FitParams &p, int B, const int *layout, int L, int nmax, 
 }
 
 static int set_fit_attrs() {
-    static bool attr = false;
-    const int smem = kFitSmem;
-    if (!attr) {
-        SKC_CUDA(cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        SKC_CUDA(cudaFuncSetAttribute(fit_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        SKC_CUDA(cudaFuncSetAttribute(adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    return SKC_OK;
+    int rc;
+    if ((rc = smem_optin((const void *)fit_kernel, kFitSmem))) return rc;
+    if ((rc = smem_optin((const void *)fit_init_kernel, kFitSmem))) return rc;
+    return smem_optin((const void *)adam_kernel, kFitSmem);
 }
 
-static int fit_launch(const FitParams &p, cudaStream_t s) {
+static int fit_launch(const FitParams &p, cudaStream_t s, int grid = -1) {
     int rc = set_fit_attrs();
     if (rc) return rc;
-    fit_kernel<<<p.B, kFitThreads, kFitSmem, s>>>(p);
+    fit_kernel<<<grid < 0 ? p.B : grid, kFitThreads, kFitSmem, s>>>(p);
     SKC_LAUNCH_CHECK("fit_kernel");
     return SKC_OK;
 }
 
-static int alloc_scratch(FitParams &p, int cap, cudaStream_t s) {
+static int alloc_scratch(FitParams &p, int cap, cudaStream_t s, int ctas = -1) {
     p.cap = cap;
-    const size_t bytes = (size_t)p.B * p.L * cap * cap * sizeof(float);
+    const size_t bytes = (size_t)(ctas < 0 ? p.B : ctas) * p.L * cap * cap * sizeof(float);
     void *ptr = nullptr;
     int rc = pool_alloc(&ptr, bytes, s);
     if (rc) return rc;
@@ -1081,32 +1079,66 @@ int skc_fit_run(float *state, int B, const int *layout, int L, int nmax, const f
     p.status = status;
     const size_t stride = SKC_FIT_STATE_FLOATS(L, nmax);
     std::vector<int> hdr((size_t)B * 4), hs((size_t)B * 4);
-    // scratch capacity from the current canvases (+ growth slack); kernels
-    // that outgrow it park with kNeedGrow and are resumed with a larger one
-    for (int attempt = 0; attempt < 64; ++attempt) {
-        SKC_CUDA(cudaMemcpy2DAsync(hdr.data(), 4 * sizeof(int), state, stride * sizeof(float),
-                                   4 * sizeof(int), B, cudaMemcpyDeviceToHost, s));
-        SKC_CUDA(cudaStreamSynchronize(s));
-        // generous first capacity (diverging fits grow their canvas every step;
-        // a parked target resumes alone, so relaunches are expensive tails)
-        int cap = 1;
-        for (int b = 0; b < B; ++b) cap = std::max(cap, hdr[4 * b + 1]);
-        cap = attempt == 0 ? 2 * cap + 32 : cap + cap / 2 + 64;
-        if ((rc = alloc_scratch(p, cap, s))) return rc;
-        rc = fit_launch(p, s);
+    // Every target starts in one launch with a generous scratch canvas.  A
+    // target whose canvas outgrows it parks (kNeedGrow); only the parked
+    // targets are relaunched, compacted through an index list with scratch
+    // sized for them (optim.py:429-434 grows only that fit's canvas).  A
+    // canvas beyond kMaxFitCanvas stops that target with SKC_ETRUNC in its
+    // status row; the rest of the batch is unaffected.
+    constexpr int kMaxFitCanvas = 4097;
+    SKC_CUDA(cudaMemcpy2DAsync(hdr.data(), 4 * sizeof(int), state, stride * sizeof(float),
+                               4 * sizeof(int), B, cudaMemcpyDeviceToHost, s));
+    SKC_CUDA(cudaStreamSynchronize(s));
+    int cap = 1;
+    for (int b = 0; b < B; ++b) cap = std::max(cap, hdr[4 * b + 1]);
+    cap = std::min(2 * cap + 32, kMaxFitCanvas);
+    std::vector<int> parked;
+    int *d_idx = nullptr;
+    for (int attempt = 0;; ++attempt) {
+        const int ctas = attempt == 0 ? B : (int)parked.size();
+        p.idx = attempt == 0 ? nullptr : d_idx;
+        if ((rc = alloc_scratch(p, cap, s, ctas))) break;
+        rc = fit_launch(p, s, ctas);
         if (rc == SKC_OK) {
             cudaError_t e = cudaMemcpyAsync(hs.data(), status, hs.size() * sizeof(int),
                                             cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaMemcpy2DAsync(hdr.data(), 4 * sizeof(int), state, stride * sizeof(float),
+                                                        4 * sizeof(int), B, cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) rc = cuda_fail(e, "skc_fit_run status");
         }
         pool_free(p.scratch, s);
-        if (rc) return rc;
-        bool again = false;
-        for (int b = 0; b < B; ++b) again |= hs[4 * b] == kNeedGrow;
-        if (!again) return SKC_OK;
+        if (rc) break;
+        parked.clear();
+        int need = 0;
+        for (int b = 0; b < B; ++b) {
+            if (hs[4 * b] != kNeedGrow) continue;
+            if (hdr[4 * b + 1] > kMaxFitCanvas) {
+                const int row[4] = {SKC_ETRUNC, 0, -1, hs[4 * b + 3]};
+                cudaError_t e = cudaMemcpyAsync(status + 4 * b, row, sizeof(row), cudaMemcpyHostToDevice, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess) { rc = cuda_fail(e, "skc_fit_run status"); break; }
+                continue;
+            }
+            parked.push_back(b);
+            need = std::max(need, hdr[4 * b + 1]);
+        }
+        if (rc || parked.empty()) break;
+        cap = std::min(need + need / 2 + 64, kMaxFitCanvas);
+        // bound one relaunch's scratch; targets left out stay parked and run
+        // in a later round of this loop
+        const size_t per = (size_t)L * cap * cap * sizeof(float);
+        const size_t fit = std::max<size_t>(1, (size_t(8) << 30) / per);
+        if (parked.size() > fit) parked.resize(fit);
+        if (d_idx) pool_free(d_idx, s);
+        d_idx = nullptr;
+        if ((rc = pool_alloc((void **)&d_idx, parked.size() * sizeof(int), s))) break;
+        cudaError_t e = cudaMemcpyAsync(d_idx, parked.data(), parked.size() * sizeof(int), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // `parked` is reused next round
+        if (e != cudaSuccess) { rc = cuda_fail(e, "skc_fit_run index"); break; }
     }
-    return fail(SKC_ECUDA, "fit canvas kept growing (diverging fit?)");
+    if (d_idx) pool_free(d_idx, s);
+    return rc;
 }
 
 int skc_adam_step(float *params, const float *grads, float *m, float *v, const int *layout, int L,

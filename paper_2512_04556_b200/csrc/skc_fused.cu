@@ -340,9 +340,7 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
     if (rc) return rc;
     if ((rc = pool_alloc(&buf[1], n * sizeof(float), s))) { pool_free(buf[0], s); return rc; }
     rc = relayout(in, idt, false, buf[0], SKC_F32, true, B, H, W, C, s);
-    static cudaError_t attr =
-        cudaFuncSetAttribute(fused2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
-    if (rc == SKC_OK && attr != cudaSuccess) rc = cuda_fail(attr, "cudaFuncSetAttribute(fused2)");
+    if (rc == SKC_OK) rc = smem_optin((const void *)fused2_kernel, kMaxSmem);
     int k = 0;
     for (int gi = 0; gi < ng && rc == SKC_OK; ++gi, k ^= 1) {
         dim3 grid(ceil_div(W, kF2TW) * C, ceil_div(H, kF2TH), B);

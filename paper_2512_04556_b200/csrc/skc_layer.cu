@@ -602,7 +602,7 @@ template <int KR, typename TI, typename TO, int CC>
 static int launch_tap_cluster(const TI *in, TO *out, int B, int H, int W, const LGeom &g, const TapList &tl,
                               size_t smem, cudaStream_t s) {
     auto kern = layer_tap_cluster_kernel<KR, TI, TO, CC>;
-    static int attr = set_smem_attr(kern);
+    const int attr = set_smem_attr(kern);
     if (attr) return attr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ceil_div(W, kTTW) * CC, ceil_div(H, kTWY * 8 * KR), B);
@@ -872,8 +872,7 @@ static LGeom make_geom(int H, int W, int C, int boundary, int accumulate, int tw
 
 template <typename K>
 static int set_smem_attr(K kern) {
-    SKC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    return SKC_OK;
+    return smem_optin((const void *)kern, kMaxSmem);
 }
 
 // Rows per thread of the tap kernel: SKC_TAP_KR (5 or 7) overrides; default 5
@@ -944,9 +943,9 @@ static int launch_taps(const void *in, void *out, int B, int H, int W, int C, co
     if (smem <= (size_t)kMaxSmem) {
         auto kern = KR == 7 ? layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>
                             : (KR == 5 ? layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL> : layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
-        static int attr3 = set_smem_attr(layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
-        static int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
-        static int attr7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>);
+        const int attr3 = set_smem_attr(layer_tap_kernel<3, TI, TO, IN_PL, OUT_PL>);
+        const int attr5 = set_smem_attr(layer_tap_kernel<5, TI, TO, IN_PL, OUT_PL>);
+        const int attr7 = set_smem_attr(layer_tap_kernel<7, TI, TO, IN_PL, OUT_PL>);
         if (attr3 || attr5 || attr7) return attr3 ? attr3 : (attr5 ? attr5 : attr7);
         dim3 grid(ceil_div(W, kTTW) * C, ceil_div(H, TH), B);
         kern<<<grid, kTWX * kTWY * 32, smem, s>>>(pin, pout, g, tl);
@@ -975,7 +974,7 @@ template <int D, int SH, typename T>
 static int launch_stencil2_d(const void *in, void *out, int B, int C, const DenseList2 &dl, const LGeom &g,
                              cudaStream_t s) {
     auto kern = layer_stencil2_kernel<D, SH, T>;
-    static int attr = set_smem_attr(kern);
+    const int attr = set_smem_attr(kern);
     if (attr) return attr;
     const size_t smem = tile_smem<T, true>(g);
     dim3 grid(ceil_div(g.W, kDenTW) * C, ceil_div(g.H, kF2TH), B);
@@ -1001,7 +1000,7 @@ static int launch_stencil_d(const void *in, void *out, int B, int H, int W, int 
                             const LGeom &g, cudaStream_t s) {
     const size_t smem = tile_smem<TI, IN_PL>(g);
     auto kern = layer_stencil_kernel<D, KR, TI, TO, IN_PL, OUT_PL>;
-    static int attr = set_smem_attr(kern);
+    const int attr = set_smem_attr(kern);
     if (attr) return attr;
     dim3 grid(ceil_div(W, kDenTW) * C, ceil_div(H, kDenWY * 8 * KR), B);
     kern<<<grid, kDenWX * kDenWY * 32, smem, s>>>(static_cast<const TI *>(in), static_cast<TO *>(out), g, dl);

@@ -15,9 +15,11 @@
 // per-tap window reloads, no zero work.  Config 1's radius-8 layer (32 taps ->
 // 102 positions in 15 x 17) reads ~10 words per output instead of ~41.
 //
-// The kernel source is emitted per layer (weights as hex-float immediates),
-// compiled once per process with NVRTC (dlopen'ed libnvrtc.so.12, no link-time
-// dependency), loaded with cudaLibraryLoadData and cached by source text.
+// The kernel source is emitted per position pattern (the merged weights are a
+// kernel parameter), compiled with NVRTC (dlopen'ed libnvrtc.so.12, no
+// link-time dependency) on a background thread while the tap / dense kernels
+// serve the layer (SKC_JIT=sync waits instead), loaded with
+// cudaLibraryLoadData and kept in a bounded LRU cache keyed by the source.
 // SKC_SPARSE=0 disables the path; SKC_SPARSE=1 forces it for every eligible
 // layer regardless of the cost model; SKC_SPARSE_DUMP=<dir> writes the
 // generated sources.
@@ -27,6 +29,10 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -229,7 +235,8 @@ __device__ __forceinline__ void cp16(float *dst, const float *src) {
 }
 
 extern "C" __global__ void __launch_bounds__(NWARP * 32, MINB)
-skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W, int C, int clamp) {
+skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W, int C, int clamp,
+                   const __grid_constant__ KWT kw) {
     extern __shared__ __align__(16) float smem[];
     const long long hw = (long long)H * W;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -455,10 +462,18 @@ const char *kSpHwcEpilogue = R"CUDA(
     }
 )CUDA";
 
-std::string hexf(float v) {
-    char buf[64];
-    std::snprintf(buf, sizeof buf, "%af", (double)v);
-    return buf;
+// The kernel parameter the generated body reads: (K, K) per position, in
+// the body's order (stencil row a, then position within the row).
+std::vector<float> kw_table(const SpPlan &p) {
+    std::vector<float> t;
+    t.reserve(2 * std::max(1, p.npos));
+    for (int a = 0; a < p.Dy; ++a)
+        for (const SpPos &e : p.rows[a]) {
+            t.push_back(e.k);
+            t.push_back(e.k);
+        }
+    if (t.empty()) t.assign(2, 0.f);
+    return t;
 }
 
 std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0) {
@@ -482,13 +497,12 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "#define KR " << p.KR << "\n#define TH " << p.TH << "\n#define PITCH " << p.pitch << "\n#define ROWS "
       << p.nrows << "\n#define DX0 " << p.DX0 << "\n#define DY0 " << p.dy_min << "\n#define NW " << p.nw << "\n";
     const bool f2 = sp_f2() != 0;
+    // the merged weights arrive as a kernel parameter (constant bank 0), one
+    // (K, K) pair per position in the body's order: the source -- and so the
+    // compiled kernel -- depends only on the position pattern, and a layer
+    // with new weights at the same positions reuses it
+    s << "#define NPOS " << std::max(1, p.npos) << "\nstruct KWT { float2 k[NPOS]; };\n#define KW kw.k\n";
     if (f2) {
-        // (K, K) pairs for fma.rn.f32x2, in position order of the body below
-        s << "__constant__ float2 KW[" << std::max(1, p.npos) << "] = {";
-        int n = 0;
-        for (int a = 0; a < p.Dy; ++a)
-            for (const SpPos &e : p.rows[a]) s << (n++ ? ", " : "") << "{" << hexf(e.k) << ", " << hexf(e.k) << "}";
-        s << "};\n";
         s << "__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {\n"
              "    unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a), rb = *reinterpret_cast<unsigned long long *>(&b),\n"
              "        rc = *reinterpret_cast<unsigned long long *>(&c), rd;\n"
@@ -496,6 +510,8 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
              "    return *reinterpret_cast<float2 *>(&rd);\n}\n";
     }
     s << kSpPrelude;
+    std::vector<int> first(p.Dy + 1, 0);  // index of stencil row a's first position in KW
+    for (int a = 0; a < p.Dy; ++a) first[a + 1] = first[a] + (int)p.rows[a].size();
     if (f2) {
         // Window words as aligned pairs wp<m> = (w[2m], w[2m+1]).  A position at
         // window column c0 feeds output j from w[c0 + j]: for even c0 the output
@@ -503,8 +519,6 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
         // (2m+1, 2m+2) do, with outputs 0 and 7 as scalar FFMAs -- two
         // accumulator sets (e: even-paired, o: odd-paired + 2 scalars), summed
         // in the epilogue.  No register moves to re-pair the window.
-        std::vector<int> first(p.Dy + 1, 0);  // index of row a's first position in KW
-        for (int a = 0; a < p.Dy; ++a) first[a + 1] = first[a] + (int)p.rows[a].size();
         s << "    float2";
         for (int i = 0; i < p.KR; ++i)
             for (int j = 0; j < 4; ++j) s << (i || j ? ", " : " ") << "e" << i << "_" << j << " = make_float2(0.f, 0.f)";
@@ -627,8 +641,9 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
               << " = t.y; w" << 4 * ch + 2 << " = t.z; w" << 4 * ch + 3 << " = t.w; }\n";
         for (int a = a_lo; a <= a_hi; ++a) {
             const int i = q - a;
-            for (const SpPos &e : p.rows[a]) {
-                const std::string k = hexf(e.k);
+            for (size_t ei = 0; ei < p.rows[a].size(); ++ei) {
+                const SpPos &e = p.rows[a][ei];
+                const std::string k = "KW[" + std::to_string(first[a] + (int)ei) + "].x";
                 for (int j = 0; j < 8; ++j)
                     s << "        a" << i << "_" << j << " = fmaf(" << k << ", w" << p.SH + e.b + j << ", a" << i << "_" << j
                       << ");\n";
@@ -656,6 +671,7 @@ struct Nvrtc {
     nvrtcResult (*cubin_size)(nvrtcProgram, size_t *) = nullptr;
     nvrtcResult (*get_cubin)(nvrtcProgram, char *) = nullptr;
     nvrtcResult (*destroy)(nvrtcProgram *) = nullptr;
+    nvrtcResult (*version)(int *, int *) = nullptr;
 };
 
 Nvrtc &nvrtc() {
@@ -675,6 +691,7 @@ Nvrtc &nvrtc() {
         r.cubin_size = (decltype(r.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
         r.get_cubin = (decltype(r.get_cubin))dlsym(h, "nvrtcGetCUBIN");
         r.destroy = (decltype(r.destroy))dlsym(h, "nvrtcDestroyProgram");
+        r.version = (decltype(r.version))dlsym(h, "nvrtcVersion");
         r.ok = r.create && r.compile && r.log_size && r.get_log && r.cubin_size && r.get_cubin && r.destroy;
         if (!r.ok) r.why = "libnvrtc lacks an expected symbol";
         return r;
@@ -721,22 +738,33 @@ std::vector<char> compile_cubin(const std::string &src, std::string *why) {
     return cubin;
 }
 
-// On-disk cubin cache (a cold cache only costs compile time): $SKC_CACHE_DIR,
-// else $XDG_CACHE_HOME/skc, else $HOME/.cache/skc; keyed by an FNV-1a hash
-// and the length of the generated source.
+unsigned long long fnv1a(const std::string &src) {
+    unsigned long long h = 1469598103934665603ULL;
+    for (unsigned char ch : src) h = (h ^ ch) * 1099511628211ULL;
+    return h;
+}
+
+// Optional on-disk cubin cache (a cold cache only costs compile time).  Off
+// unless SKC_CACHE_DIR names a directory; the directory must belong to this
+// user and must not be group/world-writable (a shared writable cache could
+// inject code).  The key covers the generated source (FNV-1a + length), the
+// NVRTC version and the driver version.
 std::string cache_path(const std::string &src) {
-    std::string dir;
-    if (const char *d = std::getenv("SKC_CACHE_DIR")) dir = d;
-    else if (const char *x = std::getenv("XDG_CACHE_HOME")) dir = std::string(x) + "/skc";
-    else if (const char *h = std::getenv("HOME")) dir = std::string(h) + "/.cache/skc";
-    else return "";
-    if (dir.empty() || dir == "0") return "";
-    unsigned long long hsh = 1469598103934665603ULL;
-    for (unsigned char ch : src) hsh = (hsh ^ ch) * 1099511628211ULL;
-    char name[96];
-    std::snprintf(name, sizeof name, "/sparse_sm100a_%016llx_%zu.cubin", hsh, src.size());
+    const char *d = std::getenv("SKC_CACHE_DIR");
+    if (!d || !*d || std::string(d) == "0") return "";
+    const std::string dir = d;
     for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p without a shell
-        if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0755);
+        if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0700);
+    struct stat st;
+    if (::stat(dir.c_str(), &st) != 0 || !S_ISDIR(st.st_mode) || st.st_uid != ::geteuid() || (st.st_mode & 022))
+        return "";
+    int nv_major = 0, nv_minor = 0, drv = 0;
+    Nvrtc &n = nvrtc();
+    if (n.ok && n.version) n.version(&nv_major, &nv_minor);
+    cudaDriverGetVersion(&drv);
+    char name[160];
+    std::snprintf(name, sizeof name, "/sparse_sm100a_nvrtc%d.%d_drv%d_%016llx_%zu.cubin", nv_major, nv_minor, drv,
+                  fnv1a(src), src.size());
     return dir + name;
 }
 
@@ -765,35 +793,140 @@ std::vector<char> cached_cubin(const std::string &src, std::string *why) {
     return cubin;
 }
 
+// ------------------------------------------------------- kernel cache ---
+// Compiled kernels keyed by their source (hash + length; the source names
+// only the position pattern and the variant).  A miss starts an NVRTC
+// compile on a background thread and returns nullptr, so the caller serves
+// the layer with the tap / dense kernels until the kernel is ready (first
+// calls on a new complex are not stalled by the 1-3 s compile); in sync mode
+// (SKC_JIT=sync or skc_set_jit_mode(1)) the caller waits instead, so every
+// call of a layer runs the same kernel.  At most kMaxKernels stay loaded
+// (least recently used are unloaded).
+enum { kCompiling = 0, kReady = 1, kFailed = 2 };
 struct SpKernel {
+    int state = kCompiling;
+    bool built = false;          // background compile finished (cubin or why set)
+    std::vector<char> cubin;
+    std::string why;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
-    bool failed = false;
+    unsigned long long devmask = 0;  // devices whose shared-memory opt-in is set
+    size_t smem = 0;
+    unsigned long long last_use = 0;
 };
-
+struct Key {
+    unsigned long long h;
+    size_t n;
+    bool operator==(const Key &o) const { return h == o.h && n == o.n; }
+};
+struct KeyHash {
+    size_t operator()(const Key &k) const { return (size_t)(k.h ^ (k.n * 0x9e3779b97f4a7c15ULL)); }
+};
+constexpr size_t kMaxKernels = 128;
 std::mutex g_mu;
-std::unordered_map<std::string, SpKernel> g_cache;
+std::condition_variable g_cv;
+std::unordered_map<Key, std::shared_ptr<SpKernel>, KeyHash> g_cache;
+unsigned long long g_clock = 0;
+std::atomic<int> g_jit_mode{-1};
 
-// The compiled kernel for `src` (compiling on first use); nullptr when the
-// run-time compiler is unavailable or failed (the caller takes the tap path).
-cudaKernel_t get_kernel(const std::string &src, size_t smem) {
-    std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_cache.find(src);
-    if (it != g_cache.end()) return it->second.failed ? nullptr : it->second.kern;
-    SpKernel k;
-    std::string why;
-    const std::vector<char> cubin = cached_cubin(src, &why);
-    if (cubin.empty() ||
-        cudaLibraryLoadData(&k.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-        cudaLibraryGetKernel(&k.kern, k.lib, "skc_sparse_stencil") != cudaSuccess ||
-        cudaFuncSetAttribute((const void *)k.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess) {
-        cudaGetLastError();
-        k.failed = true;
-        if (std::getenv("SKC_SPARSE_VERBOSE")) std::fprintf(stderr, "skc sparse stencil unavailable: %s\n", why.c_str());
+int jit_sync() {
+    int m = g_jit_mode.load();
+    if (m < 0) {
+        const char *e = std::getenv("SKC_JIT");
+        m = (e && std::string(e) == "sync") ? 1 : 0;
+        g_jit_mode.store(m);
     }
-    g_cache.emplace(src, k);
-    return k.failed ? nullptr : k.kern;
+    return m;
+}
+
+void evict_lru_locked() {
+    while (g_cache.size() > kMaxKernels) {
+        auto victim = g_cache.end();
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+            if (it->second->state != kCompiling && (victim == g_cache.end() || it->second->last_use < victim->second->last_use))
+                victim = it;
+        if (victim == g_cache.end()) return;
+        SpKernel &k = *victim->second;
+        if (k.lib) {
+            // launches of this kernel may still be queued: drain the devices it ran on
+            int cur = 0;
+            cudaGetDevice(&cur);
+            for (int d = 0; d < 64; ++d)
+                if (k.devmask >> d & 1ULL) {
+                    cudaSetDevice(d);
+                    cudaDeviceSynchronize();
+                }
+            cudaSetDevice(cur);
+            cudaLibraryUnload(k.lib);
+            cudaGetLastError();
+        }
+        g_cache.erase(victim);
+    }
+}
+
+// Load a finished cubin (caller holds g_mu).
+void finish_locked(SpKernel &k) {
+    if (k.cubin.empty() ||
+        cudaLibraryLoadData(&k.lib, k.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&k.kern, k.lib, "skc_sparse_stencil") != cudaSuccess) {
+        cudaGetLastError();
+        k.state = kFailed;
+        if (std::getenv("SKC_SPARSE_VERBOSE")) std::fprintf(stderr, "skc sparse stencil unavailable: %s\n", k.why.c_str());
+    } else {
+        k.state = kReady;
+    }
+    std::vector<char>().swap(k.cubin);
+}
+
+// The compiled kernel for `src` (see above); nullptr while it compiles in
+// the background or when the run-time compiler is unavailable / failed.
+std::shared_ptr<SpKernel> get_kernel(const Key &key, const std::string &src, size_t smem) {
+    std::unique_lock<std::mutex> lock(g_mu);
+    auto it = g_cache.find(key);
+    std::shared_ptr<SpKernel> k;
+    if (it == g_cache.end()) {
+        k = std::make_shared<SpKernel>();
+        k->smem = smem;
+        g_cache.emplace(key, k);
+        evict_lru_locked();
+        if (jit_sync()) {
+            lock.unlock();
+            std::string why;
+            std::vector<char> cubin = cached_cubin(src, &why);
+            lock.lock();
+            k->cubin.swap(cubin);
+            k->why = why;
+            k->built = true;
+        } else {
+            std::thread([k, src] {
+                std::string why;
+                std::vector<char> cubin = cached_cubin(src, &why);
+                std::lock_guard<std::mutex> lk(g_mu);
+                k->cubin.swap(cubin);
+                k->why = why;
+                k->built = true;
+                g_cv.notify_all();
+            }).detach();
+        }
+    } else {
+        k = it->second;
+    }
+    if (k->state == kCompiling && !k->built && jit_sync()) g_cv.wait(lock, [&] { return k->built; });
+    if (k->state == kCompiling && k->built) finish_locked(*k);
+    k->last_use = ++g_clock;
+    return k->state == kReady ? k : nullptr;
+}
+
+// Wait for every background compile to finish (skc_jit_wait).
+void wait_all_compiles() {
+    std::unique_lock<std::mutex> lock(g_mu);
+    g_cv.wait(lock, [] {
+        for (auto &kv : g_cache)
+            if (kv.second->state == kCompiling && !kv.second->built) return false;
+        return true;
+    });
+    for (auto &kv : g_cache)
+        if (kv.second->state == kCompiling && kv.second->built) finish_locked(*kv.second);
 }
 
 // All-channel head eligibility (and its shared memory in p.smem): C
@@ -807,17 +940,21 @@ bool allc_ok(SpPlan &p, int S, int C, bool in_f32) {
 }
 
 // Per-layer memo (host cost per launch is a hash lookup, not a plan and a
-// 300 KB source string): keyed by the tap bytes, the variant and the knobs.
+// 300 KB source string): keyed by the tap bytes, the variant and the knobs;
+// holds the launch geometry, the kernel's cache key and the layer's weight
+// table.  Bounded: cleared when it exceeds kMaxMemo entries.
 struct SpLaunch {
     bool eligible = false;
     int npos = 0, TH = 0;
     double words_per_out = 0.0;
     size_t smem = 0;
-    cudaKernel_t kern = nullptr;  // null: the run-time compiler failed
-    unsigned long long devmask = 0;  // devices whose shared-memory opt-in is set
+    Key key{0, 0};
+    std::string src;           // kept until the kernel is ready
+    std::vector<float> kw;     // (K, K) per position: the kernel parameter
 };
+constexpr size_t kMaxMemo = 4096;
 std::mutex g_memo_mu;
-std::unordered_map<std::string, SpLaunch> g_memo;
+std::unordered_map<std::string, std::shared_ptr<SpLaunch>> g_memo;
 
 std::string memo_key(const double *taps, int S, int variant) {
     std::string k((const char *)taps, sizeof(double) * 3 * (size_t)S);
@@ -827,6 +964,18 @@ std::string memo_key(const double *taps, int S, int variant) {
     return k;
 }
 
+void memo_put(const std::string &key, std::shared_ptr<SpLaunch> l) {
+    std::lock_guard<std::mutex> lock(g_memo_mu);
+    if (g_memo.size() >= kMaxMemo) g_memo.clear();
+    g_memo[key] = std::move(l);
+}
+
+std::shared_ptr<SpLaunch> memo_get(const std::string &key) {
+    std::lock_guard<std::mutex> lock(g_memo_mu);
+    auto it = g_memo.find(key);
+    return it == g_memo.end() ? nullptr : it->second;
+}
+
 }  // namespace
 
 // Plan query for skc_layer_plan: 1 and the position count / LDS words per
@@ -834,27 +983,18 @@ std::string memo_key(const double *taps, int S, int variant) {
 // run-time compiler is not consulted).
 bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
     const std::string key = memo_key(taps, S, -1);
-    {
-        std::lock_guard<std::mutex> lock(g_memo_mu);
-        auto it = g_memo.find(key);
-        if (it != g_memo.end()) {
-            *npos = it->second.npos;
-            *words_per_out = it->second.words_per_out;
-            return it->second.eligible;
-        }
+    std::shared_ptr<SpLaunch> l = memo_get(key);
+    if (!l) {
+        const SpPlan p = make_plan(taps, S);
+        l = std::make_shared<SpLaunch>();
+        l->eligible = eligible(p, S);
+        l->npos = p.npos;
+        l->words_per_out = p.words_per_out;
+        memo_put(key, l);
     }
-    const SpPlan p = make_plan(taps, S);
-    SpLaunch l;
-    l.eligible = eligible(p, S);
-    l.npos = p.npos;
-    l.words_per_out = p.words_per_out;
-    {
-        std::lock_guard<std::mutex> lock(g_memo_mu);
-        g_memo.emplace(key, l);
-    }
-    *npos = p.npos;
-    *words_per_out = p.words_per_out;
-    return l.eligible;
+    *npos = l->npos;
+    *words_per_out = l->words_per_out;
+    return l->eligible;
 }
 
 // Would an HWC head (fp32 or fp16 storage, planar output of the same dtype)
@@ -876,43 +1016,43 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (in_hwc && !allc && sp_hwc() != 1) return -1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4));
-    SpLaunch l;
-    bool found = false;
-    {
-        std::lock_guard<std::mutex> lock(g_memo_mu);
-        auto it = g_memo.find(key);
-        if (it != g_memo.end()) {
-            l = it->second;
-            found = true;
-        }
-    }
-    if (!found) {
+    std::shared_ptr<SpLaunch> l = memo_get(key);
+    if (!l) {
         SpPlan p = make_plan(taps, S);
-        l.eligible = eligible(p, S);
-        if (allc) l.eligible = allc_ok(p, S, allc, in_f32);
-        l.npos = p.npos;
-        l.TH = p.TH;
-        l.words_per_out = p.words_per_out;
-        l.smem = p.smem;
-        if (l.eligible) l.kern = get_kernel(generate(p, in_f32, out_f32, out_pl, in_hwc, allc), p.smem);
-        std::lock_guard<std::mutex> lock(g_memo_mu);
-        g_memo[key] = l;
+        l = std::make_shared<SpLaunch>();
+        l->eligible = eligible(p, S);
+        if (allc) l->eligible = allc_ok(p, S, allc, in_f32);
+        l->npos = p.npos;
+        l->TH = p.TH;
+        l->words_per_out = p.words_per_out;
+        l->smem = p.smem;
+        if (l->eligible) {
+            l->src = generate(p, in_f32, out_f32, out_pl, in_hwc, allc);
+            l->key = Key{fnv1a(l->src), l->src.size()};
+            l->kw = kw_table(p);
+        }
+        memo_put(key, l);
     }
-    if (!l.eligible || !l.kern) return -1;
+    if (!l->eligible) return -1;
+    std::shared_ptr<SpKernel> k = get_kernel(l->key, l->src, l->smem);
+    if (!k) return -1;   // compiling in the background (or unavailable): tap / dense kernels
     {   // the shared-memory opt-in is per device: set it once for each device used
         int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess && dev < 64 && !(l.devmask >> dev & 1ULL)) {
-            const cudaError_t ae = cudaFuncSetAttribute((const void *)l.kern,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l.smem);
-            if (ae != cudaSuccess) return cuda_fail(ae, "cudaFuncSetAttribute(skc_sparse_stencil)");
-            std::lock_guard<std::mutex> lock(g_memo_mu);
-            g_memo[key].devmask |= 1ULL << dev;
+        if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
+            std::lock_guard<std::mutex> lock(g_mu);
+            if (!(k->devmask >> dev & 1ULL)) {
+                const cudaError_t ae = cudaFuncSetAttribute((const void *)k->kern,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l->smem);
+                if (ae != cudaSuccess) return cuda_fail(ae, "cudaFuncSetAttribute(skc_sparse_stencil)");
+                k->devmask |= 1ULL << dev;
+            }
         }
     }
-    dim3 grid(ceil_div(W, kSpTW) * (allc ? 1 : C), ceil_div(H, l.TH), B);
+    dim3 grid(ceil_div(W, kSpTW) * (allc ? 1 : C), ceil_div(H, l->TH), B);
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
-    void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp};
-    const cudaError_t e = cudaLaunchKernel((const void *)l.kern, grid, dim3(128 * sp_wy()), args, l.smem, s);
+    void *kwp = (void *)l->kw.data();
+    void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp, kwp};
+    const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * sp_wy()), args, l->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
 }
@@ -937,6 +1077,17 @@ int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_lay
     const std::vector<char> cubin = compile_cubin(
         generate(p, in_dtype == SKC_F32, out_dtype == SKC_F32, out_layout == SKC_CHW, in_layout == SKC_HWC, allc), &why);
     return cubin.empty() ? fail(SKC_ECUDA, why) : SKC_OK;
+}
+
+int skc_set_jit_mode(int mode) {
+    if (mode != 0 && mode != 1) return skc::fail(SKC_EBADARG, "jit mode must be 0 (async) or 1 (sync)");
+    skc::g_jit_mode.store(mode);
+    return SKC_OK;
+}
+
+int skc_jit_wait(void) {
+    skc::wait_all_compiles();
+    return SKC_OK;
 }
 
 }  // extern "C"

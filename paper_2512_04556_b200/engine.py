@@ -232,13 +232,21 @@ def apply_complex_batch(imgs, cpx: KernelComplex, boundary: str = "zero", out=No
                         chunk: int = 4):
     """Batched frames (B, H, W[, C]) through one complex in a single call per layer.
 
-    Device tensors are filtered in place on the device.  Pinned host tensors
-    with a pinned host `out` stream through the GPU in chunks of `chunk`
-    frames, overlapping both copy directions with the kernels."""
+    Device tensors are filtered on the device.  A pinned, contiguous float32
+    or float16 host tensor with a pinned host `out` of the same shape and
+    dtype streams through the GPU in chunks of `chunk` frames, overlapping
+    both copy directions with the kernels; the call synchronises before it
+    returns, so `out` holds the result.  Every other input (numpy, other
+    dtypes, pageable memory) goes through the generic path (fp32 on device,
+    result converted back)."""
     t = torch()
     if (isinstance(imgs, t.Tensor) and not imgs.is_cuda and imgs.is_pinned() and isinstance(out, t.Tensor)
-            and not out.is_cuda and out.is_pinned() and imgs.dim() in (3, 4)):
-        return _pipelined_host_batch(imgs, cpx, boundary, out, chunk)
+            and not out.is_cuda and out.is_pinned() and imgs.dim() in (3, 4)
+            and imgs.dtype in (t.float32, t.float16) and out.dtype == imgs.dtype
+            and tuple(out.shape) == tuple(imgs.shape) and imgs.is_contiguous() and out.is_contiguous()):
+        _pipelined_host_batch(imgs, cpx, boundary, out, chunk)
+        t.cuda.current_stream().synchronize()   # `out` is complete when the call returns
+        return out
     im = Image(imgs, batched=True)
     res = _chain(im, cpx, boundary)
     if out is not None:

@@ -140,6 +140,8 @@ def _raise_status(st, what: str):
                          + (f", sample {sample}" if sample >= 0 else " (accumulated overflow)"))
     if code == nat.SKC_EDEGENERATE:
         raise OptimError(f"SUM normalization degenerate at layer {layer}: |weight sum| < {SUM_DEGENERACY_EPS}")
+    if code == nat.SKC_ETRUNC:
+        raise OptimError(f"{what}: canvas grew beyond the device limit at step {int(st[3])} (diverging fit)")
     if code != nat.SKC_OK:
         raise OptimError(f"{what}: device status {code}")
 

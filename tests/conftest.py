@@ -11,6 +11,12 @@ if str(ROOT) not in sys.path:
 
 GOLDEN = ROOT / "tests" / "golden"
 
+# Parity tests compare runs bit for bit (layouts, env switches, subprocesses):
+# compile generated stencils on first use so every call of a layer runs the
+# same kernel.  The default background mode has its own test
+# (test_gpu_engine.py::test_jit_async_first_call).
+os.environ.setdefault("SKC_JIT", "sync")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

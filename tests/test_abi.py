@@ -27,7 +27,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     nm = subprocess.run(["nm", "-D", "--defined-only", str(lib_path)], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (skc_\w+)", nm))
     assert set(declared_symbols()) <= exported
-    assert lib.skc_version() == 100
+    assert lib.skc_version() == 200
     assert lib.skc_max_taps() >= 128
 
 

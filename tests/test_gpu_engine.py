@@ -533,3 +533,75 @@ def test_sparse_stencil_path(skc, orc):
                         subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/t.npy", mode], check=True,
                                        env=dict(os.environ, **var), cwd=root)
                         assert normwise(ours, np.load(f"{td}/t.npy").astype(np.float64)) < tol, var
+
+
+def test_jit_async_first_call(skc, orc):
+    """Default (background) stencil compiles: the first call on a complex with
+    a new position pattern is served by the tap / dense kernels without
+    waiting for NVRTC, and every call -- before and after the generated kernel
+    is ready -- matches the oracle.  A second complex with the SAME positions
+    and new weights reuses the compiled kernel (weights are a launch
+    parameter)."""
+    import time
+    import torch
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    rng = np.random.default_rng(1234)
+    frames = torch.from_numpy(np.stack([synth.c1_frame(b)[:600] for b in range(2)])).cuda()
+    # a fresh pattern: disk taps jittered by a random sub-pixel shift
+    base = synth.c1_complex()
+    shift = rng.uniform(0.05, 0.45, size=2)
+    layers = tuple(skc.SparseLayer(l.offsets + shift, l.weights) for l in base.layers)
+    cpx = skc.KernelComplex(layers)
+    ref = orc.apply_complex(frames[0].cpu().numpy().astype(np.float64),
+                            [(l.offsets, l.weights) for l in cpx.layers], orc.ZERO)
+    try:
+        nat.set_jit_mode(False)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        first = skc.apply_complex_batch(frames, cpx)
+        torch.cuda.synchronize()
+        t_first = time.perf_counter() - t0
+        assert normwise(first[0].cpu().numpy(), ref) < TOL32
+        nat.jit_wait()
+        second = skc.apply_complex_batch(frames, cpx)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            second = skc.apply_complex_batch(frames, cpx)
+        torch.cuda.synchronize()
+        t_steady = (time.perf_counter() - t0) / 3
+        assert normwise(second[0].cpu().numpy(), ref) < TOL32
+        # no multi-second NVRTC stall on the first call (host overhead bound)
+        assert t_first < max(0.5, 20 * t_steady), (t_first, t_steady)
+        # new weights, same positions: no recompile needed -> the generated path at once
+        w2 = tuple(skc.SparseLayer(l.offsets, l.weights[::-1].copy()) for l in cpx.layers)
+        cpx2 = skc.KernelComplex(w2)
+        ref2 = orc.apply_complex(frames[0].cpu().numpy().astype(np.float64),
+                                 [(l.offsets, l.weights) for l in cpx2.layers], orc.ZERO)
+        assert normwise(skc.apply_complex_batch(frames, cpx2)[0].cpu().numpy(), ref2) < TOL32
+    finally:
+        nat.set_jit_mode(True)
+
+
+def test_pinned_host_batch_path(skc, orc):
+    """apply_complex_batch from pinned host memory (the e2e route): float32 and
+    float16 frames equal the device path; other dtypes or mismatched `out`
+    take the generic path instead of reinterpreting bytes."""
+    import torch
+    from paper_2512_04556_b200 import synth
+    cpx = synth.c0_complex()
+    rng = np.random.default_rng(3)
+    for dt in (torch.float32, torch.float16):
+        host = torch.from_numpy(rng.random((5, 64, 48, 3)).astype(np.float32)).to(dt).pin_memory()
+        out = torch.empty_like(host).pin_memory()
+        got = skc.apply_complex_batch(host, cpx, out=out, chunk=2)
+        assert got is out
+        dev = skc.apply_complex_batch(host.cuda(), cpx)
+        assert torch.equal(out, dev.cpu())
+    # bf16 / uint8 pinned frames: generic path, compared with the fp32 result
+    host = torch.from_numpy((rng.random((3, 40, 36, 3)) * 255).astype(np.uint8)).pin_memory()
+    out = torch.empty((3, 40, 36, 3), dtype=torch.float32).pin_memory()
+    skc.apply_complex_batch(host, cpx, out=out)
+    ref = skc.apply_complex_batch(host.to(torch.float32).cuda(), cpx).cpu()
+    assert torch.equal(out, ref)
