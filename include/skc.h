@@ -97,8 +97,11 @@ int skc_layer_fwd_ex(const void *in, int in_dtype, int in_layout, void *out, int
                      int out_layout, int B, int H, int W, int C,
                      const double *taps, int S, int boundary, void *stream);
 
-/* 1 when skc_chain_fwd runs this complex as one fused launch (small total
- * reach, <= 16 taps per layer: the config-3 Kawase fast path), else 0. */
+/* 1 when skc_chain_fwd runs this complex as one fused launch (in = out
+ * dtype, zero boundary), else 0: Kawase ladders (4 taps (+-r_l, +-r_l),
+ * r_l = l + 1/2, equal weights per layer, L <= 6) on fp16 RGBA with even W
+ * run the separable TMA-fed kernel of skc_kawase.cu (config 3); other small-
+ * reach chains the opt-in fused tile kernel (SKC_FUSED=1). */
 int skc_chain_is_fused(const double *taps, const int *layout, int L, int H, int W, int C,
                        int out_dtype);
 

@@ -18,12 +18,14 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libskc.so"
-SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_sparse.cu", "skc_fused.cu", "skc_fit.cu"]
+SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_sparse.cu", "skc_fused.cu", "skc_fit.cu",
+           "skc_kawase.cu"]
+GEN = OBJ / "skc_kawase_gen.inc"      # straight-line pass bodies (csrc/gen_kawase.py)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                "-I", str(ROOT / "include")]
+                "-I", str(ROOT / "include"), "-I", str(OBJ)]
 
 
 def _stale(target: Path, deps) -> bool:
@@ -37,13 +39,23 @@ def _headers():
     return [CSRC / "skc_common.cuh", CSRC / "skc_tile.cuh", ROOT / "include" / "skc.h"]
 
 
+def _generate(force: bool) -> None:
+    gen = CSRC / "gen_kawase.py"
+    if force or _stale(GEN, [gen]):
+        r = subprocess.run([sys.executable, str(gen), str(GEN)], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"gen_kawase.py failed\n{r.stdout}\n{r.stderr}")
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
+    _generate(force)
     jobs = []
     for src in SOURCES:
         s = CSRC / src
         o = OBJ / (s.stem + ".o")
-        if force or _stale(o, [s, *_headers()]):
+        deps = [s, *_headers()] + ([GEN] if src == "skc_kawase.cu" else [])
+        if force or _stale(o, deps):
             jobs.append([NVCC, *FLAGS, "-c", str(s), "-o", str(o)])
 
     def run(cmd):

@@ -360,6 +360,9 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
 extern "C" int skc_chain_is_fused(const double *taps, const int *layout, int L, int H, int W, int C,
                                   int out_dtype) {
     if (!taps || !layout || L < 1) return 0;
+    if (skc::kawase_chain(nullptr, out_dtype, nullptr, out_dtype, 1, H, W, C, taps, layout, L, SKC_ZERO, nullptr) ==
+        SKC_OK)
+        return 1;
     return skc::fused_chain(nullptr, SKC_F32, nullptr, out_dtype, 1, H, W, C, taps, layout, L, SKC_ZERO,
                             nullptr, true) == SKC_OK;
 }

@@ -1,0 +1,361 @@
+// skc_kawase.cu -- fused, separable Kawase chains (BASELINE config 3, SURVEY
+// §2.2 K3) in one persistent launch per call, TMA-fed.
+//
+// Reference: engine.apply_complex (engine.py:173-178) materialises every
+// layer; a layer is apply_sparse_layer (engine.py:160-170) -> sample_shifted
+// (118-130) -> _accum_shift (106-115) with zero padding.
+//
+// A Kawase layer has 4 taps (+-r, +-r) with r = b + 1/2 (b >= 0 integer) and
+// one weight w.  Each bilinear tap sits at fraction 1/2 on both axes, so the
+// layer is w/4 * (H4 (x) V4) with the unweighted 1-D sum
+//     H4 x(p) = x(p-b-1) + x(p-b) + x(p+b) + x(p+b+1),
+// and zero padding is a separable mask applied after every layer.  The whole
+// chain is therefore  prod_l(w_l/4) * [prod_l My V4_l] [prod_l Mx H4_l] in
+// (verified equal to the 2-D chain for zero padding).  Each 1-D
+// pass is a pair sum s(p) = x(p) + x(p-1) followed by y(p) = s(p) + s(p-2b-1):
+// two adds per output per layer per axis, the scale applied once at the end
+// (a power of two for w = 1/4, so exact).
+//
+// Kernel: persistent CTAs walk work items (frame, 128-column band, row
+// segment).  Per 32-row iteration:
+//   * one elected producer thread loads the band's rows with one 3-D TMA box
+//     (cp.async.bulk.tensor, 64-bit elements = one fp16 RGBA pixel) into a
+//     2-stage ring; out-of-image columns/rows arrive as zeros;
+//   * 2 H warps (lane = row x channel pair) stream their row along x through
+//     the L horizontal passes in registers (fully unrolled; intermediate
+//     columns outside the image are zeroed per layer in edge bands) and store
+//     128 fp32 channel-pair columns into a 2-stage H-result ring;
+//   * 8 V warps (lane = column x channel pair) stream down the rows with the
+//     vertical passes' delay lines carried in registers across iterations
+//     and across the whole segment (no vertical halo recompute), zero rows
+//     outside the image per layer at the top/bottom, scale, round to fp16
+//     once and store coalesced.
+// HBM traffic per pixel: 8 B in + 8 B out (the horizontal halo of 2 x reach
+// columns per 128 is re-read from L2); fp32 arithmetic throughout; one fp16
+// rounding of the output.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "skc_tile.cuh"
+
+namespace skc {
+namespace {
+
+constexpr int kKwTW = 128;        // output columns per band
+constexpr int kKwR = 32;          // rows per iteration
+constexpr int kKwNH = 2;          // H warps (16 rows each)
+constexpr int kKwNV = kKwTW / 16; // V warps (16 columns x 2 channel pairs each)
+constexpr int kKwThreads = 32 * (kKwNH + kKwNV + 1);  // + producer warp
+constexpr int kKwHP = kKwTW * 4 + 2;                  // H-result row pitch (words): 2 mod 32
+
+struct KwParams {
+    __half *out;
+    int B, H, W;
+    int bands, segs, seglen, items;
+    float scale;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    const unsigned a = smem_u32(bar);
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, unsigned long long *bar, int x, int y,
+                                            int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long ra, rb, rd;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+    return d;
+}
+
+__device__ __forceinline__ float2 h2f2(unsigned hv) {
+    return __half22float2(*reinterpret_cast<const __half2 *>(&hv));
+}
+
+// The pass bodies for the ladders b_l = l (generated: build/skc_kawase_gen.inc)
+#include "skc_kawase_gen.inc"
+
+struct Item {
+    int f, x0, y0, y1, iters;
+};
+
+template <int L>
+__device__ __forceinline__ Item item_of(const KwParams &p, int it) {
+    Item r;
+    const int seg = it % p.segs;
+    const int rest = it / p.segs;
+    const int band = rest % p.bands;
+    r.f = rest / p.bands;
+    r.x0 = band * kKwTW;
+    r.y0 = seg * p.seglen;
+    r.y1 = min(p.H, r.y0 + p.seglen);
+    r.iters = (r.y1 - r.y0 + 2 * KwGen<L>::kReach + kKwR - 1) / kKwR;
+    return r;
+}
+
+template <int L>
+__global__ void __launch_bounds__(kKwThreads, 1)
+    kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
+    using G = KwGen<L>;
+    constexpr int RX = G::kReach;
+    constexpr int IW = kKwTW + 2 * RX;
+    constexpr unsigned kStageBytes = (unsigned)kKwR * IW * 8;
+    extern __shared__ __align__(128) unsigned char smem[];
+    // stage s of the input ring at smem + s * kStageBytes, of the H-result
+    // ring at hres0 + s * kKwR * kKwHP (arithmetic, not a pointer array: an
+    // array indexed by s would live in local memory)
+    float *const hres0 = reinterpret_cast<float *>(smem + 2 * kStageBytes);
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + 2 * kStageBytes + 2 * kKwR * kKwHP * 4);
+    unsigned long long *full_in = bars, *empty_in = bars + 2, *full_h = bars + 4, *empty_h = bars + 6;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full_in[i], 1);
+            mbar_init(&empty_in[i], 32 * kKwNH);
+            mbar_init(&full_h[i], 32 * kKwNH);
+            mbar_init(&empty_h[i], 32 * kKwNV);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kKwNH + kKwNV) {
+        // ------------------------------------------------ TMA producer ---
+        if (lane == 0) {
+            unsigned g = 0;
+            for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+                const Item m = item_of<L>(p, it);
+                for (int i = 0; i < m.iters; ++i, ++g) {
+                    const int s = g & 1;
+                    if (g >= 2) mbar_wait(&empty_in[s], ((g >> 1) - 1) & 1);
+                    mbar_expect_tx(&full_in[s], kStageBytes);
+                    tma_load_3d(smem + s * kStageBytes, &tmap, &full_in[s], m.x0 - RX, m.y0 - RX + i * kKwR, m.f);
+                }
+            }
+        }
+        return;
+    }
+    if (warp < kKwNH) {
+        // ------------------------------------------ horizontal passes ---
+        const int r = warp * 16 + (lane & 15), pr = lane >> 4;
+        unsigned g = 0;
+        for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+            const Item m = item_of<L>(p, it);
+            const bool edge = m.x0 - RX < 0 || m.x0 + kKwTW + RX > p.W;
+            for (int i = 0; i < m.iters; ++i, ++g) {
+                const int s = g & 1;
+                mbar_wait(&full_in[s], (g >> 1) & 1);
+                if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1);
+                const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) + r * IW * 2 + pr;
+                float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + pr;
+                if (edge) G::template h<true>(row, orow, m.x0 - RX, p.W);
+                else G::template h<false>(row, orow, m.x0 - RX, p.W);
+                mbar_arrive(&empty_in[s]);
+                mbar_arrive(&full_h[s]);
+            }
+        }
+        return;
+    }
+    // ------------------------------------------------ vertical passes ---
+    const int vw = warp - kKwNH;
+    const int xl = vw * 16 + (lane >> 1), pr = lane & 1;
+    unsigned g = 0;
+    for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+        const Item m = item_of<L>(p, it);
+        typename G::State S;
+        G::zero(S);
+        const int x = m.x0 + xl;
+        __half *outp = p.out + (((long long)m.f * p.H) * p.W + x) * 4 + 2 * pr;
+        const float2 sc = make_float2(p.scale, p.scale);
+        for (int i = 0; i < m.iters; ++i, ++g) {
+            const int s = g & 1;
+            mbar_wait(&full_h[s], (g >> 1) & 1);
+            const float2 *col = reinterpret_cast<const float2 *>(hres0 + s * kKwR * kKwHP) + 2 * xl + pr;
+            const int yin0 = m.y0 - RX + i * kKwR;
+            // intermediate rows outside the image occur only near the top and
+            // bottom: those iterations zero them per layer
+            const bool mask = yin0 - RX < 0 || yin0 + kKwR - 1 >= p.H;
+            // a column past the image edge runs the stream (its lanes share the
+            // warp's barriers) but stores nothing
+            const int y1 = x < p.W ? m.y1 : m.y0;
+            if (mask) G::template v<true>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+            else G::template v<false>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+            mbar_arrive(&empty_h[s]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host ---
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        cudaGetLastError();
+        return (EncodeTiledFn)f;
+    }();
+    return fn;
+}
+
+int kawase_env() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_KAWASE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+// The chain as (L, b_l) when every layer is a Kawase quadruple (+-r, +-r),
+// r = b + 1/2, with equal weights; scale = prod_l w_l / 4.
+bool kawase_pattern(const double *taps, const int *layout, int L, int *b, double *scale) {
+    if (L < 1 || L > 8) return false;
+    double sc = 1.0;
+    const double *t = taps;
+    for (int l = 0; l < L; ++l, t += 3 * layout[l - 1]) {
+        if (layout[l] != 4) return false;
+        const double r = std::fabs(t[0]);
+        const double w = t[2];
+        const double bb = r - 0.5;
+        if (!(bb >= 0) || bb != std::floor(bb) || bb > 15) return false;
+        bool seen[4] = {false, false, false, false};
+        for (int i = 0; i < 4; ++i) {
+            const double ox = t[3 * i], oy = t[3 * i + 1];
+            if (t[3 * i + 2] != w || std::fabs(ox) != r || std::fabs(oy) != r) return false;
+            seen[(ox > 0 ? 1 : 0) | (oy > 0 ? 2 : 0)] = true;
+        }
+        if (!(seen[0] && seen[1] && seen[2] && seen[3])) return false;
+        b[l] = (int)bb;
+        sc *= w / 4.0;
+    }
+    *scale = sc;
+    return true;
+}
+
+template <int L>
+int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, cudaStream_t s) {
+    constexpr int RX = KwGen<L>::kReach;
+    constexpr int IW = kKwTW + 2 * RX;
+    static_assert(IW <= 256, "TMA box width");
+    const size_t smem = 2 * (size_t)kKwR * IW * 8 + 2 * (size_t)kKwR * kKwHP * 4 + 8 * sizeof(unsigned long long);
+    if (smem > (size_t)kMaxSmem) return -1;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return -1;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 8, (cuuint64_t)W * H * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)IW, (cuuint32_t)kKwR, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(in), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+    KwParams p;
+    p.out = static_cast<__half *>(out);
+    p.B = B;
+    p.H = H;
+    p.W = W;
+    p.bands = ceil_div(W, kKwTW);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // row segments: enough items to balance the persistent grid, each segment
+    // long against its 2 x reach warm-up rows
+    const long long cols = (long long)B * p.bands;
+    int segs = 1;
+    double best = 1e30;
+    for (int k = 1; k <= 64; ++k) {
+        const int len = ceil_div(H, k);
+        if (k > 1 && len < 8 * RX) break;
+        const long long items = cols * k;
+        const long long rounds = (items + nsm - 1) / nsm;
+        const double cost = (double)rounds * (len + 2 * RX + kKwR);
+        if (cost < best * 0.98) {
+            best = cost;
+            segs = k;
+        }
+    }
+    p.segs = segs;
+    p.seglen = ceil_div(H, segs);
+    p.items = (int)(cols * segs);
+    p.scale = scale;
+    auto kern = kawase_sep_kernel<L>;
+    if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;
+    const int grid = std::min(p.items, nsm);
+    kern<<<grid, kKwThreads, smem, s>>>(map, p);
+    SKC_LAUNCH_CHECK("kawase_sep_kernel");
+    return SKC_OK;
+}
+
+}  // namespace
+
+// Fused separable Kawase chain (see top of file) for fp16 RGBA, zero
+// boundary; -1 when the chain or the image does not qualify (the per-layer
+// path runs instead).
+int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C, const double *taps,
+                 const int *layout, int L, int boundary, cudaStream_t s) {
+    if (kawase_env() == 0) return -1;
+    if (C != 4 || idt != SKC_F16 || odt != SKC_F16 || boundary != SKC_ZERO || (W & 1)) return -1;
+    if (in && ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 7))) return -1;
+    int b[8];
+    double scale;
+    if (!kawase_pattern(taps, layout, L, b, &scale)) return -1;
+    for (int l = 0; l < L; ++l)
+        if (b[l] != l) return -1;  // instantiated: the standard Kawase ladder r_l = l + 1/2
+    if (!in) return encode_fn() ? SKC_OK : -1;  // plan query
+    switch (L) {
+        case 1: return launch_kawase<1>(in, out, B, H, W, (float)scale, s);
+        case 2: return launch_kawase<2>(in, out, B, H, W, (float)scale, s);
+        case 3: return launch_kawase<3>(in, out, B, H, W, (float)scale, s);
+        case 4: return launch_kawase<4>(in, out, B, H, W, (float)scale, s);
+        case 5: return launch_kawase<5>(in, out, B, H, W, (float)scale, s);
+        case 6: return launch_kawase<6>(in, out, B, H, W, (float)scale, s);
+        default: return -1;
+    }
+}
+
+}  // namespace skc

@@ -1513,6 +1513,9 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
     }
     if (!finite_taps(taps, (int)total)) return fail(SKC_EBADARG, "sparse layer parameters must be finite");
     cudaStream_t s = (cudaStream_t)stream;
+    // Kawase ladders on fp16 RGBA: one fused separable launch (skc_kawase.cu)
+    rc = kawase_chain(in, in_dtype, out, out_dtype, B, H, W, C, taps, layout, L, boundary, s);
+    if (rc != -1) return rc;
     if (L == 1) return last_layer(in, in_dtype, false, out, out_dtype, B, H, W, C, taps, layout[0], boundary, s);
     rc = fused_chain(in, in_dtype, out, out_dtype, B, H, W, C, taps, layout, L, boundary, s);
     if (rc != -1) return rc;

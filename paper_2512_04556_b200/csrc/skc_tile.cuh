@@ -123,6 +123,10 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc = false);
 bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out);
 bool sparse_head_allc(const double *taps, int S, int C, bool f32);
+// Fused separable Kawase chain (skc_kawase.cu): -1 when the chain or image
+// does not qualify; with in == nullptr a plan query (SKC_OK = would run).
+int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C, const double *taps,
+                 const int *layout, int L, int boundary, cudaStream_t s);
 
 // Argument checks shared by the image entry points (skc_layer.cu).
 int check_image_args(const void *in, int idt, const void *out, int odt, int B, int H, int W, int C,

@@ -16,6 +16,11 @@ GOLDEN = ROOT / "tests" / "golden"
 # same kernel.  The default background mode has its own test
 # (test_gpu_engine.py::test_jit_async_first_call).
 os.environ.setdefault("SKC_JIT", "sync")
+# share compiled stencils with the subprocess tests (the on-disk cache is
+# opt-in; a private 0700 directory per session)
+if "SKC_CACHE_DIR" not in os.environ:
+    import tempfile
+    os.environ["SKC_CACHE_DIR"] = tempfile.mkdtemp(prefix="skc_cache_")
 
 
 def pytest_configure(config):
