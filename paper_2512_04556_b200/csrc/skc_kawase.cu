@@ -55,6 +55,7 @@ struct KwParams {
     int B, H, W;
     int bands, segs, seglen, items;
     float scale;
+    int dbg;   // SKC_KAWASE_DBG bits (bring-up): 1 = no TMA, 2 = no H math, 4 = no V math
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -118,6 +119,20 @@ struct Item {
     int f, x0, y0, y1, iters;
 };
 
+// TMA box geometry.  The box's first column must sit on a 16-byte boundary
+// (an odd 8-byte pixel start faults), so the box starts one pixel early when
+// the reach is odd; its width is padded to 2 mod 4 pixels so the staged row
+// pitch spreads the H lanes' half2 reads over 16 banks (2-way at worst).
+template <int L>
+struct KwBox {
+    static constexpr int RX = KwGen<L>::kReach;
+    static constexpr int OFF = RX & 1;                       // leading pad pixels
+    static constexpr int IW = kKwTW + 2 * RX;                // pixels the passes read
+    static constexpr int IWB = ((IW + OFF + 1) / 4) * 4 + 2 >= IW + OFF ? ((IW + OFF + 1) / 4) * 4 + 2
+                                                                        : ((IW + OFF + 1) / 4) * 4 + 6;
+    static constexpr unsigned kStageBytes = (unsigned)kKwR * IWB * 8;
+};
+
 template <int L>
 __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
     Item r;
@@ -128,7 +143,8 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
     r.x0 = band * kKwTW;
     r.y0 = seg * p.seglen;
     r.y1 = min(p.H, r.y0 + p.seglen);
-    r.iters = (r.y1 - r.y0 + 2 * KwGen<L>::kReach + kKwR - 1) / kKwR;
+    // the vertical wavefront is skewed by one step per layer: L - 1 extra steps
+    r.iters = (r.y1 - r.y0 + 2 * KwGen<L>::kReach + (L - 1) + kKwR - 1) / kKwR;
     return r;
 }
 
@@ -137,8 +153,8 @@ __global__ void __launch_bounds__(kKwThreads, 1)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
     using G = KwGen<L>;
     constexpr int RX = G::kReach;
-    constexpr int IW = kKwTW + 2 * RX;
-    constexpr unsigned kStageBytes = (unsigned)kKwR * IW * 8;
+    using BX = KwBox<L>;
+    constexpr unsigned kStageBytes = BX::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     // stage s of the input ring at smem + s * kStageBytes, of the H-result
     // ring at hres0 + s * kKwR * kKwHP (arithmetic, not a pointer array: an
@@ -167,8 +183,12 @@ __global__ void __launch_bounds__(kKwThreads, 1)
                 for (int i = 0; i < m.iters; ++i, ++g) {
                     const int s = g & 1;
                     if (g >= 2) mbar_wait(&empty_in[s], ((g >> 1) - 1) & 1);
-                    mbar_expect_tx(&full_in[s], kStageBytes);
-                    tma_load_3d(smem + s * kStageBytes, &tmap, &full_in[s], m.x0 - RX, m.y0 - RX + i * kKwR, m.f);
+                    if (p.dbg & 1) {
+                        mbar_arrive(&full_in[s]);
+                    } else {
+                        mbar_expect_tx(&full_in[s], kStageBytes);
+                        tma_load_3d(smem + s * kStageBytes, &tmap, &full_in[s], m.x0 - RX - BX::OFF, m.y0 - RX + i * kKwR, m.f);
+                    }
                 }
             }
         }
@@ -185,9 +205,10 @@ __global__ void __launch_bounds__(kKwThreads, 1)
                 const int s = g & 1;
                 mbar_wait(&full_in[s], (g >> 1) & 1);
                 if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1);
-                const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) + r * IW * 2 + pr;
+                const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) + (r * BX::IWB + BX::OFF) * 2 + pr;
                 float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + pr;
-                if (edge) G::template h<true>(row, orow, m.x0 - RX, p.W);
+                if (p.dbg & 2) {
+                } else if (edge) G::template h<true>(row, orow, m.x0 - RX, p.W);
                 else G::template h<false>(row, orow, m.x0 - RX, p.W);
                 mbar_arrive(&empty_in[s]);
                 mbar_arrive(&full_h[s]);
@@ -213,11 +234,12 @@ __global__ void __launch_bounds__(kKwThreads, 1)
             const int yin0 = m.y0 - RX + i * kKwR;
             // intermediate rows outside the image occur only near the top and
             // bottom: those iterations zero them per layer
-            const bool mask = yin0 - RX < 0 || yin0 + kKwR - 1 >= p.H;
+            const bool mask = yin0 - RX - (L - 1) < 0 || yin0 + kKwR - 1 >= p.H;
             // a column past the image edge runs the stream (its lanes share the
             // warp's barriers) but stores nothing
             const int y1 = x < p.W ? m.y1 : m.y0;
-            if (mask) G::template v<true>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+            if (p.dbg & 4) {
+            } else if (mask) G::template v<true>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             else G::template v<false>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             mbar_arrive(&empty_h[s]);
         }
@@ -279,16 +301,16 @@ bool kawase_pattern(const double *taps, const int *layout, int L, int *b, double
 template <int L>
 int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, cudaStream_t s) {
     constexpr int RX = KwGen<L>::kReach;
-    constexpr int IW = kKwTW + 2 * RX;
-    static_assert(IW <= 256, "TMA box width");
-    const size_t smem = 2 * (size_t)kKwR * IW * 8 + 2 * (size_t)kKwR * kKwHP * 4 + 8 * sizeof(unsigned long long);
+    using BX = KwBox<L>;
+    static_assert(BX::IWB <= 256 && BX::IWB % 2 == 0 && BX::IWB >= BX::IW + BX::OFF, "TMA box width");
+    const size_t smem = 2 * (size_t)BX::kStageBytes + 2 * (size_t)kKwR * kKwHP * 4 + 8 * sizeof(unsigned long long);
     if (smem > (size_t)kMaxSmem) return -1;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return -1;
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     const cuuint64_t strides[2] = {(cuuint64_t)W * 8, (cuuint64_t)W * H * 8};
-    const cuuint32_t box[3] = {(cuuint32_t)IW, (cuuint32_t)kKwR, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)BX::IWB, (cuuint32_t)kKwR, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(in), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -323,6 +345,10 @@ int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, c
     p.seglen = ceil_div(H, segs);
     p.items = (int)(cols * segs);
     p.scale = scale;
+    {
+        const char *e = std::getenv("SKC_KAWASE_DBG");
+        p.dbg = e ? std::atoi(e) : 0;
+    }
     auto kern = kawase_sep_kernel<L>;
     if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;
     const int grid = std::min(p.items, nsm);
