@@ -376,57 +376,65 @@ class Chain:
 
 
 class Strips:
-    """c3big across N GPUs: one 16384^2 RGBA fp16 image in row strips; each step
-    exchanges the exact corner-reach halo (21 rows for Kawase 6x4)
-    with the neighbours over NCCL point-to-point, runs the chain on the
-    extended strip and keeps its own rows (paper_2512_04556_b200.dist)."""
+    """c3big across N GPUs: one 16384^2 RGBA fp16 image in row strips.  Each
+    rank's strip lives in a dist.StripPipeline: per step the exact
+    corner-reach halo (21 rows for Kawase 6x4) is exchanged with
+    the neighbours over NCCL point-to-point straight into the extended
+    buffer while the strip's interior rows are filtered, then the two border
+    bands are filtered (no concatenation, no whole-strip copy).
+    `shape` / `compute_into` / `device` overrides exist for the CPU gloo
+    test of this exact rank path (tests/test_dist.py)."""
 
-    def __init__(self, args, dev, rank, world):
+    def __init__(self, args, dev, rank, world, shape=None, compute_into=None, dtype=None):
         import torch
         from paper_2512_04556_b200 import synth
-        from paper_2512_04556_b200.dist import corner_reach, strip_bounds
-        self.h, self.w, self.c = synth.C3_BIG
+        from paper_2512_04556_b200.dist import StripPipeline, corner_reach, strip_bounds
+        self.h, self.w, self.c = shape or synth.C3_BIG
         self.cpx = synth.kawase_complex()
         self.rank, self.world = rank, world
-        full = synth.value_noise_frame_device(self.h, self.w, self.c, 100, dev, dtype=torch.float16)
+        dt = dtype or torch.float16
+        full = synth.value_noise_frame_device(self.h, self.w, self.c, 100, dev, dtype=dt)
         r0, r1 = strip_bounds(self.h, rank, world)
-        self.strip = full[r0:r1].contiguous()
+        self.rows = (r0, r1)
+        self.pipe = StripPipeline(r1 - r0, self.w, self.c, dt, dev, self.cpx, rank, world, "zero",
+                                  compute_into=compute_into)
+        self.pipe.strip.copy_(full[r0:r1])
         del full
-        torch.cuda.empty_cache()
+        if dev.type == "cuda":
+            torch.cuda.empty_cache()
         self.halo = corner_reach(self.cpx)[:2]
-        self.launches_per_step = 1
+        self.launches_per_step = 1                          # the pipeline step is timed as one unit
+        self.kernels_per_step = 1 + len(self.pipe._bands)   # interior + border bands
         self.units_per_step = self.h * self.w // world
         self.alg_bytes = [(r1 - r0) * self.w * self.c * 2 * 2]
         self.metric = "filtered Mpix/s (16384x16384 RGBA fp16, Kawase 6 layers x 4 taps, row strips)"
         self.dtype = "f16 storage, f32 accumulate"
         self.scaling = "strong"
-        self.storage = torch.float16
-        self.config = {"workload": f"c3big: one 16384x16384x4 fp16 image in {world} row strips, halo {self.halo} rows "
-                                   "exchanged over NCCL P2P each step", "l2": "inputs larger than L2, no flush"}
-        self.kernel = "layer kernels + NCCL halo exchange"
+        self.storage = dt
+        self.config = {"workload": f"c3big: one {self.h}x{self.w}x{self.c} fp16 image in {world} row strips, halo "
+                                   f"{self.halo} rows exchanged over NCCL P2P each step, overlapped with the "
+                                   "strip interior", "l2": "inputs larger than L2, no flush"}
+        self.kernel = "fused Kawase chain (interior + 2 border bands) + NCCL halo exchange"
 
     def pre_step(self):
         pass
 
     def step(self, stream, events=None):
-        from paper_2512_04556_b200.dist import apply_complex_strips
         if events is not None:
             events[0][0].record(stream)
-        self.out = apply_complex_strips(self.strip, self.cpx, self.rank, self.world, "zero")
+        self.out = self.pipe.step()
         if events is not None:
             events[0][1].record(stream)
 
     def e2e_setup(self):
-        self.host = self.strip.cpu().pin_memory()
+        self.host = self.pipe.strip.cpu().pin_memory()
+        self.host_out = torch_mod().empty_like(self.host).pin_memory()
         n = self.host.numel() * 2
         return n, n
 
     def e2e_step(self):
-        import torch
-        from paper_2512_04556_b200.dist import apply_complex_strips
-        dev_strip = self.host.to(self.strip.device, non_blocking=True)
-        out = apply_complex_strips(dev_strip, self.cpx, self.rank, self.world, "zero")
-        self.host.copy_(out, non_blocking=True)
+        self.pipe.strip.copy_(self.host, non_blocking=True)
+        self.host_out.copy_(self.pipe.step(), non_blocking=True)
 
     def cpu_sample(self, threads):
         wl = _cpu_only_workload("c3big", None)
@@ -742,7 +750,7 @@ def run_ours(args):
                          "per_launch_ms": per_launch,
                          "share_of_step": per_launch[dom] / (ms_max / args.steps),
                          "step_hbm_frac": sum(wl.alg_bytes) / (total_launch_ms / 1e3) / 1e9 / peak},
-            "gpu_launches": args.steps * nl,
+            "gpu_launches": args.steps * getattr(wl, "kernels_per_step", nl),
             "clocks": clk,
         }
         if getattr(wl, "smem_bytes", None) and wl.smem_bytes[dom] > 0:

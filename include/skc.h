@@ -42,6 +42,7 @@ extern "C" {
 /* storage dtypes (arithmetic is always fp32) */
 #define SKC_F32 0
 #define SKC_F16 1
+#define SKC_F64 2          /* skc_bilinear_sample images only              */
 
 /* boundary modes: ZERO = reference zero padding (engine.py:106-115);
  * CLAMP = clamp-to-edge (BASELINE config 0) */
@@ -209,6 +210,68 @@ int skc_ir_energies(const float *taps, int B, const int *layout, int L, int nmax
                     const float *tgt, int M, int loss_kind, float loss_eps, double *energies,
                     void *stream);
 
+/* Parallel simulated tempering configuration (baselines.PSTConfig,
+ * baselines.py:93-114).  t_max / t_min NaN = the reference defaults 1e-2 and
+ * 1e-6 times the start state's energy (baselines.py:195-198). */
+typedef struct skc_pst_cfg {
+    int chains;               /* PSTConfig.chains (2..1024)                   */
+    int iterations;           /* PSTConfig.iterations                         */
+    int swap_interval;        /* PSTConfig.swap_interval                      */
+    int sum_normalize;        /* PSTConfig.sum_normalize                      */
+    double t_max, t_min;      /* ladder ends, NaN = default                   */
+    double sigma_offset;      /* resolved PSTConfig.sigma_offset (px)         */
+    double sigma_weight;      /* PSTConfig.sigma_weight                       */
+    unsigned long long seed;  /* Philox key (PSTConfig.seed)                  */
+    int loss_kind;            /* SKC_LOSS_*                                   */
+    float loss_eps;           /* LossKind.epsilon                             */
+} skc_pst_cfg;
+/*
+ * A whole PST run on the device (baselines.pst_fit, baselines.py:143-254):
+ * per iteration Gaussian proposals for every chain, per-layer weight sum
+ * normalisation, every chain's energy (as skc_ir_energies), Metropolis
+ * acceptance at the chain's ladder temperature, best-state tracking and
+ * every swap_interval iterations the adjacent-pair swap sweep
+ * (baselines.py:132-140).  No host round trip per iteration: the loop is a
+ * replayed CUDA graph; the host syncs once for the start energy (the ladder)
+ * and once at the end.
+ *   start_taps : device float32 (L, nmax, 3) init complex, zero padded
+ *   tgt        : device float32 (M, M) target; canvas odd >= M
+ *   noise      : NULL = Philox(seed) draws; else device float64
+ *                (iterations, chains*L*nmax*3 + 2*chains - 1) standard
+ *                normals / uniforms in the reference's numpy draw order
+ *                (offset normals (chains,L,nmax,2), weight normals
+ *                (chains,L,nmax), acceptance uniforms (chains), swap
+ *                uniforms (chains-1)), so a seeded reference run replays
+ *   ladder_out : HOST float64 (chains) temperature ladder
+ *   trace      : device float64 (iterations, 2 + chains) rows
+ *                (iteration, best energy, chain energies)
+ *   best_taps  : HOST float64 (L, nmax, 3); best_energy HOST float64 (1)
+ *   accepts    : HOST int64 (chains) accepted proposals per ladder slot;
+ *   swaps      : HOST int64 (chains - 1) accepted exchanges per pair
+ */
+int skc_pst_run(const float *start_taps, const int *layout, int L, int nmax, int canvas, const float *tgt,
+                int M, const skc_pst_cfg *cfg, const double *noise, double *ladder_out, double *trace,
+                double *best_taps, double *best_energy, long long *accepts, long long *swaps, void *stream);
+/*
+ * Per-element bilinear lookup with zero padding (engine.bilinear_sample,
+ * engine.py:212-248).  img device (NB, H, W) SKC_F32 or SKC_F64; x, y device
+ * float64 (n,) coordinates; element e samples image bidx[e] (device int64,
+ * or NULL: e / inner, or image 0 when inner == 0); out device float64 (n,).
+ * Float64 weights and corner order (0,0), (0,1), (1,0), (1,1) as the
+ * reference, so float64 images reproduce its values.
+ */
+int skc_bilinear_sample(const void *img, int img_dtype, int NB, int H, int W, const double *x, const double *y,
+                        const long long *bidx, long long n, long long inner, double *out, void *stream);
+/*
+ * Spatially varying dense ground truth (svfilter.sv_ground_truth,
+ * svfilter.py:206-235): out[c, y, x] = sum_{u,v} img[c, u, v] *
+ * K_k[r + y - u, r + x - v], k = kidx[y, x], zero padding.
+ *   img / out : device float32 planar (C, H, W)
+ *   kidx      : device int32 (H, W) kernel index per pixel
+ *   kernels   : device float32 (K, M, M), M odd, each centred (zero padded)
+ */
+int skc_sv_ground_truth(const float *img, int H, int W, int C, const int *kidx, const float *kernels, int K,
+                        int M, float *out, void *stream);
 /* Fit configuration (optim.TrainConfig, ConstraintConfig, LossKind). */
 typedef struct skc_fit_cfg {
     int steps;            /* TrainConfig.steps                          */

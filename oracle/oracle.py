@@ -61,6 +61,7 @@ def lib():
         _lib = ctypes.CDLL(str(LIB_PATH))
         _lib.or_num_threads.restype = ctypes.c_int
         _lib.or_backward.restype = ctypes.c_int64
+        _lib.or_backward_g.restype = ctypes.c_int64
         _lib.or_fit.restype = ctypes.c_int
     return _lib
 
@@ -190,6 +191,27 @@ def backward(layers, tgt_embedded, kind="charbonnier", eps=1e-6):
         grads.append((d_off[base:base + n].copy(), d_w[base:base + n].copy()))
         base += n
     return float(value.value), grads
+
+
+def backward_with_grad(layers, g):
+    """_backward_pass (optim.py:231-263) driven by an explicit upstream
+    gradient g (canvas, canvas) -- e.g. the sign pattern an fp32 forward
+    produced -- instead of the loss gradient.  Returns the per-layer grads."""
+    off, wt, layout = _flat_taps(layers)
+    g = _f64(g)
+    canvas = g.shape[0]
+    d_off = np.zeros_like(off)
+    d_w = np.zeros_like(wt)
+    bad = ctypes.c_int64(-1)
+    rc = lib().or_backward_g(_d(off), _d(wt), _i(layout), ctypes.c_int64(layout.size), ctypes.c_int64(canvas),
+                             _d(g), _d(d_off), _d(d_w), ctypes.byref(bad))
+    if rc >= 0:
+        raise OracleError(f"non-finite intermediate at layer {rc}")
+    grads, base = [], 0
+    for n in layout:
+        grads.append((d_off[base:base + n].copy(), d_w[base:base + n].copy()))
+        base += n
+    return grads
 
 
 def _cfg(steps, lr_start, lr_end, beta1, beta2, eps, weight_norm, kws, loss_kind, loss_eps):

@@ -405,6 +405,26 @@ int64_t or_backward(const double *off, const double *w, const int64_t *layout, i
     return -1;
 }
 
+/* _backward_pass (optim.py:231-263) with a caller-given upstream gradient g
+ * (canvas^2) instead of the loss gradient: lets a test feed the sign pattern
+ * an fp32 implementation evaluated, so an L1 gradient comparison is not
+ * dominated by pixels where |IR - target| is below fp32 resolution.
+ * Returns -1 or the failing layer. */
+int64_t or_backward_g(const double *off, const double *w, const int64_t *layout, int64_t L,
+                      int64_t canvas, const double *g_in, double *d_off, double *d_w,
+                      int64_t *bad_sample) {
+    int64_t n = canvas * canvas;
+    double *inter = (double *)malloc(sizeof(double) * (size_t)n * (size_t)(L + 1));
+    int64_t bad = forward_ir(off, w, layout, L, canvas, inter, bad_sample);
+    if (bad >= 0) { free(inter); return bad; }
+    double *g = (double *)malloc(sizeof(double) * (size_t)n);
+    memcpy(g, g_in, sizeof(double) * (size_t)n);
+    backward_pass(off, w, layout, L, canvas, inter, g, d_off, d_w);
+    free(g);
+    free(inter);
+    return -1;
+}
+
 /* optim.py:312-325 _project_kws */
 static int project_kws(double *off, double *wp, const int64_t *layout, int64_t L) {
     static const double SX[4] = {1.0, -1.0, -1.0, 1.0};

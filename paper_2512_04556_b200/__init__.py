@@ -17,6 +17,7 @@ from .engine import (
     apply_complex_batch,
     apply_sparse_layer,
     auto_canvas,
+    bilinear_sample,
     dense_convolve,
     psnr,
     required_canvas,
@@ -27,12 +28,19 @@ from .engine import (
 from .kernels import (
     DenseKernel,
     KernelError,
+    KernelSpec,
     delta_kernel,
     disk_kernel,
     gaussian_kernel,
+    generate_kernel,
+    heart_kernel,
+    load_kernel_image,
     polygon_kernel,
+    read_image,
     ring_kernel,
+    save_kernel_image,
     star_kernel,
+    write_image,
 )
 from .optim import (
     AdamState,
@@ -60,15 +68,18 @@ from .initializers import (
     ss_init,
     support_rejection_sample,
 )
+from .baselines import PSTConfig, PSTResult, pst_fit
 from .svfilter import (
     FilterBasis,
     FilterBasisGrid,
     build_basis,
+    build_basis_grid,
     interp_weights,
     load_basis,
     save_basis,
     sv_filter,
     sv_filter_grid,
+    sv_ground_truth,
     synthesize_filter,
 )
 

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libskc.so"
 SOURCES = ["skc_api.cu", "skc_filter.cu", "skc_layer.cu", "skc_sparse.cu", "skc_fused.cu", "skc_fit.cu",
-           "skc_kawase.cu"]
+           "skc_kawase.cu", "skc_pst.cu", "skc_gather.cu"]
 GEN = OBJ / "skc_kawase_gen.inc"      # straight-line pass bodies (csrc/gen_kawase.py)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

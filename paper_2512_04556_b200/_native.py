@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libskc.so"
 
 SKC_OK, SKC_EBADARG, SKC_ENONFINITE, SKC_ETRUNC, SKC_ECUDA, SKC_EDEGENERATE = 0, 1, 2, 3, 4, 5
-SKC_F32, SKC_F16 = 0, 1
+SKC_F32, SKC_F16, SKC_F64 = 0, 1, 2
 SKC_ZERO, SKC_CLAMP = 0, 1
 SKC_HWC, SKC_CHW = 0, 1
 LOSS_IDS = {"charbonnier": 0, "l1": 1, "l2": 2}
@@ -31,7 +31,7 @@ EXPORTS = (
     "skc_version", "skc_last_error", "skc_release_scratch", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check", "skc_set_jit_mode", "skc_jit_wait",
     "skc_chain_fwd",
     "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
-    "skc_adam_step",
+    "skc_adam_step", "skc_pst_run", "skc_bilinear_sample", "skc_sv_ground_truth",
 )
 
 
@@ -55,6 +55,22 @@ class FitCfg(ctypes.Structure):
         ("eps", ctypes.c_float),
         ("weight_norm", ctypes.c_int),
         ("kws", ctypes.c_int),
+        ("loss_kind", ctypes.c_int),
+        ("loss_eps", ctypes.c_float),
+    ]
+
+
+class PstCfg(ctypes.Structure):
+    _fields_ = [
+        ("chains", ctypes.c_int),
+        ("iterations", ctypes.c_int),
+        ("swap_interval", ctypes.c_int),
+        ("sum_normalize", ctypes.c_int),
+        ("t_max", ctypes.c_double),
+        ("t_min", ctypes.c_double),
+        ("sigma_offset", ctypes.c_double),
+        ("sigma_weight", ctypes.c_double),
+        ("seed", ctypes.c_ulonglong),
         ("loss_kind", ctypes.c_int),
         ("loss_eps", ctypes.c_float),
     ]
@@ -96,6 +112,11 @@ def _declare(lib):
                                 _vp]
     lib.skc_adam_step.argtypes = [_vp, _vp, _vp, _vp, _ip, _i, _i, ctypes.POINTER(FitCfg),
                                   ctypes.c_float, _vp, _vp]
+    lib.skc_pst_run.argtypes = [_vp, _ip, _i, _i, _i, _vp, _i, ctypes.POINTER(PstCfg), _vp, _dp, _vp, _dp,
+                                _dp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _vp]
+    lib.skc_bilinear_sample.argtypes = [_vp, _i, _i, _i, _i, _vp, _vp, _vp, ctypes.c_longlong, ctypes.c_longlong,
+                                        _vp, _vp]
+    lib.skc_sv_ground_truth.argtypes = [_vp, _i, _i, _i, _vp, _vp, _i, _i, _vp, _vp]
     for name in EXPORTS[2:]:
         getattr(lib, name).restype = _i
 

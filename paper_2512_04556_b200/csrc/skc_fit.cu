@@ -947,6 +947,57 @@ static bool cfg_ok(const skc_fit_cfg *c) {
            (c->loss_kind >= 0 && c->loss_kind <= 2) && c->loss_eps > 0;
 }
 
+
+// ------------------------------------------------- PST energy evaluation ---
+// skc_pst.cu replays the MODE_ENERGY launch once per tempering iteration on
+// fixed device buffers (proposal taps in, chain energies out), so its
+// parameter block is built once and the launch is CUDA-graph capturable.
+struct EnergyPlan {
+    FitParams p;
+};
+
+int energy_plan_create(EnergyPlan **out, int B, const int *layout, int L, int nmax, int canvas,
+                       const float *tgt, int M, int loss_kind, float loss_eps, const float *taps,
+                       double *energies, cudaStream_t s) {
+    *out = nullptr;
+    EnergyPlan *e = new EnergyPlan();
+    FitParams &p = e->p;
+    int rc = fill_params(p, B, layout, L, nmax, M);
+    if (!rc && (canvas < M || (canvas & 1) == 0 || (M & 1) == 0))
+        rc = fail(SKC_EBADARG, "canvas/target must be odd, canvas >= M");
+    if (!rc && (loss_kind < 0 || loss_kind > 2 || !(loss_eps > 0))) rc = fail(SKC_EBADARG, "bad loss kind");
+    if (rc) { delete e; return rc; }
+    p.mode = MODE_ENERGY;
+    p.canvas_fixed = canvas;
+    p.taps_in = taps;
+    p.tgts = tgt;
+    p.tgt_shared = 1;
+    p.energy_out = energies;
+    p.cfg.steps = 1;
+    p.cfg.loss_kind = loss_kind;
+    p.cfg.loss_eps = loss_eps;
+    void *st = nullptr;
+    if ((rc = pool_alloc(&st, (size_t)B * 4 * sizeof(int), s))) { delete e; return rc; }
+    p.status = (int *)st;
+    if ((rc = alloc_scratch(p, canvas, s))) { pool_free(st, s); delete e; return rc; }
+    if ((rc = set_fit_attrs())) { pool_free(p.scratch, s); pool_free(st, s); delete e; return rc; }
+    *out = e;
+    return SKC_OK;
+}
+
+int energy_plan_launch(const EnergyPlan *e, cudaStream_t s) {
+    fit_kernel<<<e->p.B, kFitThreads, kFitSmem, s>>>(e->p);
+    SKC_LAUNCH_CHECK("fit_kernel (energies)");
+    return SKC_OK;
+}
+
+void energy_plan_destroy(EnergyPlan *e, cudaStream_t s) {
+    if (!e) return;
+    pool_free(e->p.scratch, s);
+    pool_free(e->p.status, s);
+    delete e;
+}
+
 }  // namespace skc
 
 using namespace skc;

@@ -27,6 +27,7 @@ __all__ = [
     "apply_complex",
     "apply_complex_batch",
     "dense_convolve",
+    "bilinear_sample",
     "synthesize_ir",
     "synthesize_ir_batch",
     "required_canvas",
@@ -169,6 +170,37 @@ def _chain(im: Image, cpx: KernelComplex, boundary: str, out_dtype=None):
     return out
 
 
+def chain_into(src, dst, cpx: KernelComplex, boundary: str = "zero", stream=None):
+    """skc_chain_fwd from one contiguous CUDA tensor into another (H, W[, C])
+    or (B, H, W, C), fp32 or fp16, no allocation of the output: the building
+    block of the overlapped strip pipeline (dist.StripPipeline)."""
+    t = torch()
+    lib = nat.lib()
+    for name, ten in (("src", src), ("dst", dst)):
+        if not (isinstance(ten, t.Tensor) and ten.is_cuda and ten.is_contiguous()
+                and ten.dtype in (t.float32, t.float16)):
+            raise EngineError(f"chain_into: {name} must be a contiguous fp32/fp16 CUDA tensor")
+    if src.shape != dst.shape:
+        raise EngineError(f"chain_into: shapes differ {tuple(src.shape)} vs {tuple(dst.shape)}")
+    shp = tuple(src.shape)
+    if len(shp) == 2:
+        b, h, w, c = 1, shp[0], shp[1], 1
+    elif len(shp) == 3:
+        b, (h, w, c) = 1, shp
+    elif len(shp) == 4:
+        b, h, w, c = shp
+    else:
+        raise EngineError(f"chain_into: bad shape {shp}")
+    dt = {t.float32: nat.SKC_F32, t.float16: nat.SKC_F16}
+    taps = cpx.taps()
+    layout = np.ascontiguousarray(cpx.layout, dtype=np.int32)
+    rc = lib.skc_chain_fwd(nat.ptr(src), dt[src.dtype], nat.ptr(dst), dt[dst.dtype], b, h, w, c, nat.dbl(taps),
+                           nat.ints(layout), layout.size, _boundary(boundary), nat.stream_ptr(stream))
+    if rc:
+        _raise(rc, "chain_into")
+    return dst
+
+
 def apply_complex(img, cpx: KernelComplex, boundary: str = "zero"):
     """All layers in order (engine.py:173-178); intermediates stay fp32 on device."""
     im = Image(img)
@@ -271,6 +303,64 @@ def dense_convolve(img, kernel: DenseKernel, boundary: str = "zero"):
         return im.restore(im.empty_like().zero_())
     off = np.stack([-(ii - r), -(jj - r)], axis=1).astype(np.float64)
     return apply_sparse_layer(img, SparseLayer(off, w[jj, ii]), boundary)
+
+
+def bilinear_sample(img, x, y):
+    """Bilinear lookup at per-element fractional coordinates, zero padding
+    (engine.py:212-248).  img (..., H, W); x, y (..., A, B) broadcast
+    together and share img's leading batch dims (every batch slice samples
+    its own image).  One device gather (skc_bilinear_sample) in float64
+    coordinates and weights, the reference's corner order; float64 images
+    stay float64, so numpy inputs give the reference's values.  numpy in ->
+    float64 numpy out; CUDA tensors in -> float64 CUDA tensor out."""
+    t = torch()
+    lib = nat.lib()
+    on_dev = isinstance(img, t.Tensor) and img.is_cuda
+    dev = img.device if on_dev else t.device("cuda", t.cuda.current_device())
+
+    def dev_tensor(a, dtype):
+        if isinstance(a, t.Tensor):
+            return a.to(device=dev, dtype=dtype)
+        return t.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to(dev).to(dtype)
+
+    im = dev_tensor(img, t.float32 if isinstance(img, t.Tensor) and img.dtype in (t.float16, t.float32)
+                    else t.float64)
+    if im.dim() < 2:
+        raise EngineError(f"image must have at least 2 dims, got {tuple(im.shape)}")
+    h, w = int(im.shape[-2]), int(im.shape[-1])
+    batch = tuple(int(v) for v in im.shape[:-2])
+    xs, ys = dev_tensor(x, t.float64), dev_tensor(y, t.float64)
+    try:
+        shape = tuple(np.broadcast_shapes(tuple(xs.shape), tuple(ys.shape)))
+    except ValueError as exc:
+        raise EngineError(f"x and y do not broadcast: {exc}") from exc
+    xs = xs.expand(shape).contiguous()
+    ys = ys.expand(shape).contiguous()
+    nb = int(np.prod(batch)) if batch else 1
+    bidx, inner = None, 0
+    if batch:
+        if shape[:len(batch)] == batch:
+            inner = int(np.prod(shape[len(batch):])) if len(shape) > len(batch) else 1
+        else:
+            # general numpy broadcasting of the batch index (engine.py:234-237)
+            b = np.arange(nb).reshape(batch + (1,) * (len(shape) - len(batch)))
+            try:
+                bb = np.broadcast_to(b, np.broadcast_shapes(b.shape, shape))
+            except ValueError as exc:
+                raise EngineError(f"batch dims {batch} do not broadcast with {shape}: {exc}") from exc
+            shape = bb.shape
+            xs = xs.expand(shape).contiguous()
+            ys = ys.expand(shape).contiguous()
+            bidx = t.from_numpy(np.ascontiguousarray(bb, dtype=np.int64)).to(dev)
+    im = im.contiguous()
+    out = t.empty(shape, dtype=t.float64, device=dev)
+    n = int(out.numel())
+    rc = lib.skc_bilinear_sample(nat.ptr(im), nat.SKC_F32 if im.dtype == t.float32 else nat.SKC_F64, nb, h, w,
+                                 nat.ptr(xs), nat.ptr(ys), nat.ptr(bidx) if bidx is not None else None,
+                                 n, inner, nat.ptr(out), nat.stream_ptr())
+    if rc:
+        _raise(rc, "bilinear_sample")
+    return out if on_dev else out.cpu().numpy()
 
 
 def required_canvas(cpx: KernelComplex) -> int:

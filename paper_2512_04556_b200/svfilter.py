@@ -22,6 +22,13 @@ from .engine import BOUNDARIES, EngineError, KernelComplex, SparseLayer
 
 __all__ = [
     "FilterBasis",
+    "FilterBasisGrid",
+    "build_basis",
+    "build_basis_grid",
+    "sv_filter_grid",
+    "sv_ground_truth",
+    "save_basis",
+    "load_basis",
     "interp_weights",
     "synthesize_filter",
     "sv_filter",
@@ -210,35 +217,132 @@ def sv_filter_grid(img, grid: FilterBasisGrid, pmap2, boundary: str = "zero"):
     return im.restore(res)
 
 
-def build_basis(target_family, params, layout, cfg=None, constraints=None, init=None, loss_kind=None,
-                warm_start: bool = True) -> FilterBasis:
-    """Fit one complex per grid parameter (svfilter.py:81-113); adjacent entries
-    warm-start from the previous solution (slot correspondence).  Each fit runs
-    on device; the chain of warm starts is inherently sequential."""
+def _as_dense(tgt):
+    from .kernels import DenseKernel, generate_kernel
+    return tgt if isinstance(tgt, DenseKernel) else generate_kernel(tgt)
+
+
+def _fit_round(jobs, layout, cfg, constraints, loss_kind):
+    """Fit independent (target, init) jobs with one persistent batched launch
+    per distinct target size (fit_batch); returns the complexes in order."""
+    from .optim import fit_batch
+    out = [None] * len(jobs)
+    by_size = {}
+    for j, (tgt, _) in enumerate(jobs):
+        by_size.setdefault(tgt.size, []).append(j)
+    for idx in by_size.values():
+        res = fit_batch([jobs[j][0] for j in idx], layout, [jobs[j][1] for j in idx], cfg, constraints,
+                        loss_kind)
+        for j, r in zip(idx, res):
+            out[j] = r.complex
+    return out
+
+
+def _basis_rows(families, params, layout, cfg, constraints, inits, loss_kind, warm_start):
+    """Fit len(families) bases over the same parameter grid at once.
+
+    Row i's entry k starts from row i's entry k-1 when warm_start holds and
+    the two parameters are one grid step apart (svfilter.py:100-107), else
+    from replace(inits[i], seed=inits[i].seed + k).  Rows never depend on
+    each other, so entry k of every row is one batched fit: the warm-start
+    chain is sequential along the grid only."""
     from dataclasses import replace
-    from .initializers import InitStrategy
-    from .kernels import DenseKernel
-    from .optim import ConstraintConfig, LossKind, TrainConfig, fit, parse_layout
-    cfg = TrainConfig() if cfg is None else cfg
-    constraints = ConstraintConfig() if constraints is None else constraints
-    init = InitStrategy("ss-ir") if init is None else init
-    loss_kind = LossKind() if loss_kind is None else loss_kind
-    layout = parse_layout(layout)
     ps = np.array(sorted(params), dtype=np.float64)
     if ps.size > 1 and not (np.diff(ps) > 0).all():
         raise EngineError("basis parameters must be strictly increasing")
     step = float(np.min(np.diff(ps))) if ps.size > 1 else 0.0
-    filters, prev = [], None
+    rows = [[] for _ in families]
     for k, p in enumerate(ps):
-        tgt = target_family(p)
-        if not isinstance(tgt, DenseKernel):
-            raise EngineError("target_family must return DenseKernel targets")
         adjacent = k > 0 and abs(float(ps[k] - ps[k - 1])) <= step * (1 + 1e-9)
-        start = prev if (warm_start and prev is not None and adjacent) else replace(init, seed=init.seed + k)
-        res = fit(tgt, layout, start, cfg, constraints, loss_kind)
-        filters.append(res.complex)
-        prev = res.complex
-    return FilterBasis(ps, tuple(filters))
+        jobs = []
+        for i, fam in enumerate(families):
+            start = rows[i][-1] if (warm_start and adjacent) else replace(inits[i], seed=inits[i].seed + k)
+            jobs.append((_as_dense(fam(p)), start))
+        for i, cpx in enumerate(_fit_round(jobs, layout, cfg, constraints, loss_kind)):
+            rows[i].append(cpx)
+    return ps, rows
+
+
+def _fit_defaults(cfg, constraints, init, loss_kind):
+    from .initializers import InitStrategy
+    from .optim import ConstraintConfig, LossKind, TrainConfig
+    return (TrainConfig() if cfg is None else cfg, ConstraintConfig() if constraints is None else constraints,
+            InitStrategy("ss-ir") if init is None else init, LossKind() if loss_kind is None else loss_kind)
+
+
+def build_basis(target_family, params, layout, cfg=None, constraints=None, init=None, loss_kind=None,
+                warm_start: bool = True) -> FilterBasis:
+    """Fit one complex per grid parameter (svfilter.py:81-113).  target_family
+    maps a parameter to a DenseKernel or a KernelSpec.  Adjacent entries
+    warm-start from the previous solution (slot correspondence); without warm
+    starts every entry is fit in one batched launch."""
+    from .optim import parse_layout
+    cfg, constraints, init, loss_kind = _fit_defaults(cfg, constraints, init, loss_kind)
+    ps, rows = _basis_rows([target_family], params, parse_layout(layout), cfg, constraints, [init], loss_kind,
+                           warm_start)
+    return FilterBasis(ps, tuple(rows[0]))
+
+
+def build_basis_grid(target_family, params_u, params_v, layout, cfg=None, constraints=None, init=None,
+                     loss_kind=None, warm_start: bool = True) -> FilterBasisGrid:
+    """Fit a (u, v) grid of basis complexes (svfilter.py:272-289): every row is
+    build_basis along v of target_family(u, .), row iu starting from
+    replace(init, seed=init.seed + 1000 * iu) when warm_start, else from init.
+    The rows are independent, so each v step fits all rows in one launch."""
+    from dataclasses import replace
+    from .optim import parse_layout
+    cfg, constraints, init, loss_kind = _fit_defaults(cfg, constraints, init, loss_kind)
+    pu = np.array(sorted(params_u), dtype=np.float64)
+    inits = [replace(init, seed=init.seed + 1000 * iu) if (warm_start and iu > 0) else init
+             for iu in range(pu.size)]
+    fams = [(lambda v, u=float(u): target_family(u, v)) for u in pu]
+    pv, rows = _basis_rows(fams, params_v, parse_layout(layout), cfg, constraints, inits, loss_kind, warm_start)
+    return FilterBasisGrid(pu, pv, tuple(tuple(r) for r in rows))
+
+
+def sv_ground_truth(img, target_family, pmap, *, levels: int | None = None, max_kernels: int = 8192):
+    """Brute-force SV reference (svfilter.py:206-235): at every pixel the dense
+    kernel target_family(pmap[y, x]) (DenseKernel or KernelSpec) applied as a
+    zero-padded convolution.  The family is evaluated once per DISTINCT map
+    value on the host and the per-pixel convolutions run on the device
+    (skc_sv_ground_truth).  A continuous map has one value per pixel: pass
+    `levels=N` to snap it to N evenly spaced values between its min and max
+    first (an approximation the reference does not make)."""
+    t = torch()
+    lib = nat.lib()
+    a = np.asarray(img, dtype=np.float64)
+    pm = np.asarray(pmap, dtype=np.float64)
+    if a.ndim not in (2, 3):
+        raise EngineError(f"image must be (H, W) or (H, W, C), got {a.shape}")
+    if pm.shape != a.shape[:2]:
+        raise EngineError(f"parameter map {pm.shape} must match image {a.shape[:2]}")
+    if levels is not None:
+        if levels < 2:
+            raise EngineError(f"levels must be >= 2, got {levels}")
+        lo, hi = float(pm.min()), float(pm.max())
+        if hi > lo:
+            pm = lo + np.rint((pm - lo) / (hi - lo) * (levels - 1)) * ((hi - lo) / (levels - 1))
+    vals, inv = np.unique(pm, return_inverse=True)
+    if vals.size > max_kernels:
+        raise EngineError(f"parameter map has {vals.size} distinct values (> max_kernels={max_kernels}); "
+                          "pass levels=N to quantise it")
+    ks = [_as_dense(target_family(float(v))).weights for v in vals]
+    m = max(k.shape[0] for k in ks)
+    bank = np.stack([np.pad(k, (m - k.shape[0]) // 2) for k in ks]).astype(np.float32)
+    chans = a if a.ndim == 3 else a[:, :, None]
+    h, w, c = chans.shape
+    dev = t.device("cuda", t.cuda.current_device())
+    d_img = t.from_numpy(np.ascontiguousarray(np.moveaxis(chans, 2, 0), dtype=np.float32)).to(dev)
+    d_idx = t.from_numpy(np.ascontiguousarray(inv.reshape(h, w), dtype=np.int32)).to(dev)
+    d_k = t.from_numpy(bank).to(dev)
+    d_out = t.empty_like(d_img)
+    rc = lib.skc_sv_ground_truth(nat.ptr(d_img), h, w, c, nat.ptr(d_idx), nat.ptr(d_k), len(ks), m,
+                                 nat.ptr(d_out), nat.stream_ptr())
+    if rc == nat.SKC_EBADARG:
+        raise EngineError(f"sv_ground_truth: {nat.last_error()}")
+    nat.check(rc, "sv_ground_truth")
+    res = np.moveaxis(d_out.cpu().numpy().astype(np.float64), 0, 2)
+    return res if a.ndim == 3 else res[:, :, 0]
 
 
 def save_basis(basis, path) -> None:

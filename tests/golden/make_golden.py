@@ -351,7 +351,97 @@ def gen_next():
                         dc21=sk.dense_convolve(imgc, k21))
 
 
+def gen_round2():
+    """Round-2 rows: bilinear_sample, sv_ground_truth, KernelSpec / netpbm
+    formats, build_basis(_grid) with KernelSpec targets, a longer PST trace."""
+    import io
+    import tempfile
+    from dataclasses import replace  # noqa: F401
+    from sparsekern import baselines, kernels
+    rng = np.random.default_rng(2001)
+    cases = {}
+    # bilinear_sample (engine.py:212-248): plain, batched, broadcast, general batch broadcast
+    img = rng.uniform(size=(9, 11))
+    x = rng.uniform(-2, 13, (5, 7))
+    y = rng.uniform(-2, 11, (5, 7))
+    x[0, 0], y[0, 0] = 3.0, 4.0          # integer read
+    cases.update(bs0_img=img, bs0_x=x, bs0_y=y, bs0_out=engine.bilinear_sample(img, x, y))
+    imgb = rng.uniform(size=(3, 6, 8))
+    xb = rng.uniform(-1, 9, (3, 4, 5))
+    yb = rng.uniform(-1, 7, (3, 4, 5))
+    cases.update(bs1_img=imgb, bs1_x=xb, bs1_y=yb, bs1_out=engine.bilinear_sample(imgb, xb, yb))
+    xr = rng.uniform(-1, 9, (4, 5))
+    yr = rng.uniform(-1, 7, (1, 5))
+    cases.update(bs2_img=img, bs2_x=xr, bs2_y=yr, bs2_out=engine.bilinear_sample(img, xr, yr))
+    imgc = rng.uniform(size=(2, 3, 6, 8))
+    xc = rng.uniform(-1, 9, (2, 3, 4))
+    yc = rng.uniform(-1, 7, (2, 3, 4))
+    cases.update(bs3_img=imgc, bs3_x=xc, bs3_y=yc, bs3_out=engine.bilinear_sample(imgc, xc, yc))
+    # sv_ground_truth (svfilter.py:206-235) with a KernelSpec family and 3 map levels
+    gimg = f32(rng.uniform(size=(26, 21, 2)))
+    pm = np.choose(rng.integers(0, 3, (26, 21)), [0.0, 0.5, 1.0])
+    fam = lambda p: sk.KernelSpec("disk", (1.5 + 3.0 * p,))   # noqa: E731
+    cases.update(gt_img=gimg, gt_pmap=pm, gt_out=svfilter.sv_ground_truth(gimg, fam, pm))
+    pm2 = np.choose(rng.integers(0, 2, (26, 21)), [0.2, 0.7])
+    fam2 = lambda p: sk.gaussian_kernel(0.5 + 2.0 * p)        # noqa: E731
+    cases.update(gt2_pmap=pm2, gt2_out=svfilter.sv_ground_truth(gimg[:, :, 0], fam2, pm2))
+    # KernelSpec parse + generate_kernel
+    specs = ["gaussian:1.5", "gaussian:1.2:11", "disk:4.5", "disk:3:11", "ring:2:5", "ring:2:5:15",
+             "polygon:5:6", "polygon:6:7:19:30", "star:4:8", "star:5:8:21:15", "heart:7", "heart:6:17",
+             "delta", "delta:5"]
+    cases["spec_texts"] = np.array(specs)
+    for j, t in enumerate(specs):
+        sp = sk.KernelSpec.parse(t)
+        cases[f"spec{j}_repr"] = np.array(repr(sp))
+        cases[f"spec{j}_k"] = sk.generate_kernel(sp).weights
+    # netpbm bytes
+    with tempfile.TemporaryDirectory() as d:
+        k = sk.disk_kernel(3.3)
+        kernels.save_kernel_image(k, f"{d}/k.pgm")
+        cases["pgm_kernel_bytes"] = np.frombuffer(open(f"{d}/k.pgm", "rb").read(), np.uint8)
+        cases["pgm_kernel_loaded"] = kernels.load_kernel_image(f"{d}/k.pgm").weights
+        im2 = rng.uniform(-0.1, 1.1, (5, 7))
+        im3 = rng.uniform(0, 1, (4, 6, 3))
+        kernels.write_image(im2, f"{d}/a.pgm")
+        kernels.write_image(im3, f"{d}/b.ppm", maxval=255)
+        cases.update(img2=im2, img3=im3,
+                     pgm_img2_bytes=np.frombuffer(open(f"{d}/a.pgm", "rb").read(), np.uint8),
+                     ppm_img3_bytes=np.frombuffer(open(f"{d}/b.ppm", "rb").read(), np.uint8),
+                     img2_read=kernels.read_image(f"{d}/a.pgm"), img3_read=kernels.read_image(f"{d}/b.ppm"))
+        with open(f"{d}/c.pgm", "w") as fh:
+            fh.write("P2\n# a comment\n3 2\n# another\n10\n0 1 2\n3 4 10\n")
+        cases["ascii_read"] = kernels.read_image(f"{d}/c.pgm")
+    # basis building with KernelSpec targets (short fits: trajectories stay within fp32 noise)
+    cfg = sk.TrainConfig(steps=6)
+    lk = sk.LossKind("l1")
+    b1 = svfilter.build_basis(lambda p: sk.KernelSpec("disk", (2.0 + 2.0 * p,), size=11), [0.0, 0.5, 1.0],
+                              (4, 4), cfg=cfg, init=sk.InitStrategy("ss", seed=3), loss_kind=lk)
+    cases["bb_stack"] = stacked(b1)
+    b2 = svfilter.build_basis(lambda p: sk.KernelSpec("disk", (2.0 + 2.0 * p,), size=11), [0.0, 0.25, 1.0],
+                              (4, 4), cfg=cfg, init=sk.InitStrategy("ss", seed=3), loss_kind=lk,
+                              warm_start=False)
+    cases["bb_nows_stack"] = stacked(b2)
+    g = svfilter.build_basis_grid(lambda u, v: sk.KernelSpec("disk", (2.0 + u + 1.5 * v,), size=11),
+                                  [0.0, 1.0], [0.0, 0.5, 1.0], (4, 4), cfg=cfg,
+                                  init=sk.InitStrategy("ss", seed=5), loss_kind=lk)
+    cases["bbg_stack"] = np.stack([np.stack([stacked(g.row_basis(iu))[iv] for iv in range(3)]) for iu in range(2)])
+    # a longer seeded PST trace (numpy proposal stream) + best energies over seeds
+    tgt = sk.DenseKernel(f32(sk.disk_kernel(4.0, 13).weights))
+    res = baselines.pst_fit(tgt, (4, 4), baselines.PSTConfig(chains=5, iterations=300, seed=7),
+                            sk.InitStrategy("ss", seed=2), sk.LossKind("l1"))
+    cases.update(pst_tgt=tgt.weights, pst_trace=res.trace, pst_ladder=res.ladder, pst_best=np.float64(res.best_energy),
+                 pst_best_stack=stacked(sk.FilterBasis([0.0], (res.complex,))))
+    bests = []
+    for sd in range(12):
+        r = baselines.pst_fit(tgt, (4, 4), baselines.PSTConfig(chains=4, iterations=400, seed=100 + sd),
+                              sk.InitStrategy("ss", seed=2), sk.LossKind("l1"))
+        bests.append(r.best_energy)
+    cases["pst_seed_bests"] = np.array(bests)
+    np.savez_compressed(OUT / "round2.npz", **cases)
+
+
 if __name__ == "__main__":
+    gen_round2()
     gen_next()
     gen_pst()
     gen_init()

@@ -144,3 +144,59 @@ def test_initializers_bit_exact_vs_reference(golden):
         assert np.array_equal(w, g[f"n{k}_w"]), k
     off, r = support_rejection_sample(skc.ring_kernel(5.0, 9.0, 23), 12, seed=5, return_radius=True)
     assert np.array_equal(off, g["srs_off"]) and r == float(g["srs_r"])
+
+
+def test_kernelspec_parse_and_generate_vs_reference(golden):
+    """KernelSpec.parse / generate_kernel (kernels.py:105-171), bit-exact."""
+    g = golden("round2")
+    for j, text in enumerate(g["spec_texts"].tolist()):
+        sp = skc.KernelSpec.parse(text)
+        assert repr(sp) == str(g[f"spec{j}_repr"]), text
+        assert np.array_equal(skc.generate_kernel(sp).weights, g[f"spec{j}_k"]), text
+    for bad in ("blob:3", "gaussian", "ring:3", "file", "polygon:x:3"):
+        with pytest.raises(skc.KernelError):
+            skc.generate_kernel(skc.KernelSpec.parse(bad))
+
+
+def test_netpbm_bytes_match_reference(golden, tmp_path):
+    """PGM/PPM writers and readers (kernels.py:314-435): identical bytes."""
+    g = golden("round2")
+    skc.save_kernel_image(skc.disk_kernel(3.3), tmp_path / "k.pgm")
+    assert (tmp_path / "k.pgm").read_bytes() == g["pgm_kernel_bytes"].tobytes()
+    assert np.array_equal(skc.load_kernel_image(tmp_path / "k.pgm").weights, g["pgm_kernel_loaded"])
+    skc.write_image(g["img2"], tmp_path / "a.pgm")
+    skc.write_image(g["img3"], tmp_path / "b.ppm", maxval=255)
+    assert (tmp_path / "a.pgm").read_bytes() == g["pgm_img2_bytes"].tobytes()
+    assert (tmp_path / "b.ppm").read_bytes() == g["ppm_img3_bytes"].tobytes()
+    assert np.array_equal(skc.read_image(tmp_path / "a.pgm"), g["img2_read"])
+    assert np.array_equal(skc.read_image(tmp_path / "b.ppm"), g["img3_read"])
+    (tmp_path / "c.pgm").write_text("P2\n# a comment\n3 2\n# another\n10\n0 1 2\n3 4 10\n")
+    assert np.array_equal(skc.read_image(tmp_path / "c.pgm"), g["ascii_read"])
+    spec = skc.KernelSpec.parse(f"file:{tmp_path / 'k.pgm'}")
+    assert np.array_equal(skc.generate_kernel(spec).weights, g["pgm_kernel_loaded"])
+    (tmp_path / "bad.pgm").write_bytes(b"P7\n1 1\n255\n\x00")
+    with pytest.raises(skc.KernelError):
+        skc.read_image(tmp_path / "bad.pgm")
+    (tmp_path / "trunc.pgm").write_bytes(b"P5\n4 4\n255\n\x00\x01")
+    with pytest.raises(skc.KernelError):
+        skc.read_image(tmp_path / "trunc.pgm")
+
+
+def test_pst_config_validation_and_exports():
+    """PSTConfig (baselines.py:93-114) and the top-level PST names (__init__.py:64-71)."""
+    assert skc.PSTConfig().chains == 10 and skc.PSTConfig().iterations == 10000
+    for kw in ({"chains": 1}, {"iterations": 0}, {"swap_interval": 0}, {"t_max": 1e-3, "t_min": 1e-2}):
+        with pytest.raises(skc.KernelError):
+            skc.PSTConfig(**kw)
+    from paper_2512_04556_b200 import baselines
+    assert skc.pst_fit is baselines.pst_fit and skc.PSTResult is baselines.PSTResult
+    draws = baselines._numpy_draws(skc.PSTConfig(chains=3, iterations=4, swap_interval=2, seed=9), 2, 5)
+    rng = np.random.default_rng(9)
+    for it in range(4):   # the reference's draw order, one record per iteration
+        assert np.array_equal(draws[it, :60], 1.0 * rng.normal(0.0, 1.0, size=60))
+        assert np.array_equal(draws[it, 60:90], rng.normal(0.0, 1.0, size=30))
+        assert np.array_equal(draws[it, 90:93], rng.uniform(size=3))
+        if (it + 1) % 2 == 0:
+            assert np.array_equal(draws[it, 93:], [rng.uniform(), rng.uniform()])
+        else:
+            assert not draws[it, 93:].any()
