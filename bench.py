@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--fit-targets", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the other configs' sub-lines (c1 only)")
     return ap.parse_args()
 
 
@@ -664,35 +665,69 @@ def _cpu_only_workload(config, a):
     return wl
 
 
-def run_ours(args):
+FP32_NOMINAL_TFLOPS = 2 * 148 * 128 * 1.965e9 / 1e12   # FMA = 2 flops; an add takes an FMA slot
+
+
+def binding_roofline(wl, per_launch, step_ms, hbm_peak):
+    """The resource that binds this workload's dominant kernel (VERDICT r1:
+    FP32 pipe for the unfused chains and the fit, shared memory for SV by
+    SURVEY 8(d)'s fetch count, HBM for the fused Kawase chain), with its
+    algorithmic work per launch / the event-timed launch duration."""
+    dom = int(np.argmax(per_launch))
+    t = per_launch[dom] / 1e3
+    if isinstance(wl, Chain) and wl.fused:
+        px = wl.nf * wl.h * wl.w
+        b = px * wl.c * 2 * (2 if wl.storage == torch_mod().float16 else 4)
+        ops = px * wl.c * (4 * len(wl.taps) + 1)        # 2 adds per layer per axis + the scale
+        return {"resource": "hbm", "achieved": b / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": b / t / 1e9 / hbm_peak, "kernel": wl.kernel,
+                "definition": "compulsory image bytes in + out (fused chain) / kernel time",
+                "fp32_pipe_frac": ops / t / 1e12 / (FP32_NOMINAL_TFLOPS / 2),
+                "fp32_note": f"{4 * len(wl.taps) + 1} fp32 add/mul per channel-pixel (separable passes), "
+                             "each one FMA-pipe slot, vs nominal"}
+    if isinstance(wl, Chain):
+        fma = sum(wl.launch_fma)
+        tot = sum(per_launch) / 1e3
+        return {"resource": "fp32_pipe", "achieved": 2 * wl.launch_fma[dom] / t / 1e12,
+                "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": 2 * wl.launch_fma[dom] / t / 1e12 / FP32_NOMINAL_TFLOPS,
+                "kernel": wl.smem_kind[dom], "chain_frac": 2 * fma / tot / 1e12 / FP32_NOMINAL_TFLOPS,
+                "definition": "issued FMAs of the launch (merged bilinear corners x channels) x 2 / kernel time, "
+                              "vs nominal 148 SMs x 128 lanes x 2 x 1.965 GHz; chain_frac = whole step"}
+    pk = smem_peak_gbps()
+    if isinstance(wl, SV):
+        b = wl.h * wl.w * 4 * int(np.max(wl.basis.layout)) * wl.c * 4
+        return {"resource": "smem", "achieved": b / t / 1e9, "peak": pk, "unit": "GB/s", "frac": b / t / 1e9 / pk,
+                "kernel": wl.kernel, "definition": "SURVEY 8(d): pixels x 4 bilinear fetches x taps x C x 4 B "
+                                                   "(one pass) / kernel time, vs measured LDS.128 bandwidth"}
+    if isinstance(wl, Fit):
+        b = len(wl.targets) * wl.cfg.steps * 1408 * 4 * 129 * 129
+        return {"resource": "smem", "achieved": b / t / 1e9, "peak": pk, "unit": "GB/s", "frac": b / t / 1e9 / pk,
+                "kernel": wl.kernel, "definition": "SURVEY 8(d): 1408 fetches x 4 B x 129^2 per kernel-iteration "
+                                                   "(forward + gradient corners + adjoint) / kernel time"}
+    return None
+
+
+def measure(wl, args, steps, warmup, rank, world, dev, cpu_budget_s, with_e2e=True):
+    """Warm up, time exactly `steps` steps (events on the launching stream,
+    barrier + synchronize on both sides, max over ranks) and build the line."""
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    from paper_2512_04556_b200 import _native as nat
-    nat.lib()
-    wl = make_workload(args, dev, rank, world)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         wl.pre_step()
         wl.step(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local) if rank == 0 else None
+    clocks = ClockSampler(dev.index) if rank == 0 else None
     if clocks:
         clocks.start()
     nl = wl.launches_per_step
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
-          for _ in range(args.steps)]
-    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)] for _ in range(steps)]
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     torch.cuda.synchronize()
-    for k in range(args.steps):
+    for k in range(steps):
         wl.pre_step()                  # L2 flush (if inputs fit L2) outside the timed step
         sev[k][0].record(stream)
         wl.step(stream, ev[k])
@@ -700,23 +735,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
     ms = sum(a.elapsed_time(b) for a, b in sev)
-    launch_ms = [[ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps)] for l in range(nl)]
+    launch_ms = [[ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(steps)] for l in range(nl)]
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     scale = 1e6 if getattr(wl, "unit", "Mpix/s") == "Mpix/s" else 1.0
-    value = world * wl.units_per_step * args.steps / (ms_max / 1e3) / scale
+    value = world * wl.units_per_step * steps / (ms_max / 1e3) / scale
 
     e2e = None
-    if not args.no_e2e:
+    if with_e2e:
         bi, bo = wl.e2e_setup()
         wl.e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(1, min(args.steps, 3))
+        ke = max(1, min(steps, 3))
         e0.record(stream)
         for _ in range(ke):
             wl.e2e_step()
@@ -728,84 +763,118 @@ def run_ours(args):
         e2e = {"value": world * wl.units_per_step / (float(ems.item()) / 1e3) / scale,
                "unit": getattr(wl, "unit", "Mpix/s"), "h2d_bytes_per_step": int(bi),
                "d2h_bytes_per_step": int(bo), "ms_per_step": float(ems.item()), "steps": ke}
+    if rank != 0:
+        return None
+    peak, peak_kind = measured_peaks()
+    per_launch = [sum(v) / len(v) for v in launch_ms]
+    dom = int(np.argmax(per_launch))
+    achieved = wl.alg_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
+    total_launch_ms = sum(per_launch)
+    line = {
+        "metric": wl.metric, "value": value, "unit": getattr(wl, "unit", "Mpix/s"), "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": ms_max / steps,
+        "higher_is_better": True, "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
+        "dtype": wl.dtype, "data": DATA,
+        "config": dict(wl.config, parallelism=(f"row strips x{world} (NCCL halo exchange)"
+                                                if isinstance(wl, Strips) else
+                                                f"dp{world} (independent units sharded, no collective)")),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
+                     "kernel": wl.kernel, "launch_index": dom, "launch_ms": per_launch[dom],
+                     "alg_bytes_per_launch": wl.alg_bytes[dom],
+                     "per_launch_ms": per_launch,
+                     "share_of_step": per_launch[dom] / (ms_max / steps),
+                     "step_hbm_frac": sum(wl.alg_bytes) / (total_launch_ms / 1e3) / 1e9 / peak},
+        "gpu_launches": steps * getattr(wl, "kernels_per_step", nl),
+        "clocks": clk,
+    }
+    bind = binding_roofline(wl, per_launch, ms_max / steps, peak)
+    if bind:
+        line["roofline"]["binding"] = bind
+    if getattr(wl, "smem_bytes", None) and wl.smem_bytes[dom] > 0:
+        pk = smem_peaks()
+        peak_s = pk["lds64_GBps"] if "tap" in wl.smem_kind[dom] else pk["lds32_GBps"]
+        ach = wl.smem_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
+        line["roofline"]["smem"] = {
+            "kernel": wl.smem_kind[dom], "bytes_per_launch": wl.smem_bytes[dom], "achieved_GBps": ach,
+            "peak_GBps": peak_s, "frac": ach / peak_s,
+            "peak_kind": "measured (profiles/smem_peak.json, tools/smem_peak.cu)"}
+    if isinstance(wl, Chain):
+        esz = 2 if wl.storage == torch.float16 else 4
+        smem_bytes = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * esz * wl.units_per_step
+        hbm_bytes = wl.units_per_step * wl.c * 2 * esz          # compulsory image in + out
+        smem_peak = smem_peak_gbps()
+        t_roof = max(hbm_bytes / (peak * 1e9), smem_bytes / (smem_peak * 1e9))
+        step_s = ms_max / steps / 1e3
+        line["north_star_roofline"] = {
+            "definition": "max(compulsory image bytes / HBM BW, taps x 4 bilinear fetches x C x storage bytes / "
+                          "SMEM BW) (BASELINE.json north_star, SURVEY 8(d))",
+            "binding": "smem" if smem_bytes / smem_peak > hbm_bytes / peak else "hbm",
+            "hbm_bytes_per_step": hbm_bytes, "smem_fetch_bytes_per_step": smem_bytes,
+            "hbm_peak_GBps": peak, "smem_peak_GBps": smem_peak,
+            "roofline_value": world * wl.units_per_step / t_roof / 1e6, "unit": "Mpix/s",
+            "frac": t_roof / step_s,
+            "hbm_only_frac": hbm_bytes / (peak * 1e9) / step_s,
+            "note": "register blocking, merged corners and the separable Kawase form fetch fewer bytes than "
+                    "the definition counts, so frac can exceed 1; roofline.binding is the resource that binds"}
+    if e2e:
+        line["e2e"] = e2e
+    if cpu_budget_s > 0 and world == 1:
+        # a bounded sample of host work: repeat the workload's sample until
+        # the budget is used, report the median rate
+        t_start, vals, samples = time.perf_counter(), [], []
+        while True:
+            v, cores, sample = wl.cpu_sample(os.cpu_count())
+            vals.append(v)
+            samples.append(sample)
+            if time.perf_counter() - t_start >= cpu_budget_s:
+                break
+        line["cpu_baseline"] = {"value": statistics.median(vals), "unit": getattr(wl, "unit", "Mpix/s"),
+                                "cores": cores, "kind": "port",
+                                "sample": f"{len(vals)} x [{samples[0]}] in {time.perf_counter() - t_start:.1f}s, median"}
+    return line
 
+
+OTHER_CONFIGS = ("c0", "c2", "c3", "c3big", "c4")
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2512_04556_b200 import _native as nat
+    nat.lib()
+    # generated stencils compile on first use on this thread (not in the
+    # background): the warm-up steps already run the kernels the timed steps
+    # run, and no compiler thread is live under a profiler
+    nat.set_jit_mode(True)
+    wl = make_workload(args, dev, rank, world)
+    line = measure(wl, args, args.steps, args.warmup, rank, world, dev, 0 if args.no_cpu else 10.0,
+                   with_e2e=not args.no_e2e)
+    if world == 1 and args.config == "c1" and not args.no_others:
+        # SURVEY 8(d)'s other configurations, measured in the same run (fewer
+        # steps) so each carries driver-run evidence
+        del wl
+        torch.cuda.empty_cache()
+        others = {}
+        for c in OTHER_CONFIGS:
+            sub = argparse.Namespace(**vars(args))
+            sub.config = c
+            w2 = make_workload(sub, dev, rank, world)
+            l2 = measure(w2, sub, min(args.steps, 5), args.warmup, rank, world, dev, 0 if args.no_cpu else 4.0,
+                         with_e2e=not args.no_e2e)
+            for k in ("higher_is_better", "vs_baseline", "data", "n_gpus", "scaling"):
+                l2.pop(k, None)
+            others[c] = l2
+            del w2
+            torch.cuda.empty_cache()
+        line["other_configs"] = others
     if rank == 0:
-        peak, peak_kind = measured_peaks()
-        per_launch = [sum(v) / len(v) for v in launch_ms]
-        dom = int(np.argmax(per_launch))
-        achieved = wl.alg_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
-        total_launch_ms = sum(per_launch)
-        line = {
-            "metric": wl.metric, "value": value, "unit": getattr(wl, "unit", "Mpix/s"), "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
-            "dtype": wl.dtype, "data": DATA,
-            "config": dict(wl.config, parallelism=(f"row strips x{world} (NCCL halo exchange)"
-                                                    if isinstance(wl, Strips) else
-                                                    f"dp{world} (independent units sharded, no collective)")),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
-                         "kernel": wl.kernel, "launch_index": dom, "launch_ms": per_launch[dom],
-                         "alg_bytes_per_launch": wl.alg_bytes[dom],
-                         "per_launch_ms": per_launch,
-                         "share_of_step": per_launch[dom] / (ms_max / args.steps),
-                         "step_hbm_frac": sum(wl.alg_bytes) / (total_launch_ms / 1e3) / 1e9 / peak},
-            "gpu_launches": args.steps * getattr(wl, "kernels_per_step", nl),
-            "clocks": clk,
-        }
-        if getattr(wl, "smem_bytes", None) and wl.smem_bytes[dom] > 0:
-            pk = smem_peaks()
-            peak_s = pk["lds64_GBps"] if "tap" in wl.smem_kind[dom] else pk["lds32_GBps"]
-            ach = wl.smem_bytes[dom] / (per_launch[dom] / 1e3) / 1e9
-            line["roofline"]["smem"] = {
-                "kernel": wl.smem_kind[dom], "bytes_per_launch": wl.smem_bytes[dom], "achieved_GBps": ach,
-                "peak_GBps": peak_s, "frac": ach / peak_s,
-                "peak_kind": "measured (profiles/smem_peak.json, tools/smem_peak.cu)",
-                "note": "the dominant launch is bound by shared-memory load bandwidth, not HBM: algorithmic "
-                        "shared-memory bytes of its register-blocked windows / its event-timed duration"}
-        if getattr(wl, "launch_fma", None) and wl.launch_fma[dom] > 0:
-            # issued FMAs of the dominant launch (its kernel's own arithmetic) / its time
-            fpk = 2 * 148 * 128 * 1.965e9 / 1e12
-            ach_f = 2 * wl.launch_fma[dom] / (per_launch[dom] / 1e3) / 1e12
-            line["roofline"]["fp32_pipe"] = {
-                "kernel": wl.smem_kind[dom], "fma_per_launch": wl.launch_fma[dom], "achieved_tflops": ach_f,
-                "nominal_peak_tflops": fpk, "frac": ach_f / fpk}
-        if isinstance(wl, Chain) and not getattr(wl, "fused", False):
-            fma = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * wl.units_per_step
-            line["roofline"]["fp32_fma"] = {
-                "alg_tflops_4_per_tap": 2 * fma / (total_launch_ms / 1e3) / 1e12,
-                "nominal_peak_tflops": 2 * 148 * 128 * 1.965e9 / 1e12}
-            esz = 2 if wl.storage == torch.float16 else 4
-            smem_bytes = sum(4 * l.sample_count for l in wl.cpx.layers) * wl.c * 4 * wl.units_per_step
-            hbm_bytes = wl.units_per_step * wl.c * 2 * esz          # compulsory image in + out
-            smem_peak = smem_peak_gbps()
-            t_roof = max(hbm_bytes / (peak * 1e9), smem_bytes / (smem_peak * 1e9))
-            step_s = ms_max / args.steps / 1e3
-            line["north_star_roofline"] = {
-                "definition": "max(compulsory image bytes / HBM BW, taps x 4 bilinear fetches x C x 4 B / SMEM BW) "
-                              "(BASELINE.json north_star)",
-                "binding": "smem" if smem_bytes / smem_peak > hbm_bytes / peak else "hbm",
-                "hbm_bytes_per_step": hbm_bytes, "smem_fetch_bytes_per_step": smem_bytes,
-                "hbm_peak_GBps": peak, "smem_peak_GBps": smem_peak,
-                "roofline_value": world * wl.units_per_step / t_roof / 1e6, "unit": "Mpix/s",
-                "frac": t_roof / step_s,
-                "note": "register blocking (0.34 words/FMA) and dense-stencil merging fetch fewer bytes than "
-                        "the definition counts, so frac can exceed 1"}
-        if e2e:
-            line["e2e"] = e2e
-        if not args.no_cpu and world == 1:
-            # a bounded sample of ~10 s of host work: repeat the workload's
-            # sample until the budget is used, report the aggregate rate
-            t_start, vals, samples = time.perf_counter(), [], []
-            while True:
-                v, cores, sample = wl.cpu_sample(os.cpu_count())
-                vals.append(v)
-                samples.append(sample)
-                if time.perf_counter() - t_start >= 10.0:
-                    break
-            line["cpu_baseline"] = {"value": statistics.median(vals), "unit": getattr(wl, "unit", "Mpix/s"),
-                                    "cores": cores, "kind": "port",
-                                    "sample": f"{len(vals)} x [{samples[0]}] in {time.perf_counter() - t_start:.1f}s, median"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -182,3 +182,30 @@ def test_fit_canvas_matches_reference(skc, golden):
         n = min(10, res.losses.size)
         rel = np.abs(res.losses[:n] - g[f"f{j}_trace"][:n, 1]) / np.abs(g[f"f{j}_trace"][:n, 1])
         assert rel.max() < TOL32, (j, rel)
+
+
+def test_c4_d5_batch_statistic(skc, golden):
+    """SURVEY D5(iii) at full scale: all 256 config-4 targets x 3000 steps (the
+    bench's workload) -- mean and median final loss within 1% of the float64
+    oracle's (tests/golden/d5_c4_fit.npz, tools/make_d5.py).  Individual fits
+    are chaotic (a 1e-7 relative perturbation of the inits moves single final
+    losses by several percent); the fixture's perturbed oracle run
+    measures that spread, and the GPU's distance from the oracle is held to it."""
+    import pathlib
+    if not (pathlib.Path(__file__).parent / "golden" / "d5_c4_fit.npz").exists():
+        pytest.skip("d5 fixture not generated")
+    g = golden("d5_c4_fit")
+    n, steps = int(g["targets"]), int(g["steps"])
+    tg, inits = _c4_batch(skc, n)
+    res = skc.fit_batch(tg, (32,) * 4, inits, skc.TrainConfig(steps=steps), skc.ConstraintConfig("sum"),
+                        skc.LossKind("l1"))
+    final = np.array([r.losses[-1] for r in res])
+    ref, pert = g["exact_final"], g["perturbed_final"]
+    assert abs(final.mean() / ref.mean() - 1) < 0.01, (final.mean(), ref.mean())
+    assert abs(np.median(final) / np.median(ref) - 1) < 0.01, (np.median(final), np.median(ref))
+    # per-kernel distance to the oracle is of the order of the oracle's own
+    # perturbation spread (chaos), not a systematic bias
+    spread = np.median(np.abs(pert / ref - 1))
+    ours = np.median(np.abs(final / ref - 1))
+    assert ours < 3 * spread + 1e-3, (ours, spread)
+    assert np.array_equal(np.array([r.canvas for r in res]) >= 129, np.ones(n, bool))
