@@ -45,9 +45,12 @@ namespace {
 
 constexpr int kKwTW = 128;        // output columns per band
 constexpr int kKwR = 32;          // rows per iteration
-constexpr int kKwNH = 2;          // H warps (16 rows each)
 constexpr int kKwNV = kKwTW / 16; // V warps (16 columns x 2 channel pairs each)
-constexpr int kKwThreads = 32 * (kKwNH + kKwNV + 1);  // + producer warp
+// H warps: 2 per row segment (16 rows x 2 channel pairs each); HS = 1 runs
+// the band's whole row per lane, HS = 2 splits it into two 64-column halves
+// (each with its own 2 x reach halo) over twice the lanes
+template <int HS> __host__ __device__ constexpr int kw_nh() { return 2 * HS; }
+template <int HS> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS>() + kKwNV + 1); }  // + producer warp
 constexpr int kKwHP = kKwTW * 4 + 2;                  // H-result row pitch (words): 2 mod 32
 
 struct KwParams {
@@ -148,9 +151,11 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
     return r;
 }
 
-template <int L>
-__global__ void __launch_bounds__(kKwThreads, 1)
+// one CTA per SM: the register budget is the whole file / the CTA's threads
+template <int L, int HS>
+__global__ void __maxnreg__(HS == 1 ? 168 : 152)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
+    constexpr int kKwNH = kw_nh<HS>();
     using G = KwGen<L>;
     constexpr int RX = G::kReach;
     using BX = KwBox<L>;
@@ -196,20 +201,29 @@ __global__ void __launch_bounds__(kKwThreads, 1)
     }
     if (warp < kKwNH) {
         // ------------------------------------------ horizontal passes ---
-        const int r = warp * 16 + (lane & 15), pr = lane >> 4;
+        constexpr int SW = kKwTW / HS;            // output columns per lane
+        const int seg = warp >> 1;
+        const int r = (warp & 1) * 16 + (lane & 15), pr = lane >> 4;
         unsigned g = 0;
         for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
             const Item m = item_of<L>(p, it);
-            const bool edge = m.x0 - RX < 0 || m.x0 + kKwTW + RX > p.W;
+            const int xs = m.x0 + seg * SW;
+            const bool edge = xs - RX < 0 || xs + SW + RX > p.W;
             for (int i = 0; i < m.iters; ++i, ++g) {
                 const int s = g & 1;
                 mbar_wait(&full_in[s], (g >> 1) & 1);
                 if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1);
-                const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) + (r * BX::IWB + BX::OFF) * 2 + pr;
-                float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + pr;
+                const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) +
+                                      (r * BX::IWB + BX::OFF + seg * SW) * 2 + pr;
+                float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + seg * SW * 2 + pr;
                 if (p.dbg & 2) {
-                } else if (edge) G::template h<true>(row, orow, m.x0 - RX, p.W);
-                else G::template h<false>(row, orow, m.x0 - RX, p.W);
+                } else if (HS == 1) {
+                    if (edge) G::template h<true>(row, orow, xs - RX, p.W);
+                    else G::template h<false>(row, orow, xs - RX, p.W);
+                } else {
+                    if (edge) G::template h_half<true>(row, orow, xs - RX, p.W);
+                    else G::template h_half<false>(row, orow, xs - RX, p.W);
+                }
                 mbar_arrive(&empty_in[s]);
                 mbar_arrive(&full_h[s]);
             }
@@ -298,7 +312,15 @@ bool kawase_pattern(const double *taps, const int *layout, int L, int *b, double
     return true;
 }
 
-template <int L>
+int kawase_hs() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_KAWASE_HS");
+        return (e && std::atoi(e) == 1) ? 1 : 2;
+    }();
+    return v;
+}
+
+template <int L, int HS>
 int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, cudaStream_t s) {
     constexpr int RX = KwGen<L>::kReach;
     using BX = KwBox<L>;
@@ -349,10 +371,10 @@ int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, c
         const char *e = std::getenv("SKC_KAWASE_DBG");
         p.dbg = e ? std::atoi(e) : 0;
     }
-    auto kern = kawase_sep_kernel<L>;
+    auto kern = kawase_sep_kernel<L, HS>;
     if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;
     const int grid = std::min(p.items, nsm);
-    kern<<<grid, kKwThreads, smem, s>>>(map, p);
+    kern<<<grid, kw_threads<HS>(), smem, s>>>(map, p);
     SKC_LAUNCH_CHECK("kawase_sep_kernel");
     return SKC_OK;
 }
@@ -373,13 +395,14 @@ int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int 
     for (int l = 0; l < L; ++l)
         if (b[l] != l) return -1;  // instantiated: the standard Kawase ladder r_l = l + 1/2
     if (!in) return encode_fn() ? SKC_OK : -1;  // plan query
+    const bool two = kawase_hs() == 2;
     switch (L) {
-        case 1: return launch_kawase<1>(in, out, B, H, W, (float)scale, s);
-        case 2: return launch_kawase<2>(in, out, B, H, W, (float)scale, s);
-        case 3: return launch_kawase<3>(in, out, B, H, W, (float)scale, s);
-        case 4: return launch_kawase<4>(in, out, B, H, W, (float)scale, s);
-        case 5: return launch_kawase<5>(in, out, B, H, W, (float)scale, s);
-        case 6: return launch_kawase<6>(in, out, B, H, W, (float)scale, s);
+        case 1: return two ? launch_kawase<1, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<1, 1>(in, out, B, H, W, (float)scale, s);
+        case 2: return two ? launch_kawase<2, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<2, 1>(in, out, B, H, W, (float)scale, s);
+        case 3: return two ? launch_kawase<3, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<3, 1>(in, out, B, H, W, (float)scale, s);
+        case 4: return two ? launch_kawase<4, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<4, 1>(in, out, B, H, W, (float)scale, s);
+        case 5: return two ? launch_kawase<5, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<5, 1>(in, out, B, H, W, (float)scale, s);
+        case 6: return two ? launch_kawase<6, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<6, 1>(in, out, B, H, W, (float)scale, s);
         default: return -1;
     }
 }

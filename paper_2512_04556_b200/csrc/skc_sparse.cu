@@ -501,15 +501,23 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     // (K, K) pair per position in the body's order: the source -- and so the
     // compiled kernel -- depends only on the position pattern, and a layer
     // with new weights at the same positions reuses it
-    s << "#define NPOS " << std::max(1, p.npos) << "\nstruct KWT { float2 k[NPOS]; };\n#define KW kw.k\n";
+    s << "#define NPOS " << std::max(1, p.npos) << "\nstruct KWT { float2 k[NPOS]; };\n";
     if (f2) {
+        // register-only packing (no address-taken temporaries: thousands of
+        // inlined calls otherwise cost the front end tens of seconds)
         s << "__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {\n"
-             "    unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a), rb = *reinterpret_cast<unsigned long long *>(&b),\n"
-             "        rc = *reinterpret_cast<unsigned long long *>(&c), rd;\n"
-             "    asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(rd) : \"l\"(ra), \"l\"(rb), \"l\"(rc));\n"
-             "    return *reinterpret_cast<float2 *>(&rd);\n}\n";
+             "    float2 d;\n"
+             "    asm(\"{ .reg .b64 ra, rb, rc, rd; mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5}; mov.b64 rc, {%6, %7};\"\n"
+             "        \" fma.rn.f32x2 rd, ra, rb, rc; mov.b64 {%0, %1}, rd; }\"\n"
+             "        : \"=f\"(d.x), \"=f\"(d.y) : \"f\"(a.x), \"f\"(a.y), \"f\"(b.x), \"f\"(b.y), \"f\"(c.x), \"f\"(c.y));\n"
+             "    return d;\n}\n";
     }
     s << kSpPrelude;
+    // one named value per position, read once from the parameter struct: the
+    // body indexing the struct directly (1000+ reads) made NVRTC's optimizer
+    // take minutes on the widest layers; ptxas still folds these into
+    // constant-bank operands
+    for (int q = 0; q < std::max(1, p.npos); ++q) s << "    const float2 kw" << q << " = kw.k[" << q << "];\n";
     std::vector<int> first(p.Dy + 1, 0);  // index of stencil row a's first position in KW
     for (int a = 0; a < p.Dy; ++a) first[a + 1] = first[a] + (int)p.rows[a].size();
     if (f2) {
@@ -563,7 +571,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                 const int i = q - a;
                 for (size_t e = 0; e < p.rows[a].size(); ++e) {
                     const int c0 = p.SH + p.rows[a][e].b;
-                    const std::string kw = "KW[" + std::to_string(first[a] + (int)e) + "]";
+                    const std::string kw = "kw" + std::to_string(first[a] + (int)e);
                     if (c0 % 2 == 0) {
                         for (int j = 0; j < 4; ++j)
                             s << "        e" << i << "_" << j << " = ffma2(" << kw << ", wp" << c0 / 2 + j << ", e" << i << "_"
@@ -643,7 +651,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
             const int i = q - a;
             for (size_t ei = 0; ei < p.rows[a].size(); ++ei) {
                 const SpPos &e = p.rows[a][ei];
-                const std::string k = "KW[" + std::to_string(first[a] + (int)ei) + "].x";
+                const std::string k = "kw" + std::to_string(first[a] + (int)ei) + ".x";
                 for (int j = 0; j < 8; ++j)
                     s << "        a" << i << "_" << j << " = fmaf(" << k << ", w" << p.SH + e.b + j << ", a" << i << "_" << j
                       << ");\n";
