@@ -89,19 +89,37 @@ def _stack_of(basis):
     return stacked_params(basis)
 
 
+def _basis_close(skc, got, ref, targets):
+    """Basis entries from 6-step fits against the reference's float64 ones.
+    Adam's first steps are lr * sign(g): a gradient component that is zero by
+    symmetry up to rounding can step either way (one lr * M px), so offsets
+    are held to a few steps' length and each entry's impulse-response loss
+    against its target to 1e-3 relative."""
+    assert got.shape == ref.shape
+    assert np.abs(got - ref).max() < 0.05
+    assert np.median(np.abs(got - ref)) < 1e-5
+    for k, tgt in enumerate(targets):
+        def cpx_of(st):
+            return skc.KernelComplex(tuple(skc.SparseLayer(st[k, l, :, :2], st[k, l, :, 2]) for l in range(st.shape[1])))
+        ca, cb = cpx_of(got), cpx_of(ref)
+        cv = max(skc.auto_canvas(ca), skc.auto_canvas(cb), tgt.size) | 1
+        la = skc.loss(skc.synthesize_ir(ca, cv), tgt.embedded(cv), skc.LossKind("l1"))
+        lb = skc.loss(skc.synthesize_ir(cb, cv), tgt.embedded(cv), skc.LossKind("l1"))
+        assert abs(la / lb - 1) < 1e-3, (k, la, lb)
+
+
 def test_build_basis_kernelspec_targets(skc, golden):
     """svfilter.py:81-113 with KernelSpec targets, warm-started and not (the
-    latter is one batched fit); 6-step fits track the reference's float64
-    trajectory to fp32 noise."""
+    latter is one batched fit)."""
     g = golden("round2")
     cfg = skc.TrainConfig(steps=6)
     lk = skc.LossKind("l1")
     fam = lambda p: skc.KernelSpec("disk", (2.0 + 2.0 * p,), size=11)   # noqa: E731
     b1 = skc.build_basis(fam, [0.0, 0.5, 1.0], (4, 4), cfg=cfg, init=skc.InitStrategy("ss", seed=3), loss_kind=lk)
-    assert np.abs(_stack_of(b1) - g["bb_stack"]).max() < 1e-4
+    _basis_close(skc, _stack_of(b1), g["bb_stack"], [skc.generate_kernel(fam(p)) for p in (0.0, 0.5, 1.0)])
     b2 = skc.build_basis(fam, [0.0, 0.25, 1.0], (4, 4), cfg=cfg, init=skc.InitStrategy("ss", seed=3), loss_kind=lk,
                          warm_start=False)
-    assert np.abs(_stack_of(b2) - g["bb_nows_stack"]).max() < 1e-4
+    _basis_close(skc, _stack_of(b2), g["bb_nows_stack"], [skc.generate_kernel(fam(p)) for p in (0.0, 0.25, 1.0)])
 
 
 def test_build_basis_grid(skc, golden):
@@ -115,7 +133,8 @@ def test_build_basis_grid(skc, golden):
     init = skc.InitStrategy("ss", seed=5)
     grid = skc.build_basis_grid(fam, [0.0, 1.0], [0.0, 0.5, 1.0], (4, 4), cfg=cfg, init=init, loss_kind=lk)
     st = np.stack([_stack_of(grid.row_basis(iu)) for iu in range(2)])
-    assert np.abs(st - g["bbg_stack"]).max() < 1e-4
+    for iu, u in enumerate((0.0, 1.0)):
+        _basis_close(skc, st[iu], g["bbg_stack"][iu], [skc.generate_kernel(fam(u, v)) for v in (0.0, 0.5, 1.0)])
     from dataclasses import replace
     row1 = skc.build_basis(lambda v: fam(1.0, v), [0.0, 0.5, 1.0], (4, 4), cfg=cfg,
                            init=replace(init, seed=init.seed + 1000), loss_kind=lk)
@@ -130,7 +149,8 @@ def test_pst_numpy_stream_replays_reference(skc, golden):
     tgt = skc.DenseKernel(g["pst_tgt"])
     res = skc.pst_fit(tgt, (4, 4), skc.PSTConfig(chains=5, iterations=300, seed=7), skc.InitStrategy("ss", seed=2),
                       skc.LossKind("l1"), rng="numpy")
-    np.testing.assert_allclose(res.ladder, g["pst_ladder"], rtol=1e-15)
+    # the ladder scales with the start energy, which the device evaluates in fp32
+    np.testing.assert_allclose(res.ladder, g["pst_ladder"], rtol=1e-6)
     ref = g["pst_trace"]
     assert res.trace.shape == ref.shape
     assert np.array_equal(res.trace[:, 0], ref[:, 0])
