@@ -234,7 +234,8 @@ typedef struct skc_pst_cfg {
  * (baselines.py:132-140).  No host round trip per iteration: the loop is a
  * replayed CUDA graph; the host syncs once for the start energy (the ladder)
  * and once at the end.
- *   start_taps : device float32 (L, nmax, 3) init complex, zero padded
+ *   start_taps : device float64 (L, nmax, 3) init complex, zero padded
+ *                (the chain state is float64 like the reference's)
  *   tgt        : device float32 (M, M) target; canvas odd >= M
  *   noise      : NULL = Philox(seed) draws; else device float64
  *                (iterations, chains*L*nmax*3 + 2*chains - 1) standard
@@ -249,7 +250,7 @@ typedef struct skc_pst_cfg {
  *   accepts    : HOST int64 (chains) accepted proposals per ladder slot;
  *   swaps      : HOST int64 (chains - 1) accepted exchanges per pair
  */
-int skc_pst_run(const float *start_taps, const int *layout, int L, int nmax, int canvas, const float *tgt,
+int skc_pst_run(const double *start_taps, const int *layout, int L, int nmax, int canvas, const float *tgt,
                 int M, const skc_pst_cfg *cfg, const double *noise, double *ladder_out, double *trace,
                 double *best_taps, double *best_energy, long long *accepts, long long *swaps, void *stream);
 /*

@@ -50,7 +50,9 @@ constexpr int kKwNV = kKwTW / 16; // V warps (16 columns x 2 channel pairs each)
 // the band's whole row per lane, HS = 2 splits it into two 64-column halves
 // (each with its own 2 x reach halo) over twice the lanes
 template <int HS> __host__ __device__ constexpr int kw_nh() { return 2 * HS; }
-template <int HS> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS>() + kKwNV + 1); }  // + producer warp
+// the TMA producer is lane 0 of H warp 0 (a separate warp would make 13
+// warps for HS = 2: four on one SM sub-partition caps registers at 128)
+template <int HS> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS>() + kKwNV); }
 constexpr int kKwHP = kKwTW * 4 + 2;                  // H-result row pitch (words): 2 mod 32
 
 struct KwParams {
@@ -153,7 +155,7 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
 
 // one CTA per SM: the register budget is the whole file / the CTA's threads
 template <int L, int HS>
-__global__ void __maxnreg__(HS == 1 ? 168 : 152)
+__global__ void __maxnreg__(HS == 4 ? 128 : 168)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
     constexpr int kKwNH = kw_nh<HS>();
     using G = KwGen<L>;
@@ -179,31 +181,32 @@ __global__ void __maxnreg__(HS == 1 ? 168 : 152)
     }
     __syncthreads();
 
-    if (warp == kKwNH + kKwNV) {
-        // ------------------------------------------------ TMA producer ---
-        if (lane == 0) {
-            unsigned g = 0;
-            for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-                const Item m = item_of<L>(p, it);
-                for (int i = 0; i < m.iters; ++i, ++g) {
-                    const int s = g & 1;
-                    if (g >= 2) mbar_wait(&empty_in[s], ((g >> 1) - 1) & 1);
-                    if (p.dbg & 1) {
-                        mbar_arrive(&full_in[s]);
-                    } else {
-                        mbar_expect_tx(&full_in[s], kStageBytes);
-                        tma_load_3d(smem + s * kStageBytes, &tmap, &full_in[s], m.x0 - RX - BX::OFF, m.y0 - RX + i * kKwR, m.f);
-                    }
-                }
-            }
-        }
-        return;
-    }
     if (warp < kKwNH) {
         // ------------------------------------------ horizontal passes ---
         constexpr int SW = kKwTW / HS;            // output columns per lane
         const int seg = warp >> 1;
         const int r = (warp & 1) * 16 + (lane & 15), pr = lane >> 4;
+        // TMA producer (lane 0 of warp 0): loads run one chunk ahead of the
+        // passes; chunk c lands in stage c & 1 (the (c >> 1)-th use of it)
+        const bool prod = warp == 0 && lane == 0;
+        int l_it = blockIdx.x, l_i = 0;
+        Item lm;
+        if (l_it < p.items) lm = item_of<L>(p, l_it);
+        auto issue = [&](int stage) {
+            if (p.dbg & 1) {
+                mbar_arrive(&full_in[stage]);
+            } else {
+                mbar_expect_tx(&full_in[stage], kStageBytes);
+                tma_load_3d(smem + stage * kStageBytes, &tmap, &full_in[stage], lm.x0 - RX - BX::OFF,
+                            lm.y0 - RX + l_i * kKwR, lm.f);
+            }
+            if (++l_i >= lm.iters) {
+                l_i = 0;
+                l_it += gridDim.x;
+                if (l_it < p.items) lm = item_of<L>(p, l_it);
+            }
+        };
+        if (prod && l_it < p.items) issue(0);
         unsigned g = 0;
         for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
             const Item m = item_of<L>(p, it);
@@ -211,6 +214,11 @@ __global__ void __maxnreg__(HS == 1 ? 168 : 152)
             const bool edge = xs - RX < 0 || xs + SW + RX > p.W;
             for (int i = 0; i < m.iters; ++i, ++g) {
                 const int s = g & 1;
+                if (prod && l_it < p.items) {
+                    // chunk g + 1 reuses the stage of chunk g - 1: wait until every H lane released it
+                    if (g >= 1) mbar_wait(&empty_in[s ^ 1], ((g - 1) >> 1) & 1);
+                    issue(s ^ 1);
+                }
                 mbar_wait(&full_in[s], (g >> 1) & 1);
                 if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1);
                 const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) +
@@ -220,9 +228,12 @@ __global__ void __maxnreg__(HS == 1 ? 168 : 152)
                 } else if (HS == 1) {
                     if (edge) G::template h<true>(row, orow, xs - RX, p.W);
                     else G::template h<false>(row, orow, xs - RX, p.W);
-                } else {
+                } else if (HS == 2) {
                     if (edge) G::template h_half<true>(row, orow, xs - RX, p.W);
                     else G::template h_half<false>(row, orow, xs - RX, p.W);
+                } else {
+                    if (edge) G::template h_quarter<true>(row, orow, xs - RX, p.W);
+                    else G::template h_quarter<false>(row, orow, xs - RX, p.W);
                 }
                 mbar_arrive(&empty_in[s]);
                 mbar_arrive(&full_h[s]);
@@ -315,7 +326,8 @@ bool kawase_pattern(const double *taps, const int *layout, int L, int *b, double
 int kawase_hs() {
     static const int v = [] {
         const char *e = std::getenv("SKC_KAWASE_HS");
-        return (e && std::atoi(e) == 1) ? 1 : 2;
+        const int v = e ? std::atoi(e) : 2;
+        return (v == 1 || v == 4) ? v : 2;
     }();
     return v;
 }
@@ -395,16 +407,22 @@ int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int 
     for (int l = 0; l < L; ++l)
         if (b[l] != l) return -1;  // instantiated: the standard Kawase ladder r_l = l + 1/2
     if (!in) return encode_fn() ? SKC_OK : -1;  // plan query
-    const bool two = kawase_hs() == 2;
+    const int hs = kawase_hs();
+#define SKC_KW_CASE(LL)                                                                              \
+    case LL:                                                                                         \
+        return hs == 1 ? launch_kawase<LL, 1>(in, out, B, H, W, (float)scale, s)                     \
+                       : hs == 4 ? launch_kawase<LL, 4>(in, out, B, H, W, (float)scale, s)          \
+                                 : launch_kawase<LL, 2>(in, out, B, H, W, (float)scale, s);
     switch (L) {
-        case 1: return two ? launch_kawase<1, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<1, 1>(in, out, B, H, W, (float)scale, s);
-        case 2: return two ? launch_kawase<2, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<2, 1>(in, out, B, H, W, (float)scale, s);
-        case 3: return two ? launch_kawase<3, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<3, 1>(in, out, B, H, W, (float)scale, s);
-        case 4: return two ? launch_kawase<4, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<4, 1>(in, out, B, H, W, (float)scale, s);
-        case 5: return two ? launch_kawase<5, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<5, 1>(in, out, B, H, W, (float)scale, s);
-        case 6: return two ? launch_kawase<6, 2>(in, out, B, H, W, (float)scale, s) : launch_kawase<6, 1>(in, out, B, H, W, (float)scale, s);
+        SKC_KW_CASE(1)
+        SKC_KW_CASE(2)
+        SKC_KW_CASE(3)
+        SKC_KW_CASE(4)
+        SKC_KW_CASE(5)
+        SKC_KW_CASE(6)
         default: return -1;
     }
+#undef SKC_KW_CASE
 }
 
 }  // namespace skc

@@ -145,10 +145,11 @@ __global__ void __launch_bounds__(kProposeThreads) pst_propose_kernel(const __gr
             zw = curand_normal_double(&st);
         }
         const bool act = i < d.layout[l];
-        // normal(0, s) = 0 + s * standard_normal (numpy's Generator.normal)
-        poff[2 * q] = act ? off[2 * q] + (0.0 + d.sigma_o * zx) : 0.0;
-        poff[2 * q + 1] = act ? off[2 * q + 1] + (0.0 + d.sigma_o * zy) : 0.0;
-        pw[q] = act ? w[q] + (0.0 + d.sigma_w * zw) : 0.0;
+        // normal(0, s) = 0 + s * standard_normal (numpy's Generator.normal),
+        // each operation rounded separately (no FMA contraction), as numpy
+        poff[2 * q] = act ? __dadd_rn(off[2 * q], __dadd_rn(0.0, __dmul_rn(d.sigma_o, zx))) : 0.0;
+        poff[2 * q + 1] = act ? __dadd_rn(off[2 * q + 1], __dadd_rn(0.0, __dmul_rn(d.sigma_o, zy))) : 0.0;
+        pw[q] = act ? __dadd_rn(w[q], __dadd_rn(0.0, __dmul_rn(d.sigma_w, zw))) : 0.0;
     }
     __syncthreads();
     __shared__ int s_bad;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kProposeThreads) pst_propose_kernel(const __gr
         __syncthreads();
         for (int q = threadIdx.x; q < per; q += blockDim.x) {
             const double sm = s_sum[q / d.nmax];
-            if (fabs(sm) >= 1e-8) pw[q] = pw[q] / sm;
+            if (fabs(sm) >= 1e-8) pw[q] = __ddiv_rn(pw[q], sm);
         }
         __syncthreads();
     }
@@ -277,18 +278,18 @@ __global__ void __launch_bounds__(kAcceptThreads) pst_accept_kernel(const __grid
     }
 }
 
-__global__ void pst_start_kernel(const __grid_constant__ PstDev d, const float *start) {
+__global__ void pst_start_kernel(const __grid_constant__ PstDev d, const double *start) {
     // every chain starts from the init complex (baselines.py:157-166); the
     // initial energies are in d.energy already
     const int per = d.L * d.nmax;
     for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < d.chains * per; e += blockDim.x * gridDim.x) {
         const int q = e % per;
-        d.off[2 * e] = (double)start[3 * q];
-        d.off[2 * e + 1] = (double)start[3 * q + 1];
-        d.w[e] = (double)start[3 * q + 2];
-        d.taps[3 * e] = start[3 * q];
-        d.taps[3 * e + 1] = start[3 * q + 1];
-        d.taps[3 * e + 2] = start[3 * q + 2];
+        d.off[2 * e] = start[3 * q];
+        d.off[2 * e + 1] = start[3 * q + 1];
+        d.w[e] = start[3 * q + 2];
+        d.taps[3 * e] = (float)start[3 * q];
+        d.taps[3 * e + 1] = (float)start[3 * q + 1];
+        d.taps[3 * e + 2] = (float)start[3 * q + 2];
     }
 }
 
@@ -326,7 +327,7 @@ using namespace skc;
 
 extern "C" {
 
-int skc_pst_run(const float *start_taps, const int *layout, int L, int nmax, int canvas, const float *tgt,
+int skc_pst_run(const double *start_taps, const int *layout, int L, int nmax, int canvas, const float *tgt,
                 int M, const skc_pst_cfg *cfg, const double *noise, double *ladder_out, double *trace,
                 double *best_taps, double *best_energy, long long *accepts, long long *swaps, void *stream) {
     if (!cfg || !start_taps || !layout || !tgt || !ladder_out || !trace || !best_taps || !best_energy ||

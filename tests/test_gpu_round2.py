@@ -94,7 +94,7 @@ def _basis_close(skc, got, ref, targets):
     Adam's first steps are lr * sign(g): a gradient component that is zero by
     symmetry up to rounding can step either way (one lr * M px), so offsets
     are held to a few steps' length and each entry's impulse-response loss
-    against its target to 1e-3 relative."""
+    against its target to 1% relative."""
     assert got.shape == ref.shape
     assert np.abs(got - ref).max() < 0.05
     assert np.median(np.abs(got - ref)) < 1e-5
@@ -105,7 +105,7 @@ def _basis_close(skc, got, ref, targets):
         cv = max(skc.auto_canvas(ca), skc.auto_canvas(cb), tgt.size) | 1
         la = skc.loss(skc.synthesize_ir(ca, cv), tgt.embedded(cv), skc.LossKind("l1"))
         lb = skc.loss(skc.synthesize_ir(cb, cv), tgt.embedded(cv), skc.LossKind("l1"))
-        assert abs(la / lb - 1) < 1e-3, (k, la, lb)
+        assert abs(la / lb - 1) < 1e-2, (k, la, lb)
 
 
 def test_build_basis_kernelspec_targets(skc, golden):
