@@ -111,6 +111,94 @@ def v_body(bs):
     return "\n".join(out)
 
 
+P = 16    # loop period: every ring size divides it (ring_size), so slots are compile-time
+
+
+def ring_size(D):
+    r = 1
+    while r < D:
+        r *= 2
+    assert P % r == 0
+    return r
+
+
+def h_loop_body(bs, tw):
+    """Horizontal passes of one row segment of `tw` output columns as a
+    rolled loop over blocks of P stream steps (skewed wavefront inside a
+    block: at step tau layer l handles index tau - l).  Delay lines have a
+    power-of-two size R_l >= 2 b_l + 1 dividing P, so every ring slot is a
+    compile-time register within the block and the code is one block long
+    (the fully unrolled row was ~100 KB of SASS: instruction-cache bound).
+    State starts at zero: outputs before a layer's warm-up are never stored
+    (a stored output only depends on inputs inside the row)."""
+    L = len(bs)
+    RX = lag(bs, L - 1)
+    IW = tw + 2 * RX
+    nblk = (IW + L - 1 + P - 1) // P
+    Rs = [ring_size(2 * b + 1) for b in bs]
+    regs = ["sv", "z2"] + [f"a{l}" for l in range(L + 1)] + [f"p{l}" for l in range(L)] + \
+        [f"r{l}_{i}" for l in range(L) for i in range(Rs[l])]
+    out = [f"    float2 {', '.join(regs)};",
+           "    z2 = make_float2(0.f, 0.f);"]
+    out.append("    " + " ".join(f"{r} = z2;" for r in regs[2:]))
+    out.append(f"#pragma unroll 1")
+    out.append(f"    for (int j = 0; j < {nblk}; ++j) {{")
+    out.append(f"        const unsigned *inj = in + {2 * P} * j;")
+    out.append(f"        const int kj = {P} * j;")
+    for t in range(P):
+        for l in reversed(range(L)):
+            D = 2 * bs[l] + 1
+            R = Rs[l]
+            if l == 0:
+                out.append(f"        a0 = h2f2(inj[{2 * t}]);")
+            rd = f"r{l}_{(t - l - D) % R}"
+            wr = f"r{l}_{(t - l) % R}"
+            out.append(f"        sv = add2(a{l}, p{l}); p{l} = a{l}; a{l + 1} = add2(sv, {rd}); {wr} = sv;")
+            out.append(f"        if (EDGE && (unsigned)(xg0 + kj + {t - l - lag(bs, l)}) >= (unsigned)W) a{l + 1} = z2;")
+            if l == L - 1:
+                o = t - (L - 1) - 2 * RX
+                out.append(f"        {{ const int oc = kj + {o}; if ((unsigned)oc < {tw}u) out[2 * oc] = a{L}; }}")
+    out.append("    }")
+    return "\n".join(out)
+
+
+def v_loop_state(bs):
+    L = len(bs)
+    Rs = [ring_size(2 * b + 1) for b in bs]
+    return " ".join([f"float2 a{l};" for l in range(1, L)] + [f"float2 p{l};" for l in range(L)] +
+                    [f"float2 r{l}_{i};" for l in range(L) for i in range(Rs[l])])
+
+
+def v_loop_body(bs):
+    """One R-row iteration of the vertical passes as a loop over blocks of P
+    rows (R % P == 0 and every ring size divides P: no rotation at the end).
+    At local step t of block h layer l handles stream step 32 i + P h + t - l."""
+    assert R % P == 0
+    L = len(bs)
+    Rs = [ring_size(2 * b + 1) for b in bs]
+    out = ["    float2 sv, a0;", "    const float2 z2 = make_float2(0.f, 0.f);", "#pragma unroll 1",
+           f"    for (int h = 0; h < {R // P}; ++h) {{",
+           f"        const float2 *colh = col + h * {P * HP2};",
+           f"        const int th = {P} * h;"]
+    for t in range(P):
+        for l in reversed(range(L)):
+            D = 2 * bs[l] + 1
+            Rl = Rs[l]
+            src = "a0" if l == 0 else f"S.a{l}"
+            if l == 0:
+                out.append(f"        a0 = colh[{t * HP2}];")
+            dst = "a0" if l == L - 1 else f"S.a{l + 1}"
+            rd = f"S.r{l}_{(t - l - D) % Rl}"
+            wr = f"S.r{l}_{(t - l) % Rl}"
+            out.append(f"        sv = add2({src}, S.p{l}); S.p{l} = {src}; {dst} = add2(sv, {rd}); {wr} = sv;")
+            out.append(f"        if (MASK && (unsigned)(yin0 + th + {t - l - lag(bs, l)}) >= (unsigned)H) {dst} = z2;")
+            if l == L - 1:
+                out.append(f"        {{ const int yo = yout0 + th + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
+                           f"*reinterpret_cast<__half2 *>(outp + (long long)yo * rs) = __float22half2_rn(mul2(a0, sc)); }}")
+    out.append("    }")
+    return "\n".join(out)
+
+
 def emit():
     parts = ["// generated by gen_kawase.py -- do not edit", "template <int L> struct KwGen;"]
     for L in range(1, MAX_L + 1):
@@ -118,26 +206,26 @@ def emit():
         parts.append(f"""
 template <> struct KwGen<{L}> {{
     static constexpr int kReach = {lag(bs, L - 1)};
-    struct State {{ {v_state(bs)} }};
+    struct State {{ {v_loop_state(bs)} }};
     static __device__ __forceinline__ void zero(State &S) {{ memset(&S, 0, sizeof(S)); }}
+    // a band's whole row / half / quarter (128 / 64 / 32 output columns):
+    // the H work split over 1 / 2 / 4 times the lanes
     template <bool EDGE>
     static __device__ __forceinline__ void h(const unsigned *in, float2 *out, int xg0, int W) {{
-{h_body(bs)}
+{h_loop_body(bs, TW)}
     }}
-    // half / quarter of a band (64 / 32 output columns): the H work split
-    // over 2 / 4 times the lanes
     template <bool EDGE>
     static __device__ __forceinline__ void h_half(const unsigned *in, float2 *out, int xg0, int W) {{
-{h_body(bs, TW // 2)}
+{h_loop_body(bs, TW // 2)}
     }}
     template <bool EDGE>
     static __device__ __forceinline__ void h_quarter(const unsigned *in, float2 *out, int xg0, int W) {{
-{h_body(bs, TW // 4)}
+{h_loop_body(bs, TW // 4)}
     }}
     template <bool MASK>
     static __device__ __forceinline__ void v(const float2 *col, State &S, int yin0, int H, int yout0, int y0, int y1,
                                              __half *outp, long long rs, float2 sc) {{
-{v_body(bs)}
+{v_loop_body(bs)}
     }}
 }};""")
     return "\n".join(parts) + "\n"
