@@ -179,7 +179,8 @@ def v_loop_body(bs):
     out = ["    float2 sv, a0;", "    const float2 z2 = make_float2(0.f, 0.f);", "#pragma unroll 1",
            f"    for (int h = 0; h < {R // P}; ++h) {{",
            f"        const float2 *colh = col + h * {P * HP2};",
-           f"        const int th = {P} * h;"]
+           f"        const int th = {P} * h;",
+           f"        __half *orow = outp + (long long)(yout0 + th - {L - 1}) * rs;   // advanced by one row per step"]
     for t in range(P):
         for l in reversed(range(L)):
             D = 2 * bs[l] + 1
@@ -194,7 +195,7 @@ def v_loop_body(bs):
             out.append(f"        if (MASK && (unsigned)(yin0 + th + {t - l - lag(bs, l)}) >= (unsigned)H) {dst} = z2;")
             if l == L - 1:
                 out.append(f"        {{ const int yo = yout0 + th + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
-                           f"*reinterpret_cast<__half2 *>(outp + (long long)yo * rs) = __float22half2_rn(mul2(a0, sc)); }}")
+                           f"*reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs; }}")
     out.append("    }")
     return "\n".join(out)
 

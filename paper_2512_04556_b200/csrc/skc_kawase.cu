@@ -79,9 +79,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     unsigned done = 0;
     do {
         asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
-            : "r"(a), "r"(parity)
+            : "r"(a), "r"(parity), "r"(0x20000u)   // suspend (not spin) up to ~131 us per try
             : "memory");
     } while (!done);
 }
