@@ -291,7 +291,7 @@ class Chain:
                        "frames_per_gpu": self.nf,
                        "l2": "inputs larger than L2, no flush" if npx * esz > 126e6 else "L2 flushed between steps"}
         self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if npx * esz <= 126e6 else None
-        self.kernel = "fused_chain_kernel" if self.fused else "layer kernels (dense stencil / generated sparse stencil / tap tile, see roofline.fp32_pipe.kernel)"
+        self.kernel = ("kawase_sep_kernel<6,2> (fused separable Kawase chain, csrc/skc_kawase.cu)" if self.fused else "layer kernels (dense stencil / generated sparse stencil / tap tile, see roofline.fp32_pipe.kernel)")
 
     def step(self, stream, events=None):
         from paper_2512_04556_b200 import _native as nat
