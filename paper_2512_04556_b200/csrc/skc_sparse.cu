@@ -490,7 +490,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     // and 4 for small, narrow KR = 3 bodies (64 registers: config 1's 58-position
     // 9 x 9 layer 1.58 -> 1.47 ms; 5 CTAs spill)
     int minb = (allc || p.KR >= 5) ? std::min(2, sp_minb()) : sp_minb();
-    if (!allc && sp_f2() == 1 && p.KR < 5 && p.npos <= 64 && p.nw <= 20) minb = env_int("SKC_SPARSE_MINB_SMALL", 4);
+    if (!allc && (sp_f2() == 1 || sp_f2() == 3) && p.KR < 5 && p.npos <= 64 && p.nw <= 20) minb = env_int("SKC_SPARSE_MINB_SMALL", 4);
     s << "#define MINB " << minb << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define USE_TMA " << sp_tma() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
@@ -531,10 +531,15 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
         for (int i = 0; i < p.KR; ++i)
             for (int j = 0; j < 4; ++j) s << (i || j ? ", " : " ") << "e" << i << "_" << j << " = make_float2(0.f, 0.f)";
         const bool xchg = sp_f2() == 2;  // odd positions: 4 pairs (1,2)..(7,8), output 8 to the right neighbour
+        const bool pair_ends = sp_f2() == 3;  // odd positions: outputs 0 and 7 as one FFMA2
         for (int i = 0; i < p.KR; ++i)
             for (int j = 0; j < (xchg ? 4 : 3); ++j) s << ", o" << i << "_" << j << " = make_float2(0.f, 0.f)";
         s << ";\n    float";
         for (int i = 0; i < p.KR; ++i) s << (i ? ", " : " ") << "s" << i << "_0 = 0.f, s" << i << "_7 = 0.f";
+        if (pair_ends) {
+            s << ";\n    float2";
+            for (int i = 0; i < p.KR; ++i) s << (i ? ", " : " ") << "z" << i << " = make_float2(0.f, 0.f)";
+        }
         s << ";\n    float2";
         for (int m = 0; m < p.nw / 2; ++m) s << (m ? ", " : " ") << "wp" << m;
         s << ";\n";
@@ -582,6 +587,14 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                         for (int j = 0; j < 4; ++j)
                             s << "        o" << i << "_" << j << " = ffma2(" << kw << ", wp" << (c0 + 1) / 2 + j << ", o" << i
                               << "_" << j << ");\n";
+                    } else if (pair_ends) {
+                        // outputs 0 and 7 as one FFMA2 on the accumulator pair
+                        // z<i> = (out 0, out 7) with the operand pair (w[c0], w[c0+7])
+                        s << "        z" << i << " = ffma2(" << kw << ", make_float2(wp" << (c0 - 1) / 2 << ".y, wp"
+                          << (c0 + 7) / 2 << ".x), z" << i << ");\n";
+                        for (int j = 0; j < 3; ++j)
+                            s << "        o" << i << "_" << j << " = ffma2(" << kw << ", wp" << (c0 + 1) / 2 + j << ", o" << i
+                              << "_" << j << ");\n";
                     } else {
                         s << "        s" << i << "_0 = fmaf(" << kw << ".x, wp" << (c0 - 1) / 2 << ".y, s" << i << "_0);\n";
                         for (int j = 0; j < 3; ++j)
@@ -613,6 +626,8 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                   << "] = e" << i << "_" << j << ".y;\n";
             if (xchg) {
                 s << "    acc[" << i << "][0] += x" << i << "; acc[" << i << "][7] += o" << i << "_3.x;\n";
+            } else if (pair_ends) {
+                s << "    acc[" << i << "][0] += z" << i << ".x; acc[" << i << "][7] += z" << i << ".y;\n";
             } else {
                 s << "    acc[" << i << "][0] += s" << i << "_0; acc[" << i << "][7] += s" << i << "_7;\n";
             }
@@ -943,7 +958,7 @@ bool allc_ok(SpPlan &p, int S, int C, bool in_f32) {
     p.smem = in_f32 ? (size_t)p.nrows * (C * p.pitch + 1) * sizeof(float) : (size_t)p.nrows * (C * p.pitch + 2) * 2;
     const int D = dense_size_for(std::max(p.Dx, p.Dy));
     const bool stencil_like = eligible(p, S) || (D != 0 && D * D < 4 * S);
-    return sparse_mode() != 0 && sp_hwc() == 2 && sp_f2() == 1 && stencil_like && p.npos > 0 &&
+    return sparse_mode() != 0 && sp_hwc() == 2 && (sp_f2() == 1 || sp_f2() == 3) && stencil_like && p.npos > 0 &&
            (long long)p.npos * p.KR * 8 <= kSpMaxFfma && 2 * p.smem <= (size_t)kMaxSmem;
 }
 
@@ -1020,7 +1035,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
     // HWC input: the all-channel head (fp32 in, planar out), or with
     // SKC_SPARSE_HWC=1 the per-channel variant; otherwise the dense / tap kernels
-    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 == out_f32 && out_pl && sp_f2() == 1) ? C : 0;
+    const int allc = (in_hwc && sp_hwc() == 2 && in_f32 == out_f32 && out_pl && (sp_f2() == 1 || sp_f2() == 3)) ? C : 0;
     if (in_hwc && !allc && sp_hwc() != 1) return -1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4));
@@ -1078,7 +1093,7 @@ int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_lay
     if (!taps || S < 1) return fail(SKC_EBADARG, "bad layer arguments");
     const SpPlan p = make_plan(taps, S);
     // the all-channel head variant (SKC_SPARSE_HWC=2) is checked for C = 3
-    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == out_dtype && out_layout == SKC_CHW && sp_f2() == 1)
+    const int allc = (in_layout == SKC_HWC && sp_hwc() == 2 && in_dtype == out_dtype && out_layout == SKC_CHW && (sp_f2() == 1 || sp_f2() == 3))
                          ? (in_dtype == SKC_F32 ? 3 : 4) : 0;
     if (!allc && !eligible(p, S)) return 1;
     std::string why;
