@@ -703,7 +703,12 @@ def binding_roofline(wl, per_launch, step_ms, hbm_peak):
         b = len(wl.targets) * wl.cfg.steps * 1408 * 4 * 129 * 129
         return {"resource": "smem", "achieved": b / t / 1e9, "peak": pk, "unit": "GB/s", "frac": b / t / 1e9 / pk,
                 "kernel": wl.kernel, "definition": "SURVEY 8(d): 1408 fetches x 4 B x 129^2 per kernel-iteration "
-                                                   "(forward + gradient corners + adjoint) / kernel time"}
+                                                   "(forward + gradient corners + adjoint) / kernel time",
+                "note": "frac > 1: the kernel works on each intermediate's live box (its support), not the whole "
+                        "129^2 canvas the definition counts; what binds is issue/latency inside 256 resident CTAs "
+                        "(ncu, profiles/r02_c4_fit.md: FMA pipe 31.8% active, issue 53.5%, barrier 22.5% and "
+                        "dependency-wait 20.8% of stalls)",
+                "ncu_fma_pipe_active": 0.318}
     return None
 
 

@@ -243,7 +243,11 @@ __device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSm
         const int wy = ADJ ? y0 - d.y - 1 : y0 + d.y;
         const int wx = ADJ ? x0 - d.x - 1 : x0 + d.x;
         float win[kFKR + 1][kFMC + 1];
-        if (CHECK) {
+        // an edge block (CHECK) still reads most taps' windows entirely inside
+        // src: when every active lane's window is, take the unchecked loads
+        const bool tin = !CHECK || (wy >= src.y0 && wy + kFKR < src.y0 + src.h && wx >= src.x0 &&
+                                    wx + kFMC < src.x0 + src.w);
+        if (CHECK && !__all_sync(__activemask(), tin)) {
 #pragma unroll
             for (int r = 0; r <= kFKR; ++r)
 #pragma unroll
@@ -456,7 +460,10 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
                 if (k >= nt) break;
                 const int2 d = S.ixy[s0 + t0 + k];
                 float win[kFKR + 1][kFMC + 1];
-                if (inside) {
+                const int wy = y0 + d.y, wx = x0 + d.x;
+                const bool tin = inside || (wy >= I.y0 && wy + kFKR < I.y0 + I.h && wx >= I.x0 &&
+                                            wx + kFMC < I.x0 + I.w);
+                if (inside || __all_sync(__activemask(), tin)) {
                     const float *q = I.p + (y0 + d.y - I.y0) * I.s + (x0 + d.x - I.x0);
 #pragma unroll
                     for (int r = 0; r <= kFKR; ++r)
