@@ -242,6 +242,10 @@ __device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSm
         // forward: out(y,x) reads src(y + d + corner); adjoint: src(y - d - corner)
         const int wy = ADJ ? y0 - d.y - 1 : y0 + d.y;
         const int wx = ADJ ? x0 - d.x - 1 : x0 + d.x;
+        // a window that misses src's box entirely adds exact zeros: skip it
+        if (CHECK && (wy > src.y0 + src.h - 1 || wy + kFKR < src.y0 || wx > src.x0 + src.w - 1 ||
+                      wx + kFMC < src.x0))
+            continue;
         float win[kFKR + 1][kFMC + 1];
         // an edge block (CHECK) still reads most taps' windows entirely inside
         // src: when every active lane's window is, take the unchecked loads
@@ -445,6 +449,10 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
             int bx, by;
             block_of(b, nbx, nby, bx, by);
             const int y0 = g.y0 + by * kFKR, x0 = g.x0 + bx * kFMC;
+            // no tap of the layer can reach I's box from this block: nothing to add
+            if (y0 + dr.z > I.y0 + I.h - 1 || y0 + kFKR - 1 + dr.w < I.y0 || x0 + dr.x > I.x0 + I.w - 1 ||
+                x0 + kFMC - 1 + dr.y < I.x0)
+                continue;
             float gv[kFKR][kFMC];
 #pragma unroll
             for (int r = 0; r < kFKR; ++r)
@@ -461,6 +469,10 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
                 const int2 d = S.ixy[s0 + t0 + k];
                 float win[kFKR + 1][kFMC + 1];
                 const int wy = y0 + d.y, wx = x0 + d.x;
+                // a window that misses I's box reads only zeros: its products add
+                // exact zeros, so the lane skips it (I is the small support of an
+                // early intermediate, g the much larger box of a later gradient)
+                if (wy > I.y0 + I.h - 1 || wy + kFKR < I.y0 || wx > I.x0 + I.w - 1 || wx + kFMC < I.x0) continue;
                 const bool tin = inside || (wy >= I.y0 && wy + kFKR < I.y0 + I.h && wx >= I.x0 &&
                                             wx + kFMC < I.x0 + I.w);
                 if (inside || __all_sync(__activemask(), tin)) {
