@@ -449,10 +449,6 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
             int bx, by;
             block_of(b, nbx, nby, bx, by);
             const int y0 = g.y0 + by * kFKR, x0 = g.x0 + bx * kFMC;
-            // no tap of the layer can reach I's box from this block: nothing to add
-            if (y0 + dr.z > I.y0 + I.h - 1 || y0 + kFKR - 1 + dr.w < I.y0 || x0 + dr.x > I.x0 + I.w - 1 ||
-                x0 + kFMC - 1 + dr.y < I.x0)
-                continue;
             float gv[kFKR][kFMC];
 #pragma unroll
             for (int r = 0; r < kFKR; ++r)
