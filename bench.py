@@ -277,6 +277,19 @@ class Chain:
                     self.smem_bytes.append(0)
                     self.smem_kind.append("direct gather (global)")
                     self.launch_fma.append(4 * t.shape[0] * npx)
+        # config 0 (one 512^2 frame, ~10-20 us per launch) is timed through the
+        # call a user makes -- skc_chain_fwd issues its launches back to back
+        # from C -- rather than launch by launch from Python, whose per-call
+        # host overhead would leave the GPU idle between the short kernels
+        self.whole = name == "c0" and not self.fused
+        if self.whole:
+            self.kernels_per_step = self.launches_per_step
+            kinds = ", ".join(k.split(" (")[0] for k in self.smem_kind)
+            self.launch_fma = [sum(self.launch_fma)]
+            self.smem_bytes = [0]
+            self.smem_kind = [f"whole chain via skc_chain_fwd ({self.launches_per_step} launches: {kinds})"]
+            self.alg_bytes = [px * 2 * esz]
+            self.launches_per_step = 1
         self.bufs = [torch.empty(npx, dtype=torch.float16 if msz == 2 else torch.float32, device=dev)
                      for _ in range(2)]
         self.metric = {
@@ -303,7 +316,7 @@ class Chain:
         # the launch sequence skc_chain_fwd runs (SKC_CHAIN_IO policy: HWC in ->
         # planar layers (skc_chain_mid_dtype) -> relayout to HWC out), issued one launch at a
         # time so each can be timed
-        if self.fused:
+        if self.fused or self.whole:
             if events is not None:
                 events[0][0].record(stream)
             lay = np.ascontiguousarray(self.cpx.layout, dtype=np.int32)

@@ -121,10 +121,10 @@ struct SpPlan {
     size_t smem = 0;
 };
 
-SpPlan make_plan(const double *taps, int S) {
+SpPlan make_plan(const double *taps, int S, int wy = 0) {
     SpPlan p;
     p.KR = sp_kr();
-    p.WY = sp_wy();
+    p.WY = wy > 0 ? wy : sp_wy();
     p.TH = 8 * p.KR * p.WY;
     std::map<std::pair<int, int>, double> acc;  // (dy, dx) -> merged weight
     for (int i = 0; i < S; ++i) {
@@ -491,6 +491,9 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     // 9 x 9 layer 1.58 -> 1.47 ms; 5 CTAs spill)
     int minb = (allc || p.KR >= 5) ? std::min(2, sp_minb()) : sp_minb();
     if (!allc && (sp_f2() == 1 || sp_f2() == 3) && p.KR < 5 && p.npos <= 64 && p.nw <= 20) minb = env_int("SKC_SPARSE_MINB_SMALL", 4);
+    // one warp row (128 threads, half-height tiles: small images): twice the
+    // CTAs at the same registers per thread
+    if (p.WY == 1 && sp_wy() == 2) minb *= 2;
     s << "#define MINB " << minb << "\n#define F2MODE " << sp_f2() << "\n";
     s << "#define USE_TMA " << sp_tma() << "\n";
     s << "#define NWARP " << 4 * p.WY << "\n";
@@ -974,6 +977,7 @@ struct SpLaunch {
     Key key{0, 0};
     std::string src;           // kept until the kernel is ready
     std::vector<float> kw;     // (K, K) per position: the kernel parameter
+    int WY = 2;                // warps along y (CTA = 128 * WY threads)
 };
 constexpr size_t kMaxMemo = 4096;
 std::mutex g_memo_mu;
@@ -1037,16 +1041,24 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     // SKC_SPARSE_HWC=1 the per-channel variant; otherwise the dense / tap kernels
     const int allc = (in_hwc && sp_hwc() == 2 && in_f32 == out_f32 && out_pl && (sp_f2() == 1 || sp_f2() == 3)) ? C : 0;
     if (in_hwc && !allc && sp_hwc() != 1) return -1;
+    // a grid below two waves at the default tile height (small images, e.g.
+    // config 0's 512^2 frame) runs half-height tiles of one warp row instead
+    int cur_dev = 0, nsm = 148;
+    if (cudaGetDevice(&cur_dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cur_dev);
+    const int th_default = 8 * sp_wy() * sp_kr();
+    const long long ctas = (long long)ceil_div(W, kSpTW) * (allc ? 1 : C) * ceil_div(H, th_default) * B;
+    const int wy = (sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1)) ? 1 : 0;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
-                                                  (in_hwc ? 8 : 0) | (allc << 4));
+                                                  (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12));
     std::shared_ptr<SpLaunch> l = memo_get(key);
     if (!l) {
-        SpPlan p = make_plan(taps, S);
+        SpPlan p = make_plan(taps, S, wy);
         l = std::make_shared<SpLaunch>();
         l->eligible = eligible(p, S);
         if (allc) l->eligible = allc_ok(p, S, allc, in_f32);
         l->npos = p.npos;
         l->TH = p.TH;
+        l->WY = p.WY;
         l->words_per_out = p.words_per_out;
         l->smem = p.smem;
         if (l->eligible) {
@@ -1075,7 +1087,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *kwp = (void *)l->kw.data();
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp, kwp};
-    const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * sp_wy()), args, l->smem, s);
+    const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * l->WY), args, l->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
 }
