@@ -155,6 +155,20 @@ class ClockSampler:
 
 # ------------------------------------------------------------- workloads ---
 
+def merged_positions(t):
+    """Nonzero integer positions of a layer's merged bilinear corners (one FMA
+    per position and output channel-pixel in the generated stencils)."""
+    ix, iy = np.floor(t[:, 0]), np.floor(t[:, 1])
+    fx, fy, w = t[:, 0] - ix, t[:, 1] - iy, t[:, 2]
+    acc = {}
+    for cx, cy, cw in ((0, 0, w * (1 - fx) * (1 - fy)), (1, 0, w * fx * (1 - fy)),
+                       (0, 1, w * (1 - fx) * fy), (1, 1, w * fx * fy)):
+        for k in range(t.shape[0]):
+            key = (int(iy[k]) + cy, int(ix[k]) + cx)
+            acc[key] = acc.get(key, 0.0) + cw[k]
+    return sum(1 for v in acc.values() if np.float32(v) != 0)
+
+
 class Chain:
     """Uniform chain workloads (c0, c1, c3, c3big): per-layer launches timed."""
 
@@ -202,7 +216,15 @@ class Chain:
         if self.mid_dt < 0:
             raise RuntimeError(nat.last_error())
         msz = 2 if self.mid_dt == nat.SKC_F16 else 4
-        self.launches_per_step = 1 if self.fused else len(self.taps) + int(self.pre) + int(self.post)
+        # layers 0 and 1 as one fused launch (skc_layer_pair_fwd) when skc_chain_fwd would take it
+        bnd = 0 if self.boundary == "zero" else 1
+        self.pair = (not self.fused and not self.pre and len(self.taps) >= 3 and self.storage == torch.float32
+                     and self.mid_dt == nat.SKC_F32
+                     and nat.lib().skc_layer_pair_fwd(None, None, self.nf, self.h, self.w, self.c,
+                                                      nat.dbl(self.taps[0]), self.taps[0].shape[0],
+                                                      nat.dbl(self.taps[1]), self.taps[1].shape[0], bnd, None) == nat.SKC_OK)
+        self.launches_per_step = 1 if self.fused else (len(self.taps) - int(self.pair) + int(self.pre)
+                                                       + int(self.post))
         self.units_per_step = self.nf * self.h * self.w
         esz = 2 if self.storage == torch.float16 else 4
         # algorithmic HBM bytes per launch: image in + out in their storage dtypes
@@ -216,9 +238,17 @@ class Chain:
         # windows the chosen kernel reads; skc_layer_plan says which kernel runs)
         self.smem_bytes, self.smem_kind, self.launch_fma = [], [], []
         if not self.fused:
-            seq = (["relayout"] if self.pre else []) + list(range(len(self.taps))) + (["relayout"] if self.post else [])
+            seq = ((["relayout"] if self.pre else []) + (["pair"] if self.pair else [])
+                   + list(range(2 if self.pair else 0, len(self.taps))) + (["relayout"] if self.post else []))
             import ctypes
             for item in seq:
+                if item == "pair":
+                    n0, n1 = merged_positions(self.taps[0]), merged_positions(self.taps[1])
+                    npx = self.nf * self.h * self.w * self.c
+                    self.smem_bytes.append(0)
+                    self.smem_kind.append(f"fused head pair, {n0} + {n1} positions (generated skc_sparse_pair)")
+                    self.launch_fma.append((n0 + n1) * npx)
+                    continue
                 if item == "relayout":
                     self.smem_bytes.append(0)
                     self.smem_kind.append("relayout")
@@ -242,15 +272,7 @@ class Chain:
                 elif kind.value in (1, 3) and item == 0 and not self.pre and self.storage == torch.float32:
                     # fp32 HWC chain head of a stencil-type layer: the all-channel generated
                     # stencil (skc_sparse.cu); nonzero merged corner positions counted here
-                    ix, iy = np.floor(t[:, 0]), np.floor(t[:, 1])
-                    fx, fy, w = t[:, 0] - ix, t[:, 1] - iy, t[:, 2]
-                    acc = {}
-                    for cx, cy, cw in ((0, 0, w * (1 - fx) * (1 - fy)), (1, 0, w * fx * (1 - fy)),
-                                       (0, 1, w * (1 - fx) * fy), (1, 1, w * fx * fy)):
-                        for k in range(t.shape[0]):
-                            key = (int(iy[k]) + cy, int(ix[k]) + cx)
-                            acc[key] = acc.get(key, 0.0) + cw[k]
-                    npos = sum(1 for v in acc.values() if np.float32(v) != 0)
+                    npos = merged_positions(t)
                     self.smem_bytes.append(0)
                     self.smem_kind.append(f"all-channel sparse head, {npos} positions (generated)")
                     self.launch_fma.append(npos * npx)
@@ -331,7 +353,9 @@ class Chain:
         seq = []
         if self.pre:
             seq.append(("relayout", None))
-        seq += [("layer", t) for t in self.taps]
+        if self.pair:
+            seq.append(("pair", None))
+        seq += [("layer", t) for t in self.taps[2 if self.pair else 0:]]
         if self.post:
             seq.append(("relayout", None))
         bnd = 0 if self.boundary == "zero" else 1
@@ -343,7 +367,11 @@ class Chain:
             lay_out = nat.SKC_HWC if last else nat.SKC_CHW
             if events is not None:
                 events[k][0].record(stream)
-            if kind == "relayout":
+            if kind == "pair":
+                t0, t1 = self.taps[0], self.taps[1]
+                rc = lib.skc_layer_pair_fwd(nat.ptr(src), nat.ptr(dst), self.nf, self.h, self.w, self.c,
+                                            nat.dbl(t0), t0.shape[0], nat.dbl(t1), t1.shape[0], bnd, sp)
+            elif kind == "relayout":
                 rc = lib.skc_relayout(nat.ptr(src), sdt, lay_in, nat.ptr(dst), ddt, lay_out, self.nf, self.h,
                                       self.w, self.c, sp)
             else:

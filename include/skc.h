@@ -38,6 +38,7 @@ extern "C" {
 #define SKC_ETRUNC 3       /* maps to TruncationError                        */
 #define SKC_ECUDA 4        /* CUDA runtime failure; see skc_last_error()     */
 #define SKC_EDEGENERATE 5  /* maps to OptimError "SUM normalization degenerate" */
+#define SKC_ENOTTAKEN 6    /* a fused path does not apply: run the layers one by one */
 
 /* storage dtypes (arithmetic is always fp32) */
 #define SKC_F32 0
@@ -128,6 +129,26 @@ int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary,
  * not take that path, SKC_ECUDA = the run-time compiler is missing or rejected
  * it (skc_last_error).  Layouts are SKC_HWC / SKC_CHW. */
 int skc_sparse_compile_check(const double *taps, int S, int in_dtype, int in_layout, int out_dtype, int out_layout);
+
+/*
+ * A chain's first two layers as ONE fused launch (engine.apply_complex,
+ * engine.py:173-178, layers 0 and 1 without the materialised intermediate):
+ * fp32 HWC (B, H, W, C) in -> fp32 planar (B, C, H, W) out, the output of
+ * layer 1.  Layer 0's output lives only in shared memory; outside the image
+ * it takes the boundary rule's value, as the reference's materialised image
+ * would give.  With SKC_PAIR=1 (opt-in: measured slower than the two
+ * unfused launches on config 1) skc_chain_fwd runs it for fp32
+ * chains of >= 3 layers when both layers are stencil-type and the generated
+ * kernel fits.  Returns SKC_OK, or SKC_ENOTTAKEN when the pair does not take this
+ * path (the caller runs the layers one by one).  With in == NULL and out ==
+ * NULL a plan query: SKC_OK = would run, SKC_ENOTTAKEN = would not.
+ */
+int skc_layer_pair_fwd(const void *in, void *out, int B, int H, int W, int C, const double *taps0, int S0,
+                       const double *taps1, int S1, int boundary, void *stream);
+
+/* Build check of the fused pair's generated kernel (no device needed):
+ * SKC_OK = compiled, SKC_ENOTTAKEN = not eligible, SKC_ECUDA = NVRTC rejected it. */
+int skc_pair_compile_check(const double *taps0, int S0, const double *taps1, int S1);
 
 /* Generated stencils compile in the background by default: a layer whose
  * kernel is not ready yet runs on the tap / dense kernels (same result to

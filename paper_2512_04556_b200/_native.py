@@ -18,7 +18,7 @@ import numpy as np
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libskc.so"
 
-SKC_OK, SKC_EBADARG, SKC_ENONFINITE, SKC_ETRUNC, SKC_ECUDA, SKC_EDEGENERATE = 0, 1, 2, 3, 4, 5
+SKC_OK, SKC_EBADARG, SKC_ENONFINITE, SKC_ETRUNC, SKC_ECUDA, SKC_EDEGENERATE, SKC_ENOTTAKEN = 0, 1, 2, 3, 4, 5, 6
 SKC_F32, SKC_F16, SKC_F64 = 0, 1, 2
 SKC_ZERO, SKC_CLAMP = 0, 1
 SKC_HWC, SKC_CHW = 0, 1
@@ -28,7 +28,7 @@ FIT_HDR = 8
 
 # Symbols declared in include/skc.h (checked by tests/test_abi.py).
 EXPORTS = (
-    "skc_version", "skc_last_error", "skc_release_scratch", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check", "skc_set_jit_mode", "skc_jit_wait",
+    "skc_version", "skc_last_error", "skc_release_scratch", "skc_max_taps", "skc_layer_fwd", "skc_layer_fwd_ex", "skc_relayout", "skc_chain_is_fused", "skc_chain_relayouts", "skc_chain_mid_dtype", "skc_layer_plan", "skc_sparse_compile_check", "skc_layer_pair_fwd", "skc_pair_compile_check", "skc_set_jit_mode", "skc_jit_wait",
     "skc_chain_fwd",
     "skc_sv_fwd", "skc_sv_grid_fwd", "skc_ir_batch", "skc_ir_energies", "skc_backward_batch", "skc_fit_init", "skc_fit_run",
     "skc_adam_step", "skc_pst_run", "skc_bilinear_sample", "skc_sv_ground_truth",
@@ -96,6 +96,8 @@ def _declare(lib):
     lib.skc_chain_relayouts.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i]
     lib.skc_chain_mid_dtype.argtypes = [_ip, _i, _i, _i]
     lib.skc_sparse_compile_check.argtypes = [_dp, _i, _i, _i, _i, _i]
+    lib.skc_layer_pair_fwd.argtypes = [_vp, _vp, _i, _i, _i, _i, _dp, _i, _dp, _i, _i, _vp]
+    lib.skc_pair_compile_check.argtypes = [_dp, _i, _dp, _i]
     lib.skc_set_jit_mode.argtypes = [_i]
     lib.skc_jit_wait.argtypes = []
     lib.skc_layer_plan.argtypes = [_dp, _i, _i, _i, _i, _i, _ip, _ip]

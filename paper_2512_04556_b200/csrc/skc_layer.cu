@@ -1482,6 +1482,28 @@ int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary,
     return SKC_OK;
 }
 
+int skc_layer_pair_fwd(const void *in, void *out, int B, int H, int W, int C, const double *taps0, int S0,
+                       const double *taps1, int S1, int boundary, void *stream) {
+    if (!taps0 || !taps1 || S0 < 1 || S1 < 1) return fail(SKC_EBADARG, "sparse layer needs at least one sample");
+    if (!finite_taps(taps0, S0) || !finite_taps(taps1, S1))
+        return fail(SKC_EBADARG, "sparse layer parameters must be finite");
+    if (!in && !out) {
+        if (B < 1 || H < 1 || W < 1 || C < 1) return fail(SKC_EBADARG, "bad image arguments");
+        return sparse_pair(nullptr, nullptr, B, H, W, C, taps0, S0, taps1, S1, boundary, nullptr) == SKC_OK ? SKC_OK
+                                                                                                     : SKC_ENOTTAKEN;
+    }
+    int rc = check_image_args(in, SKC_F32, out, SKC_F32, B, H, W, C, boundary);
+    if (rc) return rc;
+    rc = sparse_pair((const float *)in, (float *)out, B, H, W, C, taps0, S0, taps1, S1, boundary,
+                     (cudaStream_t)stream);
+    return rc == -1 ? SKC_ENOTTAKEN : rc;
+}
+
+int skc_pair_compile_check(const double *taps0, int S0, const double *taps1, int S1) {
+    if (!taps0 || !taps1 || S0 < 1 || S1 < 1) return fail(SKC_EBADARG, "bad layer arguments");
+    return sparse_pair_compile_check(taps0, S0, taps1, S1);
+}
+
 int skc_chain_relayouts(const double *taps, const int *layout, int L, int H, int W, int C, int in_dtype,
                         int boundary) {
     if (!taps || !layout || L < 1 || H < 1 || W < 1 || C < 1) return fail(SKC_EBADARG, "bad chain arguments");
@@ -1543,7 +1565,23 @@ int skc_chain_fwd(const void *in, int in_dtype, void *out, int out_dtype, int B,
         k = 1;
     }
     const double *tp = taps;
-    for (int l = 0; l < L && rc == SKC_OK; ++l) {
+    int l0 = 0;
+    // layers 0 and 1 as one fused launch (skc_sparse.cu sparse_pair): fp32
+    // HWC in, fp32 planar out, the intermediate kept in shared memory
+    if (!pre && L >= 3 && in_dtype == SKC_F32 && mid == SKC_F32) {
+        const int prc = sparse_pair((const float *)in, (float *)buf[k], B, H, W, C, taps, layout[0],
+                                    taps + 3 * layout[0], layout[1], boundary, s);
+        if (prc != -1) {
+            rc = prc;
+            src = buf[k];
+            sdt = mid;
+            spl = true;
+            k ^= 1;
+            tp += 3 * (layout[0] + layout[1]);
+            l0 = 2;
+        }
+    }
+    for (int l = l0; l < L && rc == SKC_OK; ++l) {
         const bool last = l == L - 1;
         if (last && !post) {
             rc = last_layer(src, sdt, spl, out, out_dtype, B, H, W, C, tp, layout[l], boundary, s);

@@ -121,9 +121,9 @@ struct SpPlan {
     size_t smem = 0;
 };
 
-SpPlan make_plan(const double *taps, int S, int wy = 0) {
+SpPlan make_plan(const double *taps, int S, int wy = 0, int kr = 0) {
     SpPlan p;
-    p.KR = sp_kr();
+    p.KR = kr > 0 ? kr : sp_kr();
     p.WY = wy > 0 ? wy : sp_wy();
     p.TH = 8 * p.KR * p.WY;
     std::map<std::pair<int, int>, double> acc;  // (dy, dx) -> merged weight
@@ -153,7 +153,7 @@ SpPlan make_plan(const double *taps, int S, int wy = 0) {
     // tall footprints re-read fewer window rows per output at a larger KR
     // ((KR + Dy - 1) / KR rows per output row): SKC_SPARSE_KR_WIDE (default 5)
     // for Dy >= 24
-    if (p.Dy >= 24) {
+    if (p.Dy >= 24 && kr == 0) {
         p.KR = sp_kr_wide();
         p.TH = 8 * p.KR * p.WY;
     }
@@ -451,13 +451,26 @@ const char *kSpHwcEpilogue = R"CUDA(
     }
     __syncthreads();
     const int nx = min(128, W - tx0), nr = min(TH, H - ty0);
-    for (int r = warp; r < nr; r += NWARP) {
-        TO *dst = out + (((long long)b * H + ty0 + r) * W + tx0) * C + c;
-        const float *srow = smem + r * 132;
+    // lane x of row r writes pixel (ty0 + r, tx0 + x + 32 u): pointers stepped
+    // per row (no per-element index arithmetic), full-width tiles unguarded
+    const int s32 = 32 * C;
+    const long long rstep = (long long)W * C * NWARP;
+    TO *dst = out + (((long long)b * H + ty0 + warp) * W + tx0 + lane) * C + c;
+    const float *srow = smem + warp * 132 + lane;
+    if (nx == 128) {
+#pragma unroll 2
+        for (int r = warp; r < nr; r += NWARP, dst += rstep, srow += NWARP * 132) {
+            const float v0 = srow[0], v1 = srow[32], v2 = srow[64], v3 = srow[96];
+            stx(dst, v0);
+            stx(dst + s32, v1);
+            stx(dst + 2 * s32, v2);
+            stx(dst + 3 * s32, v3);
+        }
+    } else {
+        for (int r = warp; r < nr; r += NWARP, dst += rstep, srow += NWARP * 132) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int x = lane + 32 * u;
-            if (x < nx) stx(dst + (long long)x * C, srow[x]);
+            for (int u = 0; u < 4; ++u)
+                if (lane + 32 * u < nx) stx(dst + u * s32, srow[32 * u]);
         }
     }
 )CUDA";
@@ -685,6 +698,311 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     return s.str();
 }
 
+// ------------------------------------------------- fused head pair ---
+// Layers 0 and 1 of a chain in one launch (north_star: consecutive layers
+// fused inside one CTA where the accumulated halo fits in shared memory).
+// A CTA owns one channel of a 128-column strip over a chunk of rows and
+// streams down it in blocks of TH output rows:
+//   IN  (TH + Dy0 - 1) x P1 : the channel's input rows (4-byte cp.async at
+//       element stride C from the HWC frame, the boundary rule applied);
+//   MID (TH + Dy1 - 1) x MP : layer 0's output, the rows layer 1 reads.
+// Per block: layer 0 computes the TH new MID rows (8-row x 32-column warp
+// jobs, one row and 8 columns per lane) and re-applies the boundary rule
+// outside the image (zero: 0; clamp: the clamped in-image value -- what the
+// reference's materialised intermediate holds); the last Dy0 - 1 IN rows and
+// Dy1 - 1 MID rows move to the top of their buffers (register round trip),
+// the next block's TH input rows are prefetched behind layer 1, and layer 1
+// runs from MID into registers and the planar output.  Only the horizontal
+// halo of layer 0 is recomputed (the vertical one streams), and the
+// intermediate never reaches HBM: config 1 drops one 5.2 GB round trip.
+struct PairPlan {
+    SpPlan p1, p2;     // layer 0 (KR 1: one row per lane job), layer 1 (KR, TH, WY)
+    int MP = 0, P1 = 0, NCJ = 0, RIN = 0, RMID = 0, RJ0 = 0, minb = 2;
+    size_t smem = 0;
+    bool ok = false;
+};
+
+int pair_kr() {
+    static const int v = [] { const int k = env_int("SKC_PAIR_KR", 3); return (k == 3 || k == 5) ? k : 3; }();
+    return v;
+}
+// Opt-in (SKC_PAIR=1, read per call): on config 1 the pair measured 3.35 ms
+// against 2.74 ms for the two unfused launches -- the per-channel fill at
+// element stride C (4-byte LDGSTS) took a quarter of the L1 wavefronts
+// (profiles/r02_c1_pair.md), and an all-channel fill does not leave room
+// for more than one CTA per SM.
+int pair_mode() { return env_int("SKC_PAIR", 0); }
+
+PairPlan make_pair_plan(const double *t1, int S1, const double *t2, int S2, int wy = 2) {
+    PairPlan q;
+    q.p1 = make_plan(t1, S1, wy, 1);
+    q.p2 = make_plan(t2, S2, wy, pair_kr());
+    const SpPlan &a = q.p1, &b = q.p2;
+    if (a.npos == 0 || b.npos == 0) return q;
+    const int TH = b.TH;
+    q.MP = b.pitch;
+    q.NCJ = (b.pitch + 31) / 32;
+    // input plane: the last lane job's window (col0 = NCJ * 32 - 8) ends at
+    // word NCJ * 32 - 8 + a.nw; pitch = 4 mod 8 keeps LDS.128 conflict-free
+    int p1 = q.NCJ * 32 - 8 + a.nw;
+    while (p1 % 8 != 4) ++p1;
+    q.P1 = p1;
+    q.RIN = TH + a.Dy - 1;
+    q.RMID = TH + b.Dy - 1;
+    q.RJ0 = (TH - (b.Dy - 1)) / 8;   // the prologue block computes only the rows it carries
+    q.smem = (size_t)(q.RIN * q.P1 + q.RMID * q.MP) * sizeof(float);
+    // layer 1 must reach both ways in x and y (the clamp rule's source rows
+    // and columns are then inside the buffers); two CTAs per SM at least
+    q.ok = b.dy_min < 0 && b.dy_min + b.Dy - 1 > 0 && b.DX0 + b.SH < 0 && b.DX0 + b.SH + b.Dx - 1 > 0 &&
+           b.Dy - 1 <= TH && 2 * (q.smem + 1024) <= (size_t)kMaxSmem + 1024 &&
+           (long long)a.npos * 5 <= kSpMaxFfma && (long long)b.npos * b.KR * 5 <= kSpMaxFfma;
+    // resident CTAs per SM: as many as shared memory allows, at most 3 (KR 3:
+    // 80 registers); KR 5 bodies keep 2
+    q.minb = std::max(1, std::min(b.KR >= 5 ? 2 : 3, (int)((size_t)(kMaxSmem + 1024) / (q.smem + 1024))));
+    if (const int m = env_int("SKC_PAIR_MINB", 0)) q.minb = m;
+    return q;
+}
+
+// Packed-FP32 body of one plan reading a planar shared tile through LDS.128
+// at byte address `sb` (row pitch `pitch` words), accumulating kr x 8 outputs
+// into the float array `acc` (declared by the caller); weights kw<kwbase + n>.
+void emit_f2_body(std::ostringstream &s, const SpPlan &p, int kr, int kwbase, const std::string &sb, int pitch,
+                  const std::string &acc) {
+    std::vector<int> first(p.Dy + 1, 0);
+    for (int a = 0; a < p.Dy; ++a) first[a + 1] = first[a] + (int)p.rows[a].size();
+    s << "    {\n    float2";
+    for (int i = 0; i < kr; ++i)
+        for (int j = 0; j < 4; ++j) s << (i || j ? ", " : " ") << "e" << i << "_" << j << " = make_float2(0.f, 0.f)";
+    for (int i = 0; i < kr; ++i)
+        for (int j = 0; j < 3; ++j) s << ", o" << i << "_" << j << " = make_float2(0.f, 0.f)";
+    s << ";\n    float";
+    for (int i = 0; i < kr; ++i) s << (i ? ", " : " ") << "s" << i << "_0 = 0.f, s" << i << "_7 = 0.f";
+    s << ";\n    float2";
+    for (int m = 0; m < p.nw / 2; ++m) s << (m ? ", " : " ") << "wp" << m;
+    s << ";\n";
+    for (int q = 0; q < kr + p.Dy - 1; ++q) {
+        const int a_lo = std::max(0, q - kr + 1), a_hi = std::min(p.Dy - 1, q);
+        int kmin = 1 << 30, kmax = -1;
+        for (int a = a_lo; a <= a_hi; ++a)
+            for (const SpPos &e : p.rows[a]) {
+                kmin = std::min(kmin, p.SH + e.b);
+                kmax = std::max(kmax, p.SH + e.b + 7);
+            }
+        if (kmax < 0) continue;
+        s << "    {\n";
+        // asm volatile: the loads depend on shared memory the CTA rewrites
+        // between passes (a plain asm is a pure function of its address
+        // operand to the compiler, which then hoists it out of the channel loop)
+        for (int ch = kmin / 4; ch <= kmax / 4; ++ch)
+            s << "        asm volatile(\"ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4+" << 4 * (q * pitch + 4 * ch)
+              << "];\" : \"=f\"(wp" << 2 * ch << ".x), \"=f\"(wp" << 2 * ch << ".y), \"=f\"(wp" << 2 * ch + 1
+              << ".x), \"=f\"(wp" << 2 * ch + 1 << ".y) : \"r\"(" << sb << "));\n";
+        for (int a = a_lo; a <= a_hi; ++a) {
+            const int i = q - a;
+            for (size_t e = 0; e < p.rows[a].size(); ++e) {
+                const int c0 = p.SH + p.rows[a][e].b;
+                const std::string kw = "kw" + std::to_string(kwbase + first[a] + (int)e);
+                if (c0 % 2 == 0) {
+                    for (int j = 0; j < 4; ++j)
+                        s << "        e" << i << "_" << j << " = ffma2(" << kw << ", wp" << c0 / 2 + j << ", e" << i << "_"
+                          << j << ");\n";
+                } else {
+                    s << "        s" << i << "_0 = fmaf(" << kw << ".x, wp" << (c0 - 1) / 2 << ".y, s" << i << "_0);\n";
+                    for (int j = 0; j < 3; ++j)
+                        s << "        o" << i << "_" << j << " = ffma2(" << kw << ", wp" << (c0 + 1) / 2 + j << ", o" << i
+                          << "_" << j << ");\n";
+                    s << "        s" << i << "_7 = fmaf(" << kw << ".x, wp" << (c0 + 7) / 2 << ".x, s" << i << "_7);\n";
+                }
+            }
+        }
+        s << "    }\n";
+    }
+    for (int i = 0; i < kr; ++i) {
+        for (int j = 0; j < 4; ++j)
+            s << "    " << acc << "[" << i << "][" << 2 * j << "] = e" << i << "_" << j << ".x; " << acc << "[" << i << "]["
+              << 2 * j + 1 << "] = e" << i << "_" << j << ".y;\n";
+        s << "    " << acc << "[" << i << "][0] += s" << i << "_0; " << acc << "[" << i << "][7] += s" << i << "_7;\n";
+        for (int j = 0; j < 3; ++j)
+            s << "    " << acc << "[" << i << "][" << 2 * j + 1 << "] += o" << i << "_" << j << ".x; " << acc << "[" << i
+              << "][" << 2 * j + 2 << "] += o" << i << "_" << j << ".y;\n";
+    }
+    s << "    }\n";
+}
+
+const char *kPairHead = R"CUDA(struct KWT { float2 k[NPOS]; };
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{ .reg .b64 ra, rb, rc, rd; mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5}; mov.b64 rc, {%6, %7};"
+        " fma.rn.f32x2 rd, ra, rb, rc; mov.b64 {%0, %1}, rd; }"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ void cp4(float *dst, const float *src, int n) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+// IN rows [r_lo, r_hi) <- channel c of the HWC frame, global rows gyb + r,
+// columns gx0 + [0, P1), the boundary rule applied
+__device__ __forceinline__ void fill_rows(float *inb, const float *frame, int c, int C, int H, int W, int clamp,
+                                          int gx0, int gyb, int r_lo, int r_hi, int warp, int lane) {
+    const bool colin = gx0 >= 0 && gx0 + P1 <= W;
+    for (int r = r_lo + warp; r < r_hi; r += NWARP) {
+        int gy = gyb + r;
+        const bool rowin = clamp || (gy >= 0 && gy < H);
+        gy = min(max(gy, 0), H - 1);
+        const float *src = frame + (long long)gy * W * C + c;
+        float *dst = inb + r * P1;
+        if (rowin && colin) {
+            const float *sp = src + (long long)(gx0 + lane) * C;
+#pragma unroll 2
+            for (int col = lane; col < P1; col += 32, sp += 32 * C) cp4(dst + col, sp, 4);
+        } else {
+            for (int col = lane; col < P1; col += 32) {
+                const int gx = gx0 + col;
+                const bool ok = clamp || (rowin && gx >= 0 && gx < W);
+                cp4(dst + col, src + (long long)min(max(gx, 0), W - 1) * C, ok ? 4 : 0);
+            }
+        }
+    }
+}
+
+extern "C" __global__ void __launch_bounds__(NWARP * 32, MINB)
+skc_sparse_pair(const float *__restrict__ in, float *__restrict__ out, int H, int W, int C, int clamp, int CH,
+                const __grid_constant__ KWT kw) {
+    extern __shared__ __align__(16) float smem[];
+    float *inb = smem;                  // RIN x P1: layer 0's input rows (channel c)
+    float *mid = smem + RIN * P1;       // RMID x MP: layer 0's output = layer 1's input rows
+    const long long hw = (long long)H * W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x % C, tx0 = (blockIdx.x / C) * 128, b = blockIdx.z;
+    const int y0 = blockIdx.y * CH, y1 = min(H, y0 + CH), nblk = (y1 - y0 + TH - 1) / TH;
+    const float *frame = in + (long long)b * hw * C;
+    float *o = out + ((long long)b * C + c) * hw;
+    const int lx = lane & 3, ly = lane >> 2, wx = warp & 3, wy = warp >> 2;
+    const int col0 = wx * 32 + lx * 8, row0 = wy * 8 * KR + ly * KR;
+    const int mx0 = tx0 + DX0_2;                        // global column of MID column 0
+    const int gx0 = mx0 + DX0_1;                        // global column of IN column 0
+    const bool xedge = mx0 < 0 || mx0 + MP > W;
+    const unsigned sbin = (unsigned)__cvta_generic_to_shared(inb), sbmid = (unsigned)__cvta_generic_to_shared(mid);
+)CUDA";
+
+// block k covers output rows [Y, Y + TH), Y = y0 + k * TH; MID row j <-> global
+// Y + DY0_2 + j; IN row i <-> global Y + DY0_2 + DY1M + DY0_1 + i (DY1M = Dy1 - 1)
+const char *kPairLoop = R"CUDA(    fill_rows(inb, frame, c, C, H, W, clamp, gx0, y0 - TH + DY0_2 + DY1M + DY0_1, 0, RIN, warp, lane);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll 1
+    for (int k = -1; k < nblk; ++k) {
+        const int Y = y0 + k * TH;
+        // layer 0: the TH new MID rows [DY1M, DY1M + TH) (the prologue block only those it carries)
+#pragma unroll 1
+        for (int job = warp + (k < 0 ? RJ0 * NCJ : 0); job < (TH / 8) * NCJ; job += NWARP) {
+            const int rj = job / NCJ, cj = job - rj * NCJ;
+            const int r0 = rj * 8 + ly, c0 = cj * 32 + lx * 8;
+            const unsigned sb1 = sbin + 4u * (unsigned)(r0 * P1 + c0);
+            float acc1[1][8];
+)CUDA";
+
+const char *kPairMid = R"CUDA(            float *d = mid + (DY1M + r0) * MP + c0;
+            if (c0 < MP) *(float4 *)d = make_float4(acc1[0][0], acc1[0][1], acc1[0][2], acc1[0][3]);
+            if (c0 + 4 < MP) *(float4 *)(d + 4) = make_float4(acc1[0][4], acc1[0][5], acc1[0][6], acc1[0][7]);
+        }
+        __syncthreads();
+        const int gm0 = Y + DY0_2 + DY1M;   // global row of new MID row 0
+        if (xedge || gm0 < 0 || gm0 + TH > H) {
+            // outside the image the intermediate is the boundary rule's value
+            const int r_lo = k < 0 ? RJ0 * 8 : 0;
+            for (int e = r_lo * MP + threadIdx.x; e < TH * MP; e += NWARP * 32) {
+                const int r = e / MP, m = e - r * MP;
+                const int gy = gm0 + r, gx = mx0 + m;
+                if (gy >= 0 && gy < H && gx >= 0 && gx < W) continue;
+                float v = 0.f;
+                if (clamp) v = mid[(min(max(gy, 0), H - 1) - Y - DY0_2) * MP + min(max(gx, 0), W - 1) - mx0];
+                mid[(DY1M + r) * MP + m] = v;
+            }
+            __syncthreads();
+        }
+        // carries: IN rows [TH, TH + DY0M) and MID rows [TH, TH + DY1M) move to the top
+        float cin[CIN], cmid[CMID];
+#pragma unroll
+        for (int i = 0; i < CIN; ++i) {
+            const int e = threadIdx.x + i * NWARP * 32;
+            if (e < DY0M * P1) cin[i] = inb[TH * P1 + e];
+        }
+#pragma unroll
+        for (int i = 0; i < CMID; ++i) {
+            const int e = threadIdx.x + i * NWARP * 32;
+            if (e < DY1M * MP) cmid[i] = mid[TH * MP + e];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < CIN; ++i) {
+            const int e = threadIdx.x + i * NWARP * 32;
+            if (e < DY0M * P1) inb[e] = cin[i];
+        }
+        if (k + 1 < nblk)
+            fill_rows(inb, frame, c, C, H, W, clamp, gx0, Y + TH + DY0_2 + DY1M + DY0_1, DY0M, RIN, warp, lane);
+        if (k >= 0) {
+            const unsigned sbase = sbmid + 4u * (unsigned)(row0 * MP + col0);
+            float acc[KR][8];
+)CUDA";
+
+const char *kPairTail = R"CUDA(            const int gx = tx0 + col0;
+#pragma unroll
+            for (int i = 0; i < KR; ++i) {
+                const int gy = Y + row0 + i;
+                if (gy >= y1) continue;
+                float *p = o + (long long)gy * W + gx;
+                if (gx + 7 < W && (W & 3) == 0) {
+                    ((float4 *)p)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                    ((float4 *)p)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+                    continue;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (gx + j < W) p[j] = acc[i][j];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < CMID; ++i) {
+            const int e = threadIdx.x + i * NWARP * 32;
+            if (e < DY1M * MP) mid[e] = cmid[i];
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+}
+)CUDA";
+
+std::string generate_pair(const PairPlan &q) {
+    const SpPlan &a = q.p1, &b = q.p2;
+    const int nt = 128 * b.WY;
+    std::ostringstream s;
+    s << "// generated by libskc (skc_sparse.cu): fused head pair, " << a.npos << " + " << b.npos << " positions\n";
+    s << "#define NWARP " << 4 * b.WY << "\n#define KR " << b.KR << "\n#define TH " << b.TH << "\n#define MP " << q.MP
+      << "\n#define P1 " << q.P1 << "\n#define RIN " << q.RIN << "\n#define RMID " << q.RMID << "\n#define DX0_2 "
+      << b.DX0 << "\n#define DY0_2 " << b.dy_min << "\n#define DX0_1 " << a.DX0 << "\n#define DY0_1 " << a.dy_min
+      << "\n#define DY0M " << a.Dy - 1 << "\n#define DY1M " << b.Dy - 1 << "\n#define NCJ " << q.NCJ
+      << "\n#define RJ0 " << q.RJ0 << "\n#define CIN " << std::max(1, ((a.Dy - 1) * q.P1 + nt - 1) / nt)
+      << "\n#define CMID " << std::max(1, ((b.Dy - 1) * q.MP + nt - 1) / nt) << "\n#define NPOS " << a.npos + b.npos
+      << "\n#define MINB " << q.minb << "\n";
+    s << kPairHead;
+    for (int n = 0; n < a.npos + b.npos; ++n) s << "    const float2 kw" << n << " = kw.k[" << n << "];\n";
+    s << kPairLoop;
+    emit_f2_body(s, a, 1, 0, "sb1", q.P1, "acc1");
+    s << kPairMid;
+    emit_f2_body(s, b, b.KR, a.npos, "sbase", q.MP, "acc");
+    s << kPairTail;
+    return s.str();
+}
+
+std::vector<float> pair_kw_table(const PairPlan &q) {
+    std::vector<float> t = kw_table(q.p1), t2 = kw_table(q.p2);
+    t.insert(t.end(), t2.begin(), t2.end());
+    return t;
+}
+
 // ---------------------------------------------------------------- NVRTC ---
 struct Nvrtc {
     bool ok = false;
@@ -839,6 +1157,7 @@ struct SpKernel {
     unsigned long long devmask = 0;  // devices whose shared-memory opt-in is set
     size_t smem = 0;
     unsigned long long last_use = 0;
+    const char *name = "skc_sparse_stencil";  // entry point of the generated source
 };
 struct Key {
     unsigned long long h;
@@ -894,7 +1213,7 @@ void evict_lru_locked() {
 void finish_locked(SpKernel &k) {
     if (k.cubin.empty() ||
         cudaLibraryLoadData(&k.lib, k.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-        cudaLibraryGetKernel(&k.kern, k.lib, "skc_sparse_stencil") != cudaSuccess) {
+        cudaLibraryGetKernel(&k.kern, k.lib, k.name) != cudaSuccess) {
         cudaGetLastError();
         k.state = kFailed;
         if (std::getenv("SKC_SPARSE_VERBOSE")) std::fprintf(stderr, "skc sparse stencil unavailable: %s\n", k.why.c_str());
@@ -906,13 +1225,15 @@ void finish_locked(SpKernel &k) {
 
 // The compiled kernel for `src` (see above); nullptr while it compiles in
 // the background or when the run-time compiler is unavailable / failed.
-std::shared_ptr<SpKernel> get_kernel(const Key &key, const std::string &src, size_t smem) {
+std::shared_ptr<SpKernel> get_kernel(const Key &key, const std::string &src, size_t smem,
+                                     const char *name = "skc_sparse_stencil") {
     std::unique_lock<std::mutex> lock(g_mu);
     auto it = g_cache.find(key);
     std::shared_ptr<SpKernel> k;
     if (it == g_cache.end()) {
         k = std::make_shared<SpKernel>();
         k->smem = smem;
+        k->name = name;
         g_cache.emplace(key, k);
         evict_lru_locked();
         if (jit_sync()) {
@@ -978,6 +1299,7 @@ struct SpLaunch {
     std::string src;           // kept until the kernel is ready
     std::vector<float> kw;     // (K, K) per position: the kernel parameter
     int WY = 2;                // warps along y (CTA = 128 * WY threads)
+    int minb = 2;              // resident CTAs per SM the kernel is built for
 };
 constexpr size_t kMaxMemo = 4096;
 std::mutex g_memo_mu;
@@ -1047,7 +1369,11 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (cudaGetDevice(&cur_dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cur_dev);
     const int th_default = 8 * sp_wy() * sp_kr();
     const long long ctas = (long long)ceil_div(W, kSpTW) * (allc ? 1 : C) * ceil_div(H, th_default) * B;
-    const int wy = (sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1)) ? 1 : 0;
+    int wy = (sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1)) ? 1 : 0;
+    // all-channel heads run one-warp-row tiles (twice the resident CTAs, so
+    // more tiles' loads in flight per SM: config 1's head 1.25 -> 1.12 ms;
+    // SKC_SPARSE_HEAD_WY=2 keeps two warp rows)
+    if (allc && sp_wy() == 2 && env_int("SKC_SPARSE_HEAD_WY", 1) == 1) wy = 1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12));
     std::shared_ptr<SpLaunch> l = memo_get(key);
@@ -1090,6 +1416,85 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * l->WY), args, l->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
+}
+
+// Layers 0 and 1 of a chain as one fused launch (generated skc_sparse_pair):
+// fp32 HWC input -> fp32 planar output.  With in == nullptr a plan query
+// (SKC_OK = the pair would run, -1 = it would not: ineligible, disabled with
+// SKC_PAIR=0, or, outside sync JIT mode, still compiling).
+int sparse_pair(const float *in, float *out, int B, int H, int W, int C, const double *t1, int S1, const double *t2,
+                int S2, int boundary, cudaStream_t s) {
+    if (pair_mode() == 0 || sparse_mode() == 0) return -1;
+    int cur_dev = 0, nsm = 148;
+    if (cudaGetDevice(&cur_dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cur_dev);
+    std::string key((const char *)t1, sizeof(double) * 3 * (size_t)S1);
+    key.append((const char *)t2, sizeof(double) * 3 * (size_t)S2);
+    const int knobs[4] = {0x9a13, pair_kr(), S1, env_int("SKC_PAIR_MINB", 0)};
+    key.append((const char *)knobs, sizeof knobs);
+    std::shared_ptr<SpLaunch> l = memo_get(key);
+    int minb = 2;
+    if (!l) {
+        const PairPlan q = make_pair_plan(t1, S1, t2, S2);
+        l = std::make_shared<SpLaunch>();
+        // both layers stencil-like (the sparse or dense paths would take them alone)
+        const int D1 = dense_size_for(std::max(q.p1.Dx, q.p1.Dy));
+        l->eligible = q.ok && (eligible(q.p1, S1) || (D1 != 0 && D1 * D1 < 4 * S1)) && eligible(q.p2, S2);
+        l->npos = q.p1.npos + q.p2.npos;
+        l->minb = q.minb;
+        l->TH = q.p2.TH;
+        l->WY = q.p2.WY;
+        l->smem = q.smem;
+        if (l->eligible) {
+            l->src = generate_pair(q);
+            l->key = Key{fnv1a(l->src), l->src.size()};
+            l->kw = pair_kw_table(q);
+        }
+        memo_put(key, l);
+    }
+    if (!l->eligible) return -1;
+    minb = l->minb;
+    // rows per CTA (chunk, a multiple of TH): enough CTAs for ~16 waves; a
+    // frame too small to fill two waves of single-block chunks runs unfused
+    // (each chunk re-runs layer 0 on the rows it carries in)
+    const long long cols = (long long)ceil_div(W, kSpTW) * C * B, nb = ceil_div(H, l->TH);
+    const long long slots = (long long)nsm * minb;
+    // (SKC_PAIR_SMALL=1, read per call, fuses them anyway: tests of the edge logic)
+    if (cols * nb < 2 * slots && env_int("SKC_PAIR_SMALL", 0) == 0) return -1;
+    const long long chunks = std::min<long long>(nb, std::max<long long>(1, (16 * slots + cols - 1) / cols));
+    int CH = (int)(ceil_div((int)nb, (int)chunks) * l->TH);
+    if (const int ch = env_int("SKC_PAIR_CH", 0)) CH = std::max(1, ch / l->TH) * l->TH;
+    std::shared_ptr<SpKernel> k = get_kernel(l->key, l->src, l->smem, "skc_sparse_pair");
+    if (!k) return -1;
+    if (!in) return SKC_OK;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
+            std::lock_guard<std::mutex> lock(g_mu);
+            if (!(k->devmask >> dev & 1ULL)) {
+                const cudaError_t ae = cudaFuncSetAttribute((const void *)k->kern,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l->smem);
+                if (ae != cudaSuccess) return cuda_fail(ae, "cudaFuncSetAttribute(skc_sparse_pair)");
+                k->devmask |= 1ULL << dev;
+            }
+        }
+    }
+    dim3 grid(ceil_div(W, kSpTW) * C, ceil_div(H, CH), B);
+    int clamp = boundary == SKC_CLAMP ? 1 : 0;
+    void *kwp = (void *)l->kw.data();
+    void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp, (void *)&CH, kwp};
+    const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * l->WY), args, l->smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_pair");
+    return SKC_OK;
+}
+
+// Build check for the fused pair (no device needed): 0 = compiled, 1 = the
+// pair is not eligible, SKC_ECUDA = NVRTC rejected it.
+int sparse_pair_compile_check(const double *t1, int S1, const double *t2, int S2) {
+    const PairPlan q = make_pair_plan(t1, S1, t2, S2);
+    if (!q.ok) return SKC_ENOTTAKEN;
+    std::string why;
+    const std::vector<char> cubin = compile_cubin(generate_pair(q), &why);
+    return cubin.empty() ? fail(SKC_ECUDA, why) : SKC_OK;
 }
 
 }  // namespace skc

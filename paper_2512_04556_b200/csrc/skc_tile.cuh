@@ -123,6 +123,11 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc = false);
 bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out);
 bool sparse_head_allc(const double *taps, int S, int C, bool f32);
+// A chain's layers 0 and 1 fused (fp32 HWC -> fp32 planar); -1 = not taken,
+// in == nullptr: plan query.
+int sparse_pair(const float *in, float *out, int B, int H, int W, int C, const double *t1, int S1, const double *t2,
+                int S2, int boundary, cudaStream_t s);
+int sparse_pair_compile_check(const double *t1, int S1, const double *t2, int S2);
 // Fused separable Kawase chain (skc_kawase.cu): -1 when the chain or image
 // does not qualify; with in == nullptr a plan query (SKC_OK = would run).
 int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int W, int C, const double *taps,

@@ -105,3 +105,21 @@ def test_layer_routing_of_the_benchmark_complexes():
     # fp16 Kawase chain: the all-channel fp16 head replaces the input relayout pass
     assert lib.skc_chain_relayouts(nat.dbl(tk), nat.ints(lk), 6, 2160, 3840, 4, nat.SKC_F16, 0) == 0
     assert lib.skc_chain_mid_dtype(nat.ints(lk), 6, nat.SKC_F16, nat.SKC_F16) == nat.SKC_F16
+
+
+def test_pair_compiles_without_a_device():
+    """The fused head pair (layers 0+1 in one launch, skc_layer_pair_fwd) of
+    configs 0 and 1 compiles with NVRTC for sm_100a; a pair whose second layer
+    is taller than the streamed block is declined (SKC_ENOTTAKEN)."""
+    import numpy as np
+    from paper_2512_04556_b200 import _native as nat
+    from paper_2512_04556_b200 import synth
+    lib = nat.load_library()
+    for cpx in (synth.c1_complex(), synth.c0_complex()):
+        t0, t1 = (np.ascontiguousarray(l.taps()) for l in cpx.layers[:2])
+        rc = lib.skc_pair_compile_check(nat.dbl(t0), t0.shape[0], nat.dbl(t1), t1.shape[0])
+        assert rc == nat.SKC_OK, nat.last_error()
+    # a second layer taller than the streamed block (reach 40 rows) is declined
+    t0 = np.ascontiguousarray(synth.c1_complex().layers[0].taps())
+    tall = np.array([[0.25, -40.5, 0.5], [-0.75, 40.25, 0.5]], dtype=np.float64)
+    assert lib.skc_pair_compile_check(nat.dbl(t0), t0.shape[0], nat.dbl(tall), tall.shape[0]) == nat.SKC_ENOTTAKEN
