@@ -130,7 +130,10 @@ def h_loop_body(bs, tw):
     compile-time register within the block and the code is one block long
     (the fully unrolled row was ~100 KB of SASS: instruction-cache bound).
     State starts at zero: outputs before a layer's warm-up are never stored
-    (a stored output only depends on inputs inside the row)."""
+    (a stored output only depends on inputs inside the row).  With EDGE, a
+    block whose layer positions all lie inside the image (a per-block uniform
+    test) runs without the per-step masks: only the 2-3 blocks next to the
+    image edge pay for them."""
     L = len(bs)
     RX = lag(bs, L - 1)
     IW = tw + 2 * RX
@@ -145,19 +148,89 @@ def h_loop_body(bs, tw):
     out.append(f"    for (int j = 0; j < {nblk}; ++j) {{")
     out.append(f"        const unsigned *inj = in + {2 * P} * j;")
     out.append(f"        const int kj = {P} * j;")
+
+    def block(masked):
+        for t in range(P):
+            for l in reversed(range(L)):
+                D = 2 * bs[l] + 1
+                R = Rs[l]
+                if l == 0:
+                    out.append(f"        a0 = h2f2(inj[{2 * t}]);")
+                rd = f"r{l}_{(t - l - D) % R}"
+                wr = f"r{l}_{(t - l) % R}"
+                out.append(f"        sv = add2(a{l}, p{l}); p{l} = a{l}; a{l + 1} = add2(sv, {rd}); {wr} = sv;")
+                if masked:
+                    out.append(f"        if ((unsigned)(xg0 + kj + {t - l - lag(bs, l)}) >= (unsigned)W) a{l + 1} = z2;")
+                if l == L - 1:
+                    o = t - (L - 1) - 2 * RX
+                    out.append(f"        {{ const int oc = kj + {o}; if ((unsigned)oc < {tw}u) out[2 * oc] = a{L}; }}")
+
+    lo = -(L - 1) - RX              # smallest / largest position offset a block's layer steps touch
+    hi = P - 1 - lag(bs, 0)
+    out.append(f"        if (EDGE && (xg0 + kj + {lo} < 0 || xg0 + kj + {hi} >= W)) {{")
+    block(True)
+    out.append("        } else {")
+    block(False)
+    out.append("        }")
+    out.append("    }")
+    return "\n".join(out)
+
+
+def h_peel_body(bs, tw):
+    """Interior (no edge mask) variant of h_loop_body with the warm-up peeled:
+    the first PRO stream steps are straight-line code holding only the layer
+    steps a stored output depends on (layer l starts at its index start(l):
+    ~30% of the warm-up's layer steps drop out), every register is written
+    before it is read (no zero fill), and the stream is shifted so the first
+    stored column falls on a block boundary: the steady loop stores
+    unconditionally."""
+    L = len(bs)
+    RX = lag(bs, L - 1)
+    first_out = 2 * RX + L - 1
+    PRO = (first_out + P - 1) // P * P
+    shift = PRO - first_out
+    assert tw % P == 0
+    Rs = [ring_size(2 * b + 1) for b in bs]
+    regs = ["sv"] + [f"a{l}" for l in range(L + 1)] + [f"p{l}" for l in range(L)] + \
+        [f"r{l}_{i}" for l in range(L) for i in range(Rs[l])]
+    out = [f"    float2 {', '.join(regs)};"]
+    for tau in range(shift, PRO):
+        for l in reversed(range(L)):
+            k = tau - shift - l
+            if k < 0:
+                continue
+            if l == 0:
+                out.append(f"    a0 = h2f2(in[{2 * k}]);")
+            D = 2 * bs[l] + 1
+            R = Rs[l]
+            st = start(bs, l)
+            if k < st:
+                continue
+            if k == st:
+                out.append(f"    p{l} = a{l};")
+                continue
+            rd = f"r{l}_{(tau - l - D) % R}"
+            wr = f"r{l}_{(tau - l) % R}"
+            if k < st + D + 1:
+                out.append(f"    {wr} = add2(a{l}, p{l}); p{l} = a{l};")
+            else:
+                out.append(f"    sv = add2(a{l}, p{l}); p{l} = a{l}; a{l + 1} = add2(sv, {rd}); {wr} = sv;")
+    out.append("#pragma unroll 1")
+    out.append(f"    for (int j = 0; j < {tw // P}; ++j) {{")
+    out.append(f"        const unsigned *inj = in + {2 * (PRO - shift)} + {2 * P} * j;")
+    out.append(f"        float2 *oj = out + {2 * P} * j;")
     for t in range(P):
+        tau = PRO + t
         for l in reversed(range(L)):
             D = 2 * bs[l] + 1
             R = Rs[l]
             if l == 0:
                 out.append(f"        a0 = h2f2(inj[{2 * t}]);")
-            rd = f"r{l}_{(t - l - D) % R}"
-            wr = f"r{l}_{(t - l) % R}"
+            rd = f"r{l}_{(tau - l - D) % R}"
+            wr = f"r{l}_{(tau - l) % R}"
             out.append(f"        sv = add2(a{l}, p{l}); p{l} = a{l}; a{l + 1} = add2(sv, {rd}); {wr} = sv;")
-            out.append(f"        if (EDGE && (unsigned)(xg0 + kj + {t - l - lag(bs, l)}) >= (unsigned)W) a{l + 1} = z2;")
             if l == L - 1:
-                o = t - (L - 1) - 2 * RX
-                out.append(f"        {{ const int oc = kj + {o}; if ((unsigned)oc < {tw}u) out[2 * oc] = a{L}; }}")
+                out.append(f"        oj[{2 * t}] = a{L};")
     out.append("    }")
     return "\n".join(out)
 
@@ -222,6 +295,16 @@ template <> struct KwGen<{L}> {{
     template <bool EDGE>
     static __device__ __forceinline__ void h_quarter(const unsigned *in, float2 *out, int xg0, int W) {{
 {h_loop_body(bs, TW // 4)}
+    }}
+    // interior rows with the warm-up peeled (no edge masks)
+    static __device__ __forceinline__ void h_peel(const unsigned *in, float2 *out) {{
+{h_peel_body(bs, TW)}
+    }}
+    static __device__ __forceinline__ void h_half_peel(const unsigned *in, float2 *out) {{
+{h_peel_body(bs, TW // 2)}
+    }}
+    static __device__ __forceinline__ void h_quarter_peel(const unsigned *in, float2 *out) {{
+{h_peel_body(bs, TW // 4)}
     }}
     template <bool MASK>
     static __device__ __forceinline__ void v(const float2 *col, State &S, int yin0, int H, int yout0, int y0, int y1,

@@ -61,6 +61,8 @@ struct KwParams {
     int bands, segs, seglen, items;
     float scale;
     int dbg;   // SKC_KAWASE_DBG bits (bring-up): 1 = no TMA, 2 = no H math, 4 = no V math
+    int hint;  // mbarrier.try_wait suspend-time hint, ns (SKC_KAWASE_HINT, default 1000)
+    int peel;  // interior rows run the H passes with the warm-up peeled (SKC_KAWASE_PEEL, default 1)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -74,14 +76,20 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+// `hint` = suspend-time hint in ns: the warp sleeps (instead of spinning on the
+// issue slots the other warps need) until the phase completes or the hint
+// expires.  The wake-up on completion is not reliable enough to sleep long: at
+// 131 us per try some CTAs of config 3 lost 1 ms to expired sleeps (SM active
+// cycles 3.0 M .. 5.4 M across the grid, profiles/r02_kawase_hint.md), so the
+// default is 1 us (KwParams::hint, SKC_KAWASE_HINT).
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity, unsigned hint) {
     const unsigned a = smem_u32(bar);
     unsigned done = 0;
     do {
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
-            : "r"(a), "r"(parity), "r"(0x20000u)   // suspend (not spin) up to ~131 us per try
+            : "r"(a), "r"(parity), "r"(hint)
             : "memory");
     } while (!done);
 }
@@ -170,6 +178,11 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + 2 * kStageBytes + 2 * kKwR * kKwHP * 4);
     unsigned long long *full_in = bars, *empty_in = bars + 2, *full_h = bars + 4, *empty_h = bars + 6;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SKC_KW_FIXED_HINT
+    const unsigned hint = 0x20000u;
+#else
+    const unsigned hint = (unsigned)p.hint;
+#endif
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full_in[i], 1);
@@ -216,23 +229,32 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
                 const int s = g & 1;
                 if (prod && l_it < p.items) {
                     // chunk g + 1 reuses the stage of chunk g - 1: wait until every H lane released it
-                    if (g >= 1) mbar_wait(&empty_in[s ^ 1], ((g - 1) >> 1) & 1);
+                    if (g >= 1) mbar_wait(&empty_in[s ^ 1], ((g - 1) >> 1) & 1, hint);
                     issue(s ^ 1);
                 }
-                mbar_wait(&full_in[s], (g >> 1) & 1);
-                if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1);
+                mbar_wait(&full_in[s], (g >> 1) & 1, hint);
+                if (g >= 2) mbar_wait(&empty_h[s], ((g >> 1) - 1) & 1, hint);
                 const unsigned *row = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) +
                                       (r * BX::IWB + BX::OFF + seg * SW) * 2 + pr;
                 float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + seg * SW * 2 + pr;
                 if (p.dbg & 2) {
                 } else if (HS == 1) {
                     if (edge) G::template h<true>(row, orow, xs - RX, p.W);
+#ifndef SKC_KW_NO_PEEL
+                    else if (p.peel) G::h_peel(row, orow);
+#endif
                     else G::template h<false>(row, orow, xs - RX, p.W);
                 } else if (HS == 2) {
                     if (edge) G::template h_half<true>(row, orow, xs - RX, p.W);
+#ifndef SKC_KW_NO_PEEL
+                    else if (p.peel) G::h_half_peel(row, orow);
+#endif
                     else G::template h_half<false>(row, orow, xs - RX, p.W);
                 } else {
                     if (edge) G::template h_quarter<true>(row, orow, xs - RX, p.W);
+#ifndef SKC_KW_NO_PEEL
+                    else if (p.peel) G::h_quarter_peel(row, orow);
+#endif
                     else G::template h_quarter<false>(row, orow, xs - RX, p.W);
                 }
                 mbar_arrive(&empty_in[s]);
@@ -254,7 +276,7 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
         const float2 sc = make_float2(p.scale, p.scale);
         for (int i = 0; i < m.iters; ++i, ++g) {
             const int s = g & 1;
-            mbar_wait(&full_h[s], (g >> 1) & 1);
+            mbar_wait(&full_h[s], (g >> 1) & 1, hint);
             const float2 *col = reinterpret_cast<const float2 *>(hres0 + s * kKwR * kKwHP) + 2 * xl + pr;
             const int yin0 = m.y0 - RX + i * kKwR;
             // intermediate rows outside the image occur only near the top and
@@ -382,6 +404,10 @@ int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, c
     {
         const char *e = std::getenv("SKC_KAWASE_DBG");
         p.dbg = e ? std::atoi(e) : 0;
+        e = std::getenv("SKC_KAWASE_HINT");
+        p.hint = e ? std::max(0, std::atoi(e)) : 1000;
+        e = std::getenv("SKC_KAWASE_PEEL");
+        p.peel = e ? std::atoi(e) : 1;
     }
     auto kern = kawase_sep_kernel<L, HS>;
     if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;

@@ -475,6 +475,37 @@ const char *kSpHwcEpilogue = R"CUDA(
     }
 )CUDA";
 
+
+// The default HWC epilogue: per-element index arithmetic and guards.  The
+// pointer-stepped form above (SKC_SPARSE_EPI=1) has fewer instructions per
+// row but measured slower on config 1's 116-position KR 5 layer (3.36 vs
+// 3.17 ms; its unrolled loads lengthen the tail every CTA serialises on).
+const char *kSpHwcEpilogueIdx = R"CUDA(
+    __syncthreads();  // every warp is done reading the input tile
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        float4 *d = (float4 *)(smem + (row0 + i) * 132 + col0);
+        d[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        d[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+    __syncthreads();
+    const int nx = min(128, W - tx0), nr = min(TH, H - ty0);
+    for (int r = warp; r < nr; r += NWARP) {
+        TO *dst = out + (((long long)b * H + ty0 + r) * W + tx0) * C + c;
+        const float *srow = smem + r * 132;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = lane + 32 * u;
+            if (x < nx) stx(dst + (long long)x * C, srow[x]);
+        }
+    }
+)CUDA";
+
+int sp_epi() {
+    static const int v = env_int("SKC_SPARSE_EPI", 0);
+    return v;
+}
+
 // The kernel parameter the generated body reads: (K, K) per position, in
 // the body's order (stencil row a, then position within the row).
 std::vector<float> kw_table(const SpPlan &p) {
@@ -651,7 +682,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
                 s << "    acc[" << i << "][" << 2 * j + 1 << "] += o" << i << "_" << j << ".x; acc[" << i << "][" << 2 * j + 2
                   << "] += o" << i << "_" << j << ".y;\n";
         }
-        s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+        s << (out_pl ? kSpPlanarEpilogue : sp_epi() ? kSpHwcEpilogue : kSpHwcEpilogueIdx);
         s << (allc ? "    }\n}\n" : "}\n");
         return s.str();
     }
@@ -693,7 +724,7 @@ std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bo
     s << "    float acc[KR][8];\n";
  for (int i = 0; i < p.KR; ++i)
         for (int j = 0; j < 8; ++j) s << "    acc[" << i << "][" << j << "] = a" << i << "_" << j << ";\n";
-    s << (out_pl ? kSpPlanarEpilogue : kSpHwcEpilogue);
+    s << (out_pl ? kSpPlanarEpilogue : sp_epi() ? kSpHwcEpilogue : kSpHwcEpilogueIdx);
     s << (allc ? "    }\n}\n" : "}\n");
     return s.str();
 }

@@ -200,3 +200,17 @@ def test_pst_config_validation_and_exports():
             assert np.array_equal(draws[it, 93:], [rng.uniform(), rng.uniform()])
         else:
             assert not draws[it, 93:].any()
+
+
+def test_kawase_generated_h_bodies():
+    """The peeled horizontal pass bodies gen_kawase.py emits for the fused
+    Kawase kernel equal the direct chain of 1-D sums (engine.py:173-178 in its
+    separable form) for every instantiated ladder and row split."""
+    import importlib.util
+    from pathlib import Path
+    spec = importlib.util.spec_from_file_location(
+        "kawase_gen_check", Path(__file__).resolve().parent.parent / "tools" / "kawase_gen_check.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.check_peel()
+    mod.check_loop()
