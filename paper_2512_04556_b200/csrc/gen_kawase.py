@@ -245,7 +245,9 @@ def v_loop_state(bs):
 def v_loop_body(bs):
     """One R-row iteration of the vertical passes as a loop over blocks of P
     rows (R % P == 0 and every ring size divides P: no rotation at the end).
-    At local step t of block h layer l handles stream step 32 i + P h + t - l."""
+    At local step t of block h layer l handles stream step 32 i + P h + t - l.
+    Without MASK, a block whose P output rows all lie inside the segment's
+    [y0, y1) (a per-block uniform test) stores unguarded."""
     assert R % P == 0
     L = len(bs)
     Rs = [ring_size(2 * b + 1) for b in bs]
@@ -254,21 +256,33 @@ def v_loop_body(bs):
            f"        const float2 *colh = col + h * {P * HP2};",
            f"        const int th = {P} * h;",
            f"        __half *orow = outp + (long long)(yout0 + th - {L - 1}) * rs;   // advanced by one row per step"]
-    for t in range(P):
-        for l in reversed(range(L)):
-            D = 2 * bs[l] + 1
-            Rl = Rs[l]
-            src = "a0" if l == 0 else f"S.a{l}"
-            if l == 0:
-                out.append(f"        a0 = colh[{t * HP2}];")
-            dst = "a0" if l == L - 1 else f"S.a{l + 1}"
-            rd = f"S.r{l}_{(t - l - D) % Rl}"
-            wr = f"S.r{l}_{(t - l) % Rl}"
-            out.append(f"        sv = add2({src}, S.p{l}); S.p{l} = {src}; {dst} = add2(sv, {rd}); {wr} = sv;")
-            out.append(f"        if (MASK && (unsigned)(yin0 + th + {t - l - lag(bs, l)}) >= (unsigned)H) {dst} = z2;")
-            if l == L - 1:
-                out.append(f"        {{ const int yo = yout0 + th + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
-                           f"*reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs; }}")
+
+    def block(masked, guarded):
+        for t in range(P):
+            for l in reversed(range(L)):
+                D = 2 * bs[l] + 1
+                Rl = Rs[l]
+                src = "a0" if l == 0 else f"S.a{l}"
+                if l == 0:
+                    out.append(f"        a0 = colh[{t * HP2}];")
+                dst = "a0" if l == L - 1 else f"S.a{l + 1}"
+                rd = f"S.r{l}_{(t - l - D) % Rl}"
+                wr = f"S.r{l}_{(t - l) % Rl}"
+                out.append(f"        sv = add2({src}, S.p{l}); S.p{l} = {src}; {dst} = add2(sv, {rd}); {wr} = sv;")
+                if masked:
+                    out.append(f"        if (MASK && (unsigned)(yin0 + th + {t - l - lag(bs, l)}) >= (unsigned)H) {dst} = z2;")
+                if l == L - 1:
+                    if guarded:
+                        out.append(f"        {{ const int yo = yout0 + th + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
+                                   f"*reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs; }}")
+                    else:
+                        out.append(f"        *reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs;")
+
+    out.append(f"        if (!MASK && yout0 + th - {L - 1} >= y0 && yout0 + th + {P - 1 - (L - 1)} < y1) {{")
+    block(False, False)
+    out.append("        } else {")
+    block(True, True)
+    out.append("        }")
     out.append("    }")
     return "\n".join(out)
 
