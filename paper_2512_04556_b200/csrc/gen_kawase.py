@@ -235,6 +235,26 @@ def h_peel_body(bs, tw):
     return "\n".join(out)
 
 
+def scalarize(text):
+    """The float2 (channel pair per lane) H body as a one-channel-per-lane
+    body: float state, plain adds, `in` a const __half * at element stride 4
+    per pixel (RGBA), `out` a float * at stride 4 (kawase_sep_kernel<L, HS, true>)."""
+    import re
+    t = text
+    t = re.sub(r"h2f2\((inj|in)\[(\d+)\]\)", lambda m: f"__half2float({m.group(1)}[{2 * int(m.group(2))}])", t)
+    t = re.sub(r"add2\((\w+), (\w+)\)", r"(\1 + \2)", t)
+    t = t.replace("make_float2(0.f, 0.f)", "0.f")
+    t = re.sub(r"const unsigned \*inj = in \+ (\d+) \+ (\d+) \* j;",
+               lambda m: f"const __half *inj = in + {2 * int(m.group(1))} + {2 * int(m.group(2))} * j;", t)
+    t = re.sub(r"const unsigned \*inj = in \+ (\d+) \* j;",
+               lambda m: f"const __half *inj = in + {2 * int(m.group(1))} * j;", t)
+    t = re.sub(r"float2 \*oj = out \+ (\d+) \* j;", lambda m: f"float *oj = out + {2 * int(m.group(1))} * j;", t)
+    t = re.sub(r"oj\[(\d+)\] =", lambda m: f"oj[{2 * int(m.group(1))}] =", t)
+    t = t.replace("out[2 * oc]", "out[4 * oc]")
+    t = re.sub(r"\bfloat2 ", "float ", t)
+    return t
+
+
 def v_loop_state(bs):
     L = len(bs)
     Rs = [ring_size(2 * b + 1) for b in bs]
@@ -253,7 +273,7 @@ def v_loop_body(bs):
     Rs = [ring_size(2 * b + 1) for b in bs]
     out = ["    float2 sv, a0;", "    const float2 z2 = make_float2(0.f, 0.f);", "#pragma unroll 1",
            f"    for (int h = 0; h < {R // P}; ++h) {{",
-           f"        const float2 *colh = col + h * {P * HP2};",
+           f"        const float2 *colh = col + h * {P} * HP2;",
            f"        const int th = {P} * h;",
            f"        __half *orow = outp + (long long)(yout0 + th - {L - 1}) * rs;   // advanced by one row per step"]
 
@@ -264,7 +284,7 @@ def v_loop_body(bs):
                 Rl = Rs[l]
                 src = "a0" if l == 0 else f"S.a{l}"
                 if l == 0:
-                    out.append(f"        a0 = colh[{t * HP2}];")
+                    out.append(f"        a0 = colh[{t} * HP2];")
                 dst = "a0" if l == L - 1 else f"S.a{l + 1}"
                 rd = f"S.r{l}_{(t - l - D) % Rl}"
                 wr = f"S.r{l}_{(t - l) % Rl}"
@@ -320,7 +340,16 @@ template <> struct KwGen<{L}> {{
     static __device__ __forceinline__ void h_quarter_peel(const unsigned *in, float2 *out) {{
 {h_peel_body(bs, TW // 4)}
     }}
-    template <bool MASK>
+    // one channel per lane (scalar fp32 state): twice the H lanes at half the registers
+    template <bool EDGE>
+    static __device__ __forceinline__ void h_half_sc(const __half *in, float *out, int xg0, int W) {{
+{scalarize(h_loop_body(bs, TW // 2))}
+    }}
+    static __device__ __forceinline__ void h_half_peel_sc(const __half *in, float *out) {{
+{scalarize(h_peel_body(bs, TW // 2))}
+    }}
+    // HP2 = H-result row pitch in float2
+    template <bool MASK, int HP2>
     static __device__ __forceinline__ void v(const float2 *col, State &S, int yin0, int H, int yout0, int y0, int y1,
                                              __half *outp, long long rs, float2 sc) {{
 {v_loop_body(bs)}

@@ -49,11 +49,24 @@ constexpr int kKwNV = kKwTW / 16; // V warps (16 columns x 2 channel pairs each)
 // H warps: 2 per row segment (16 rows x 2 channel pairs each); HS = 1 runs
 // the band's whole row per lane, HS = 2 splits it into two 64-column halves
 // (each with its own 2 x reach halo) over twice the lanes
-template <int HS> __host__ __device__ constexpr int kw_nh() { return 2 * HS; }
+// SC (HS = 2 only, opt-in SKC_KAWASE_SC=1): one channel per H lane (scalar
+// fp32 state) -- 8 H warps of 8 rows x 4 channels, each with half the register
+// state and FADD (one pipe cycle) where the channel-pair lanes issue FADD2
+// (two).  A single warp issues an FADD2 every other cycle at best, and the 4
+// pair-lane H warps are the critical path (V warps wait half their time on the
+// H results, profiles/r02_kawase_peel.md).  The 16 warps launch at 128
+// registers and rebalance with setmaxnreg: H warpgroups drop to 96, V
+// warpgroups (128 registers of delay lines) take 160.  Measured slower (config
+// 3: 1.72 vs 1.50 ms): the V warps' wait disappears (10% of samples) but twice
+// the H instructions fill the issue slots (issue 72%, math-pipe throttle the
+// top stall at 63% FMA-pipe cycles), profiles/r02_kawase_sc.md.
+template <int HS, bool SC = false> __host__ __device__ constexpr int kw_nh() { return SC ? 8 : 2 * HS; }
 // the TMA producer is lane 0 of H warp 0 (a separate warp would make 13
 // warps for HS = 2: four on one SM sub-partition caps registers at 128)
-template <int HS> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS>() + kKwNV); }
-constexpr int kKwHP = kKwTW * 4 + 2;                  // H-result row pitch (words): 2 mod 32
+template <int HS, bool SC = false> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS, SC>() + kKwNV); }
+// H-result row pitch (words): 2 mod 32 for the float2 stores of the pair
+// lanes, 4 mod 32 for the scalar lanes (8 rows x 4 channels per warp: banks 4 r + c)
+template <bool SC = false> __host__ __device__ constexpr int kw_hp() { return kKwTW * 4 + (SC ? 4 : 2); }
 
 struct KwParams {
     __half *out;
@@ -162,10 +175,11 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
 }
 
 // one CTA per SM: the register budget is the whole file / the CTA's threads
-template <int L, int HS>
-__global__ void __maxnreg__(HS == 4 ? 128 : 168)
+template <int L, int HS, bool SC>
+__global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
-    constexpr int kKwNH = kw_nh<HS>();
+    constexpr int kKwNH = kw_nh<HS, SC>();
+    constexpr int kKwHP = kw_hp<SC>();
     using G = KwGen<L>;
     constexpr int RX = G::kReach;
     using BX = KwBox<L>;
@@ -196,9 +210,12 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
 
     if (warp < kKwNH) {
         // ------------------------------------------ horizontal passes ---
+        if (SC) asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
         constexpr int SW = kKwTW / HS;            // output columns per lane
-        const int seg = warp >> 1;
-        const int r = (warp & 1) * 16 + (lane & 15), pr = lane >> 4;
+        // pair lanes: 16 rows x 2 channel pairs per warp; scalar lanes: 8 rows x 4 channels
+        const int seg = SC ? warp >> 2 : warp >> 1;
+        const int r = SC ? (warp & 3) * 8 + (lane >> 2) : (warp & 1) * 16 + (lane & 15);
+        const int pr = SC ? (lane & 3) : lane >> 4;
         // TMA producer (lane 0 of warp 0): loads run one chunk ahead of the
         // passes; chunk c lands in stage c & 1 (the (c >> 1)-th use of it)
         const bool prod = warp == 0 && lane == 0;
@@ -238,6 +255,13 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
                                       (r * BX::IWB + BX::OFF + seg * SW) * 2 + pr;
                 float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + seg * SW * 2 + pr;
                 if (p.dbg & 2) {
+                } else if (SC) {
+                    const __half *rowh = reinterpret_cast<const __half *>(smem + s * kStageBytes) +
+                                         (r * BX::IWB + BX::OFF + seg * SW) * 4 + pr;
+                    float *oroww = hres0 + s * kKwR * kKwHP + r * kKwHP + seg * SW * 4 + pr;
+                    if (edge) G::template h_half_sc<true>(rowh, oroww, xs - RX, p.W);
+                    else if (p.peel) G::h_half_peel_sc(rowh, oroww);
+                    else G::template h_half_sc<false>(rowh, oroww, xs - RX, p.W);
                 } else if (HS == 1) {
                     if (edge) G::template h<true>(row, orow, xs - RX, p.W);
 #ifndef SKC_KW_NO_PEEL
@@ -264,6 +288,7 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
         return;
     }
     // ------------------------------------------------ vertical passes ---
+    if (SC) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
     const int vw = warp - kKwNH;
     const int xl = vw * 16 + (lane >> 1), pr = lane & 1;
     unsigned g = 0;
@@ -286,8 +311,8 @@ __global__ void __maxnreg__(HS == 4 ? 128 : 168)
             // warp's barriers) but stores nothing
             const int y1 = x < p.W ? m.y1 : m.y0;
             if (p.dbg & 4) {
-            } else if (mask) G::template v<true>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
-            else G::template v<false>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+            } else if (mask) G::template v<true, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+            else G::template v<false, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             mbar_arrive(&empty_h[s]);
         }
     }
@@ -354,8 +379,18 @@ int kawase_hs() {
     return v;
 }
 
-template <int L, int HS>
+// scalar H lanes (kawase_sep_kernel<L, 2, true>): SKC_KAWASE_SC, default 0
+int kawase_sc() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_KAWASE_SC");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int L, int HS, bool SC = false>
 int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, cudaStream_t s) {
+    constexpr int kKwHP = kw_hp<SC>();
     constexpr int RX = KwGen<L>::kReach;
     using BX = KwBox<L>;
     static_assert(BX::IWB <= 256 && BX::IWB % 2 == 0 && BX::IWB >= BX::IW + BX::OFF, "TMA box width");
@@ -409,10 +444,10 @@ int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, c
         e = std::getenv("SKC_KAWASE_PEEL");
         p.peel = e ? std::atoi(e) : 1;
     }
-    auto kern = kawase_sep_kernel<L, HS>;
+    auto kern = kawase_sep_kernel<L, HS, SC>;
     if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;
     const int grid = std::min(p.items, nsm);
-    kern<<<grid, kw_threads<HS>(), smem, s>>>(map, p);
+    kern<<<grid, kw_threads<HS, SC>(), smem, s>>>(map, p);
     SKC_LAUNCH_CHECK("kawase_sep_kernel");
     return SKC_OK;
 }
@@ -436,6 +471,7 @@ int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int 
     const int hs = kawase_hs();
 #define SKC_KW_CASE(LL)                                                                              \
     case LL:                                                                                         \
+        if (hs == 2 && kawase_sc()) return launch_kawase<LL, 2, true>(in, out, B, H, W, (float)scale, s); \
         return hs == 1 ? launch_kawase<LL, 1>(in, out, B, H, W, (float)scale, s)                     \
                        : hs == 4 ? launch_kawase<LL, 4>(in, out, B, H, W, (float)scale, s)          \
                                  : launch_kawase<LL, 2>(in, out, B, H, W, (float)scale, s);

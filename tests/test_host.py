@@ -212,5 +212,6 @@ def test_kawase_generated_h_bodies():
         "kawase_gen_check", Path(__file__).resolve().parent.parent / "tools" / "kawase_gen_check.py")
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    mod.check_peel()
-    mod.check_loop()
+    for scalar in (False, True):
+        mod.check_peel(scalar)
+        mod.check_loop(scalar)
