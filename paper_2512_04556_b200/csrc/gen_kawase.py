@@ -189,7 +189,6 @@ def h_peel_body(bs, tw):
     first_out = 2 * RX + L - 1
     PRO = (first_out + P - 1) // P * P
     shift = PRO - first_out
-    assert tw % P == 0
     Rs = [ring_size(2 * b + 1) for b in bs]
     regs = ["sv"] + [f"a{l}" for l in range(L + 1)] + [f"p{l}" for l in range(L)] + \
         [f"r{l}_{i}" for l in range(L) for i in range(Rs[l])]
@@ -232,6 +231,20 @@ def h_peel_body(bs, tw):
             if l == L - 1:
                 out.append(f"        oj[{2 * t}] = a{L};")
     out.append("    }")
+    # the tw % P columns after the last whole block (straight-line)
+    nb = tw // P
+    for t in range(tw % P):
+        tau = PRO + t          # slot indices repeat with period P
+        for l in reversed(range(L)):
+            D = 2 * bs[l] + 1
+            R = Rs[l]
+            if l == 0:
+                out.append(f"    a0 = h2f2(in[{2 * (PRO - shift + P * nb + t)}]);")
+            rd = f"r{l}_{(tau - l - D) % R}"
+            wr = f"r{l}_{(tau - l) % R}"
+            out.append(f"    sv = add2(a{l}, p{l}); p{l} = a{l}; a{l + 1} = add2(sv, {rd}); {wr} = sv;")
+            if l == L - 1:
+                out.append(f"    out[{2 * (P * nb + t)}] = a{L};")
     return "\n".join(out)
 
 
@@ -251,6 +264,7 @@ def scalarize(text):
     t = re.sub(r"float2 \*oj = out \+ (\d+) \* j;", lambda m: f"float *oj = out + {2 * int(m.group(1))} * j;", t)
     t = re.sub(r"oj\[(\d+)\] =", lambda m: f"oj[{2 * int(m.group(1))}] =", t)
     t = t.replace("out[2 * oc]", "out[4 * oc]")
+    t = re.sub(r"(\n\s*)out\[(\d+)\] =", lambda m: f"{m.group(1)}out[{2 * int(m.group(2))}] =", t)
     t = re.sub(r"\bfloat2 ", "float ", t)
     return t
 
@@ -262,7 +276,7 @@ def v_loop_state(bs):
                     [f"float2 r{l}_{i};" for l in range(L) for i in range(Rs[l])])
 
 
-def v_loop_body(bs):
+def v_loop_body(bs, lv=False):
     """One R-row iteration of the vertical passes as a loop over blocks of P
     rows (R % P == 0 and every ring size divides P: no rotation at the end).
     At local step t of block h layer l handles stream step 32 i + P h + t - l.
@@ -283,7 +297,13 @@ def v_loop_body(bs):
                 D = 2 * bs[l] + 1
                 Rl = Rs[l]
                 src = "a0" if l == 0 else f"S.a{l}"
-                if l == 0:
+                if l == 0 and lv:
+                    # the last horizontal layer (b = bs[-1]) on load: columns x-b-1, x-b, x+b, x+b+1
+                    # of the H warps' result, whose tile starts b + 1 columns left of the band
+                    b = bs[-1]
+                    out.append(f"        a0 = add2(add2(colh[{t} * HP2], colh[{t} * HP2 + 2]), "
+                               f"add2(colh[{t} * HP2 + {2 * (2 * b + 1)}], colh[{t} * HP2 + {2 * (2 * b + 2)}]));")
+                elif l == 0:
                     out.append(f"        a0 = colh[{t} * HP2];")
                 dst = "a0" if l == L - 1 else f"S.a{l + 1}"
                 rd = f"S.r{l}_{(t - l - D) % Rl}"
@@ -305,6 +325,32 @@ def v_loop_body(bs):
     out.append("        }")
     out.append("    }")
     return "\n".join(out)
+
+
+def lv_members(bs):
+    """LV: the H warps run the first L - 1 horizontal layers over the band plus
+    b + 1 halo columns each side, and the V lanes apply the last horizontal
+    layer when they load (4 loads and 3 adds instead of 1 load): the H warps
+    are the critical path and the V warps wait on them."""
+    L = len(bs)
+    if L < 2:
+        return "    static constexpr int kLvW = 0;"
+    w = TW + 2 * (bs[-1] + 1)
+    assert w % 2 == 0
+    return f"""    static constexpr int kLvW = {w};          // H-result columns per band with the last layer left to V
+    static constexpr int kLvReach = {lag(bs, L - 2)};       // reach of the first L - 1 layers
+    template <bool EDGE>
+    static __device__ __forceinline__ void h_half_lv(const unsigned *in, float2 *out, int xg0, int W) {{
+{h_loop_body(bs[:-1], w // 2)}
+    }}
+    static __device__ __forceinline__ void h_half_lv_peel(const unsigned *in, float2 *out) {{
+{h_peel_body(bs[:-1], w // 2)}
+    }}
+    template <bool MASK, int HP2>
+    static __device__ __forceinline__ void v_lv(const float2 *col, State &S, int yin0, int H, int yout0, int y0,
+                                                int y1, __half *outp, long long rs, float2 sc) {{
+{v_loop_body(bs, lv=True)}
+    }}"""
 
 
 def emit():
@@ -348,6 +394,7 @@ template <> struct KwGen<{L}> {{
     static __device__ __forceinline__ void h_half_peel_sc(const __half *in, float *out) {{
 {scalarize(h_peel_body(bs, TW // 2))}
     }}
+{lv_members(bs)}
     // HP2 = H-result row pitch in float2
     template <bool MASK, int HP2>
     static __device__ __forceinline__ void v(const float2 *col, State &S, int yin0, int H, int yout0, int y0, int y1,

@@ -66,7 +66,10 @@ template <int HS, bool SC = false> __host__ __device__ constexpr int kw_nh() { r
 template <int HS, bool SC = false> __host__ __device__ constexpr int kw_threads() { return 32 * (kw_nh<HS, SC>() + kKwNV); }
 // H-result row pitch (words): 2 mod 32 for the float2 stores of the pair
 // lanes, 4 mod 32 for the scalar lanes (8 rows x 4 channels per warp: banks 4 r + c)
-template <bool SC = false> __host__ __device__ constexpr int kw_hp() { return kKwTW * 4 + (SC ? 4 : 2); }
+// (LVW > 0: the LV tile of LVW columns, see KwGen::kLvW)
+template <bool SC = false, int LVW = 0> __host__ __device__ constexpr int kw_hp() {
+    return LVW > 0 ? LVW * 4 + 2 : kKwTW * 4 + (SC ? 4 : 2);
+}
 
 struct KwParams {
     __half *out;
@@ -149,13 +152,16 @@ struct Item {
 // (an odd 8-byte pixel start faults), so the box starts one pixel early when
 // the reach is odd; its width is padded to 2 mod 4 pixels so the staged row
 // pitch spreads the H lanes' half2 reads over 16 banks (2-way at worst).
-template <int L>
+// (LV: the wider H-result tile leaves no room for the pad: the box is the next
+// even width, 4-way conflicts on the H lanes' one load per step)
+template <int L, bool LV = false>
 struct KwBox {
     static constexpr int RX = KwGen<L>::kReach;
     static constexpr int OFF = RX & 1;                       // leading pad pixels
     static constexpr int IW = kKwTW + 2 * RX;                // pixels the passes read
-    static constexpr int IWB = ((IW + OFF + 1) / 4) * 4 + 2 >= IW + OFF ? ((IW + OFF + 1) / 4) * 4 + 2
-                                                                        : ((IW + OFF + 1) / 4) * 4 + 6;
+    static constexpr int IWB2 = ((IW + OFF + 1) / 4) * 4 + 2 >= IW + OFF ? ((IW + OFF + 1) / 4) * 4 + 2
+                                                                         : ((IW + OFF + 1) / 4) * 4 + 6;
+    static constexpr int IWB = LV ? ((IW + OFF + 1) & ~1) : IWB2;
     static constexpr unsigned kStageBytes = (unsigned)kKwR * IWB * 8;
 };
 
@@ -175,14 +181,19 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
 }
 
 // one CTA per SM: the register budget is the whole file / the CTA's threads
-template <int L, int HS, bool SC>
+// LV (HS = 2, pair lanes, L >= 2): the H warps run the first L - 1 horizontal
+// layers over the band plus b + 1 halo columns each side and the V lanes apply
+// the last horizontal layer as they load (4 loads + 3 adds instead of 1 load):
+// the 4 H warps are the critical path (an H warp issues at most one FADD2 every
+// other cycle) and the 8 V warps wait on them half their time.
+template <int L, int HS, bool SC, bool LV>
 __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
     constexpr int kKwNH = kw_nh<HS, SC>();
-    constexpr int kKwHP = kw_hp<SC>();
     using G = KwGen<L>;
+    constexpr int kKwHP = kw_hp<SC, LV ? G::kLvW : 0>();
     constexpr int RX = G::kReach;
-    using BX = KwBox<L>;
+    using BX = KwBox<L, LV>;
     constexpr unsigned kStageBytes = BX::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     // stage s of the input ring at smem + s * kStageBytes, of the H-result
@@ -255,6 +266,16 @@ __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
                                       (r * BX::IWB + BX::OFF + seg * SW) * 2 + pr;
                 float2 *orow = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + seg * SW * 2 + pr;
                 if (p.dbg & 2) {
+                } else if constexpr (LV) {
+                    constexpr int LW = G::kLvW / 2;               // H-result columns per lane
+                    constexpr int RXH = G::kLvReach;              // reach of the layers the H warps run
+                    const int xo = m.x0 - (RX - RXH) + seg * LW;  // first column this lane stores (global)
+                    const unsigned *rowl = reinterpret_cast<const unsigned *>(smem + s * kStageBytes) +
+                                           (r * BX::IWB + BX::OFF + seg * LW) * 2 + pr;
+                    float2 *orowl = reinterpret_cast<float2 *>(hres0 + s * kKwR * kKwHP + r * kKwHP) + seg * LW * 2 + pr;
+                    if (xo - RXH < 0 || xo + LW + RXH > p.W) G::template h_half_lv<true>(rowl, orowl, xo - RXH, p.W);
+                    else if (p.peel) G::h_half_lv_peel(rowl, orowl);
+                    else G::template h_half_lv<false>(rowl, orowl, xo - RXH, p.W);
                 } else if (SC) {
                     const __half *rowh = reinterpret_cast<const __half *>(smem + s * kStageBytes) +
                                          (r * BX::IWB + BX::OFF + seg * SW) * 4 + pr;
@@ -311,6 +332,10 @@ __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
             // warp's barriers) but stores nothing
             const int y1 = x < p.W ? m.y1 : m.y0;
             if (p.dbg & 4) {
+            } else if constexpr (LV) {
+                // col = the H-result tile at column x - (b + 1): the last horizontal layer runs on load
+                if (mask) G::template v_lv<true, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
+                else G::template v_lv<false, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             } else if (mask) G::template v<true, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             else G::template v<false, kKwHP / 2>(col, S, yin0, p.H, yin0 - RX, m.y0, y1, outp, (long long)p.W * 4, sc);
             mbar_arrive(&empty_h[s]);
@@ -379,6 +404,15 @@ int kawase_hs() {
     return v;
 }
 
+// the last horizontal layer applied by the V lanes (kawase_sep_kernel<L, 2, false, true>): SKC_KAWASE_LV, default 1
+int kawase_lv() {
+    static const int v = [] {
+        const char *e = std::getenv("SKC_KAWASE_LV");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 // scalar H lanes (kawase_sep_kernel<L, 2, true>): SKC_KAWASE_SC, default 0
 int kawase_sc() {
     static const int v = [] {
@@ -388,11 +422,11 @@ int kawase_sc() {
     return v;
 }
 
-template <int L, int HS, bool SC = false>
+template <int L, int HS, bool SC = false, bool LV = false>
 int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, cudaStream_t s) {
-    constexpr int kKwHP = kw_hp<SC>();
+    constexpr int kKwHP = kw_hp<SC, LV ? KwGen<L>::kLvW : 0>();
     constexpr int RX = KwGen<L>::kReach;
-    using BX = KwBox<L>;
+    using BX = KwBox<L, LV>;
     static_assert(BX::IWB <= 256 && BX::IWB % 2 == 0 && BX::IWB >= BX::IW + BX::OFF, "TMA box width");
     const size_t smem = 2 * (size_t)BX::kStageBytes + 2 * (size_t)kKwR * kKwHP * 4 + 8 * sizeof(unsigned long long);
     if (smem > (size_t)kMaxSmem) return -1;
@@ -444,7 +478,7 @@ int launch_kawase(const void *in, void *out, int B, int H, int W, float scale, c
         e = std::getenv("SKC_KAWASE_PEEL");
         p.peel = e ? std::atoi(e) : 1;
     }
-    auto kern = kawase_sep_kernel<L, HS, SC>;
+    auto kern = kawase_sep_kernel<L, HS, SC, LV>;
     if (int rc = smem_optin((const void *)kern, (int)smem)) return rc;
     const int grid = std::min(p.items, nsm);
     kern<<<grid, kw_threads<HS, SC>(), smem, s>>>(map, p);
@@ -472,6 +506,10 @@ int kawase_chain(const void *in, int idt, void *out, int odt, int B, int H, int 
 #define SKC_KW_CASE(LL)                                                                              \
     case LL:                                                                                         \
         if (hs == 2 && kawase_sc()) return launch_kawase<LL, 2, true>(in, out, B, H, W, (float)scale, s); \
+        if (hs == 2 && LL >= 2 && kawase_lv()) {                                                     \
+            const int rc = launch_kawase<LL, 2, false, (LL >= 2)>(in, out, B, H, W, (float)scale, s); \
+            if (rc != -1) return rc;                                                                 \
+        }                                                                                            \
         return hs == 1 ? launch_kawase<LL, 1>(in, out, B, H, W, (float)scale, s)                     \
                        : hs == 4 ? launch_kawase<LL, 4>(in, out, B, H, W, (float)scale, s)          \
                                  : launch_kawase<LL, 2>(in, out, B, H, W, (float)scale, s);

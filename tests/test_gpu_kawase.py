@@ -119,3 +119,41 @@ def test_fallbacks_keep_parity(skc, orc):
     assert not _is_fused(odd, 64, 90)
     out = skc.apply_complex(img, odd)
     assert normwise(out.astype(np.float64), orc.apply_complex(img.astype(np.float64), _layers(odd))) < TOL16
+
+
+def test_kernel_variants_keep_parity(skc, orc):
+    """The Kawase kernel's switches -- SKC_KAWASE_LV=0 (all horizontal layers
+    in the H warps), SKC_KAWASE_PEEL=0 (rolled H loop everywhere),
+    SKC_KAWASE_SC=1 (one channel per H lane, setmaxnreg), SKC_KAWASE_HS=1 (whole
+    band rows per lane) -- each in a fresh process, against the oracle on frames
+    with image edges inside a band, more than one band and more than one row
+    segment; interior pixels of the variants that share the summation order
+    agree bit for bit."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from paper_2512_04556_b200 import synth
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_2512_04556_b200 as skc; from paper_2512_04556_b200 import synth;"
+            "img = np.load(sys.argv[1]); np.save(sys.argv[2], skc.apply_complex(img, synth.kawase_complex()))")
+    root = str(__import__("pathlib").Path(__file__).parent.parent)
+    cpx = synth.kawase_complex()
+    rng = np.random.default_rng(11)
+    variants = ({}, {"SKC_KAWASE_LV": "0"}, {"SKC_KAWASE_LV": "0", "SKC_KAWASE_PEEL": "0"}, {"SKC_KAWASE_PEEL": "0"},
+                {"SKC_KAWASE_SC": "1"}, {"SKC_KAWASE_HS": "1"})
+    with tempfile.TemporaryDirectory() as td:
+        for shape in ((700, 300, 4), (90, 130, 4), (333, 1026, 4)):
+            img = (rng.random(shape) - 0.2).astype(np.float16)
+            np.save(f"{td}/in.npy", img)
+            ref = orc.apply_complex(img.astype(np.float64), _layers(cpx), orc.ZERO)
+            outs = []
+            for var in variants:
+                subprocess.run([sys.executable, "-c", code, f"{td}/in.npy", f"{td}/o.npy"], check=True,
+                               env=dict(os.environ, **var), cwd=root)
+                out = np.load(f"{td}/o.npy")
+                assert normwise(out.astype(np.float64), ref) < TOL16, (shape, var)
+                outs.append(out)
+            # LV=0 with and without the peeled warm-up run the same additions in the same order
+            assert np.array_equal(outs[1], outs[2]), shape
+            assert np.array_equal(outs[0], outs[3]), shape

@@ -41,6 +41,7 @@ def run_body(body, inp):
             st = re.sub(r"(?:h2f2|__half2float)\(in\[(\d+)\]\)", r"IN[\1]", st)
             st = re.sub(r"add2\((\w+), (\w+)\)", r"(\1+\2)", st)
             st = re.sub(r"oj\[(\d+)\] = (\w+)", r"OUT[oj+\1] = \2", st)
+            st = re.sub(r"^out\[(\d+)\] = (\w+)", r"OUT[\1] = \2", st)
             lines.append(" " * ind + st)
     env = {"IN": inp, "OUT": {}}
     exec("\n".join(lines), env)
@@ -104,7 +105,7 @@ def check_loop(scalar=False):
     """Rolled bodies, interior and with the image edge anywhere in the band
     (zero padding re-applied after every layer: engine.py:106-115 per layer)."""
     for L in (1, 3, 6):
-        for tw in (g.TW, g.TW // 2):
+        for tw in (g.TW, g.TW // 2, 70):
             bs = g.ladder(L)
             RX = g.lag(bs, L - 1)
             W = 300
@@ -135,7 +136,7 @@ def h4(v, b):
 def check_peel(scalar=False):
     st = 4 if scalar else 2      # index stride per pixel of `in` and `out`
     for L in range(1, g.MAX_L + 1):
-        for tw in (g.TW, g.TW // 2, g.TW // 4):
+        for tw in (g.TW, g.TW // 2, g.TW // 4, 70):
             bs = g.ladder(L)
             RX = g.lag(bs, L - 1)
             x = np.random.default_rng(L).random(tw + 2 * RX + 40)
