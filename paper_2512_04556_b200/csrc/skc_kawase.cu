@@ -185,7 +185,12 @@ __device__ __forceinline__ Item item_of(const KwParams &p, int it) {
 // layers over the band plus b + 1 halo columns each side and the V lanes apply
 // the last horizontal layer as they load (4 loads + 3 adds instead of 1 load):
 // the 4 H warps are the critical path (an H warp issues at most one FADD2 every
-// other cycle) and the 8 V warps wait on them half their time.
+// other cycle) and the 8 V warps wait on them half their time.  Opt-in
+// (SKC_KAWASE_LV=1): measured 2.43 vs 1.50 ms on config 3 -- the H warps alone
+// do not get faster (1.00 vs 0.99 ms: with the 140-column tile the input box
+// loses its bank-spreading pad and its loads conflict 4-way), the V lanes
+// alone slow from 0.73 to 0.95 ms, and together they overlap worse
+// (profiles/r02_kawase_lv.md: issue 40%, FMA pipe 48%).
 template <int L, int HS, bool SC, bool LV>
 __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
     kawase_sep_kernel(const __grid_constant__ CUtensorMap tmap, const KwParams p) {
@@ -404,11 +409,12 @@ int kawase_hs() {
     return v;
 }
 
-// the last horizontal layer applied by the V lanes (kawase_sep_kernel<L, 2, false, true>): SKC_KAWASE_LV, default 1
+// the last horizontal layer applied by the V lanes (kawase_sep_kernel<L, 2, false, true>):
+// SKC_KAWASE_LV, default 0 -- measured slower (config 3: 2.43 vs 1.50 ms)
 int kawase_lv() {
     static const int v = [] {
         const char *e = std::getenv("SKC_KAWASE_LV");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;
     }();
     return v;
 }

@@ -122,8 +122,8 @@ def test_fallbacks_keep_parity(skc, orc):
 
 
 def test_kernel_variants_keep_parity(skc, orc):
-    """The Kawase kernel's switches -- SKC_KAWASE_LV=0 (all horizontal layers
-    in the H warps), SKC_KAWASE_PEEL=0 (rolled H loop everywhere),
+    """The Kawase kernel's switches -- SKC_KAWASE_LV=1 (the V lanes apply the
+    last horizontal layer), SKC_KAWASE_PEEL=0 (rolled H loop everywhere),
     SKC_KAWASE_SC=1 (one channel per H lane, setmaxnreg), SKC_KAWASE_HS=1 (whole
     band rows per lane) -- each in a fresh process, against the oracle on frames
     with image edges inside a band, more than one band and more than one row
@@ -140,7 +140,7 @@ def test_kernel_variants_keep_parity(skc, orc):
     root = str(__import__("pathlib").Path(__file__).parent.parent)
     cpx = synth.kawase_complex()
     rng = np.random.default_rng(11)
-    variants = ({}, {"SKC_KAWASE_LV": "0"}, {"SKC_KAWASE_LV": "0", "SKC_KAWASE_PEEL": "0"}, {"SKC_KAWASE_PEEL": "0"},
+    variants = ({"SKC_KAWASE_LV": "1"}, {}, {"SKC_KAWASE_PEEL": "0"}, {"SKC_KAWASE_LV": "1", "SKC_KAWASE_PEEL": "0"},
                 {"SKC_KAWASE_SC": "1"}, {"SKC_KAWASE_HS": "1"})
     with tempfile.TemporaryDirectory() as td:
         for shape in ((700, 300, 4), (90, 130, 4), (333, 1026, 4)):
@@ -154,6 +154,6 @@ def test_kernel_variants_keep_parity(skc, orc):
                 out = np.load(f"{td}/o.npy")
                 assert normwise(out.astype(np.float64), ref) < TOL16, (shape, var)
                 outs.append(out)
-            # LV=0 with and without the peeled warm-up run the same additions in the same order
+            # with and without the peeled warm-up the same additions run in the same order
             assert np.array_equal(outs[1], outs[2]), shape
             assert np.array_equal(outs[0], outs[3]), shape
