@@ -1405,6 +1405,8 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     // more tiles' loads in flight per SM: config 1's head 1.25 -> 1.12 ms;
     // SKC_SPARSE_HEAD_WY=2 keeps two warp rows)
     if (allc && sp_wy() == 2 && env_int("SKC_SPARSE_HEAD_WY", 1) == 1) wy = 1;
+    // SKC_SPARSE_WY1=1: one-warp-row tiles for every generated layer (measurement switch)
+    if (!allc && sp_wy() == 2 && env_int("SKC_SPARSE_WY1", 0) == 1) wy = 1;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12));
     std::shared_ptr<SpLaunch> l = memo_get(key);
