@@ -1,11 +1,13 @@
-"""Emit the straight-line pass bodies of the fused separable Kawase kernel
-(skc_kawase.cu) for the instantiated ladders b_l = l, L = 1..6.
+"""Emit the pass bodies of the fused separable Kawase kernel (skc_kawase.cu)
+for the instantiated ladders b_l = l, L = 1..6.
 
 The passes are streaming 1-D filters with per-layer delay lines.  Written as
 templated loops over arrays, nvcc's front end spent minutes unrolling them;
-emitted here as named registers and straight-line code (the validity bounds
-and ring slots resolved in Python), they compile in seconds.  _build.py runs
-this before nvcc; the output lands in build/ (not tracked).
+emitted here as named registers and blocks of P stream steps (the ring slots
+and warm-up bounds resolved in Python), they compile in seconds.  _build.py
+runs this before nvcc; the output lands in build/ (not tracked).
+tools/kawase_gen_check.py runs the emitted H statements in Python against the
+direct chain (tests/test_host.py).
 
     python gen_kawase.py OUT.inc
 """
@@ -30,85 +32,6 @@ def lag(bs, l):
 
 def start(bs, l):
     return 2 * (lag(bs, l - 1) if l > 0 else 0)
-
-
-def h_body(bs, tw=TW):
-    """Horizontal passes of one staged row segment of `tw` output columns,
-    emitted as a skewed wavefront: at emission time tau, layer l handles
-    index tau - l, layers in decreasing order, so the L layer updates of one
-    time step are independent (ILP ~L) instead of one dependent chain per
-    index."""
-    L = len(bs)
-    RX = lag(bs, L - 1)
-    IW = tw + 2 * RX
-    out = []
-    regs = ["sv"] + [f"a{l}" for l in range(L + 1)] + [f"p{l}" for l in range(L)] + \
-        [f"r{l}_{i}" for l in range(L) for i in range(2 * bs[l] + 1)]
-    out.append(f"    float2 {', '.join(regs)};")
-    for tau in range(IW + L - 1):
-        for l in reversed(range(L)):
-            k = tau - l
-            if k < 0 or k >= IW:
-                continue
-            if l == 0:
-                out.append(f"    a0 = h2f2(in[{2 * k}]);")
-            D = 2 * bs[l] + 1
-            st = start(bs, l)
-            if k < st:
-                continue
-            if k == st:
-                out.append(f"    p{l} = a{l};")
-                continue
-            slot = f"r{l}_{k % D}"
-            out.append(f"    sv = add2(a{l}, p{l}); p{l} = a{l};")
-            if k < st + D + 1:
-                out.append(f"    {slot} = sv;")
-                continue
-            out.append(f"    a{l + 1} = add2(sv, {slot}); {slot} = sv;")
-            out.append(f"    if (EDGE && (unsigned)(xg0 + {k - lag(bs, l)}) >= (unsigned)W) a{l + 1} = make_float2(0.f, 0.f);")
-            if l == L - 1:
-                out.append(f"    out[{2 * (k - 2 * RX)}] = a{L};")
-    return "\n".join(out)
-
-
-def v_state(bs):
-    L = len(bs)
-    return " ".join([f"float2 a{l};" for l in range(1, L)] + [f"float2 p{l};" for l in range(L)] +
-                    [f"float2 r{l}_{i};" for l in range(L) for i in range(2 * bs[l] + 1)])
-
-
-def v_body(bs):
-    """One 32-row iteration of the vertical passes as a skewed wavefront
-    continuing across iterations: at local time t layer l handles stream step
-    32 i + t - l (its input a<l> carried from the previous time step), so the
-    layer updates of one time step are independent.  Layer L-1 therefore emits
-    row (step) t - (L-1) of the iteration."""
-    L = len(bs)
-    out = ["    float2 sv, a0;"]
-    for t in range(R):
-        for l in reversed(range(L)):
-            D = 2 * bs[l] + 1
-            slot = f"S.r{l}_{(t - l) % D}"
-            src = "a0" if l == 0 else f"S.a{l}"
-            if l == 0:
-                out.append(f"    a0 = col[{t * HP2}];")
-            dst = "a0" if l == L - 1 else f"S.a{l + 1}"
-            if l == L - 1:
-                dst = "a0"   # the chain's output of this time step (a0 is free again below)
-            out.append(f"    sv = add2({src}, S.p{l}); S.p{l} = {src}; {dst} = add2(sv, {slot}); {slot} = sv;")
-            out.append(f"    if (MASK && (unsigned)(yin0 + {t - l - lag(bs, l)}) >= (unsigned)H) {dst} = make_float2(0.f, 0.f);")
-            if l == L - 1:
-                out.append(f"    {{ const int yo = yout0 + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
-                           f"*reinterpret_cast<__half2 *>(outp + (long long)yo * rs) = __float22half2_rn(mul2(a0, sc)); }}")
-    # rotate the rings by R steps: slot k <- slot (k + R) mod D
-    for l in range(L):
-        D = 2 * bs[l] + 1
-        if R % D == 0:
-            continue
-        tmp = ", ".join(f"t{i} = S.r{l}_{i}" for i in range(D))
-        out.append(f"    {{ const float2 {tmp};")
-        out.append("      " + " ".join(f"S.r{l}_{k} = t{(k + R) % D};" for k in range(D)) + " }")
-    return "\n".join(out)
 
 
 P = 16    # loop period: every ring size divides it (ring_size), so slots are compile-time
