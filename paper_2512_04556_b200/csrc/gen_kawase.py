@@ -208,11 +208,14 @@ def v_loop_body(bs, lv=False):
     assert R % P == 0
     L = len(bs)
     Rs = [ring_size(2 * b + 1) for b in bs]
-    out = ["    float2 sv, a0;", "    const float2 z2 = make_float2(0.f, 0.f);", "#pragma unroll 1",
+    out = ["    float2 sv, a0;", "    const float2 z2 = make_float2(0.f, 0.f);",
+           "    const long long rsb = rs * 2;      // output row pitch in bytes", "#pragma unroll 1",
            f"    for (int h = 0; h < {R // P}; ++h) {{",
            f"        const float2 *colh = col + h * {P} * HP2;",
            f"        const int th = {P} * h;",
-           f"        __half *orow = outp + (long long)(yout0 + th - {L - 1}) * rs;   // advanced by one row per step"]
+           # a byte pointer stepped by the row pitch and kept opaque (the empty asm): without it
+           # the compiler re-derives every row's address from the base (6 integer instructions per row)
+           f"        char *orow = reinterpret_cast<char *>(outp) + (long long)(yout0 + th - {L - 1}) * rsb;"]
 
     def block(masked, guarded):
         for t in range(P):
@@ -237,9 +240,9 @@ def v_loop_body(bs, lv=False):
                 if l == L - 1:
                     if guarded:
                         out.append(f"        {{ const int yo = yout0 + th + {t - (L - 1)}; if (yo >= y0 && yo < y1) "
-                                   f"*reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs; }}")
+                                   f"st_h2(orow, mul2(a0, sc)); orow += rsb; asm volatile(\"\" : \"+l\"(orow)); }}")
                     else:
-                        out.append(f"        *reinterpret_cast<__half2 *>(orow) = __float22half2_rn(mul2(a0, sc)); orow += rs;")
+                        out.append(f"        st_h2(orow, mul2(a0, sc)); orow += rsb; asm volatile(\"\" : \"+l\"(orow));")
 
     out.append(f"        if (!MASK && yout0 + th - {L - 1} >= y0 && yout0 + th + {P - 1 - (L - 1)} < y1) {{")
     block(False, False)

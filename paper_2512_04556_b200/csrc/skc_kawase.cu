@@ -137,6 +137,14 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     return d;
 }
 
+// one fp16 pair, rounded once, to global memory (st.global: the V lanes' row
+// pointer is kept opaque to the optimiser, which would otherwise lose the
+// address space with it)
+__device__ __forceinline__ void st_h2(char *p, float2 v) {
+    const __half2 h = __float22half2_rn(v);
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(*reinterpret_cast<const unsigned *>(&h)) : "memory");
+}
+
 __device__ __forceinline__ float2 h2f2(unsigned hv) {
     return __half22float2(*reinterpret_cast<const __half2 *>(&hv));
 }
