@@ -53,7 +53,17 @@ struct Buf {
     float *p;
     int x0, y0, w, h;
     int s;   // row stride, odd: with KR odd the 32 lanes' 5x4 block origins hit 32 banks
+    int so;  // p's offset (floats) from the CTA's dynamic shared memory, -1 for a global overflow slot
 };
+
+// The CTA's dynamic shared memory as floats: window loads indexed from this
+// symbol compile to LDS with 32-bit addressing (through Buf::p they are
+// generic LD with 64-bit address arithmetic -- 8% of the fit kernel's stall
+// samples sat on those loads and 13% on their IMADs, profiles/r02_c4_fit_final.md).
+__device__ __forceinline__ const float *smem_f32() {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return reinterpret_cast<const float *>(smem_raw);
+}
 
 struct FitParams {
     int B, L, nmax, P, M, mode;
@@ -133,7 +143,9 @@ __device__ __forceinline__ float ld_chk(const Buf &b, int y, int x) {
 
 __device__ __forceinline__ Buf buf_of(const FitSmem &S, int l) {
     const Box &bx = S.box[l];
-    return Buf{S.bufp[l], bx.x0, bx.y0, bx.w, bx.h, l == 0 ? 1 : odd_stride(bx.w)};
+    float *const bp = S.bufp[l];
+    return Buf{bp, bx.x0, bx.y0, bx.w, bx.h, l == 0 ? 1 : odd_stride(bx.w),
+               __isShared(bp) ? (int)(bp - smem_f32()) : -1};
 }
 
 // Effective weights (optim.py:164-165; softmax 159-161) -- one thread per layer.
@@ -256,6 +268,13 @@ __device__ __forceinline__ void block_taps(float (&acc)[kFKR][kFMC], const FitSm
             for (int r = 0; r <= kFKR; ++r)
 #pragma unroll
                 for (int c = 0; c <= kFMC; ++c) win[r][c] = ld_chk(src, wy + r, wx + c);
+        } else if (src.so >= 0) {
+            const float *sb = smem_f32();
+            const int o = src.so + (wy - src.y0) * src.s + (wx - src.x0);
+#pragma unroll
+            for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                for (int c = 0; c <= kFMC; ++c) win[r][c] = sb[o + r * src.s + c];
         } else {
             const float *q = src.p + (wy - src.y0) * src.s + (wx - src.x0);
 #pragma unroll
@@ -472,11 +491,20 @@ __device__ void correlate(const FitParams &p, FitSmem &S, int l, const Buf I, co
                 const bool tin = inside || (wy >= I.y0 && wy + kFKR < I.y0 + I.h && wx >= I.x0 &&
                                             wx + kFMC < I.x0 + I.w);
                 if (inside || __all_sync(__activemask(), tin)) {
-                    const float *q = I.p + (y0 + d.y - I.y0) * I.s + (x0 + d.x - I.x0);
+                    if (I.so >= 0) {
+                        const float *sb = smem_f32();
+                        const int o = I.so + (y0 + d.y - I.y0) * I.s + (x0 + d.x - I.x0);
 #pragma unroll
-                    for (int r = 0; r <= kFKR; ++r)
+                        for (int r = 0; r <= kFKR; ++r)
 #pragma unroll
-                        for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * I.s + c];
+                            for (int c = 0; c <= kFMC; ++c) win[r][c] = sb[o + r * I.s + c];
+                    } else {
+                        const float *q = I.p + (y0 + d.y - I.y0) * I.s + (x0 + d.x - I.x0);
+#pragma unroll
+                        for (int r = 0; r <= kFKR; ++r)
+#pragma unroll
+                            for (int c = 0; c <= kFMC; ++c) win[r][c] = q[r * I.s + c];
+                    }
                 } else {
 #pragma unroll
                     for (int r = 0; r <= kFKR; ++r)
