@@ -216,11 +216,7 @@ __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + 2 * kStageBytes + 2 * kKwR * kKwHP * 4);
     unsigned long long *full_in = bars, *empty_in = bars + 2, *full_h = bars + 4, *empty_h = bars + 6;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef SKC_KW_FIXED_HINT
-    const unsigned hint = 0x20000u;
-#else
     const unsigned hint = (unsigned)p.hint;
-#endif
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full_in[i], 1);
@@ -298,21 +294,15 @@ __global__ void __maxnreg__((HS == 4 || SC) ? 128 : 168)
                     else G::template h_half_sc<false>(rowh, oroww, xs - RX, p.W);
                 } else if (HS == 1) {
                     if (edge) G::template h<true>(row, orow, xs - RX, p.W);
-#ifndef SKC_KW_NO_PEEL
                     else if (p.peel) G::h_peel(row, orow);
-#endif
                     else G::template h<false>(row, orow, xs - RX, p.W);
                 } else if (HS == 2) {
                     if (edge) G::template h_half<true>(row, orow, xs - RX, p.W);
-#ifndef SKC_KW_NO_PEEL
                     else if (p.peel) G::h_half_peel(row, orow);
-#endif
                     else G::template h_half<false>(row, orow, xs - RX, p.W);
                 } else {
                     if (edge) G::template h_quarter<true>(row, orow, xs - RX, p.W);
-#ifndef SKC_KW_NO_PEEL
                     else if (p.peel) G::h_quarter_peel(row, orow);
-#endif
                     else G::template h_quarter<false>(row, orow, xs - RX, p.W);
                 }
                 mbar_arrive(&empty_in[s]);
