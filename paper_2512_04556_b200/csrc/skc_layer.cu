@@ -1448,7 +1448,8 @@ int skc_layer_plan(const double *taps, int S, int H, int W, int C, int boundary,
     const Plan pl = plan_taps(taps, S);
     int np;
     double wpo;
-    if (sparse_plan(taps, S, &np, &wpo)) {  // planar-input layers (the chain's inner and last layers)
+    // planar-input layers (the chain's inner and last layers); a single frame of this shape
+    if (sparse_plan(taps, S, &np, &wpo, sparse_small_launch(1, H, W, C, false))) {
         *kind = 3;
         *param = np;
         return SKC_OK;

@@ -203,7 +203,12 @@ int sparse_mode() {
 // reads words_per_out words.  Taken when clearly cheaper (< 0.8x).
 // Footprints the dense kernels cover (D <= 9 with D^2 < 4S, skc_layer.cu
 // try_stencil) run sparse only when it skips enough zeros: npos < 0.8 D^2.
-bool eligible(const SpPlan &p, int S) {
+// `small`: the launch fills less than two waves (config 0's 512^2 frame): a
+// layer there is bound by one CTA's latency, not by throughput, and the
+// generated stencil's CTA is shorter than the tap kernel's (config 0's
+// 12-tap radius-16 layer: 10.0 vs 13.4 us), so wide layers skip the
+// throughput comparison (SKC_SPARSE_SMALL_PREFER=0 restores it)
+bool eligible(const SpPlan &p, int S, bool small = false) {
     const int mode = sparse_mode();
     if (mode == 0 || p.npos == 0) return false;
     if ((long long)p.npos * p.KR * (sp_f2() ? 5 : 8) > kSpMaxFfma) return false;
@@ -211,6 +216,7 @@ bool eligible(const SpPlan &p, int S) {
     if (mode == 1) return true;
     const int D = dense_size_for(std::max(p.Dx, p.Dy));
     if (D != 0 && D * D < 4 * S) return p.npos < 0.8 * D * D;
+    if (small && p.npos <= 160 && env_int("SKC_SPARSE_SMALL_PREFER", 1)) return true;
     const double tap = S * (7 + 1) * 9.0 / (7 * 8.0) / 32.0;  // the tap kernel at KR = 7
     const double sp = std::max(p.npos / 128.0, p.words_per_out / 32.0);
     return sp < 0.8 * tap;
@@ -1361,13 +1367,13 @@ std::shared_ptr<SpLaunch> memo_get(const std::string &key) {
 // Plan query for skc_layer_plan: 1 and the position count / LDS words per
 // output when the layer would take the sparse path (cost model only; the
 // run-time compiler is not consulted).
-bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out) {
-    const std::string key = memo_key(taps, S, -1);
+bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out, bool small) {
+    const std::string key = memo_key(taps, S, small ? -2 : -1);
     std::shared_ptr<SpLaunch> l = memo_get(key);
     if (!l) {
-        const SpPlan p = make_plan(taps, S);
+        const SpPlan p = make_plan(taps, S, small ? 1 : 0);
         l = std::make_shared<SpLaunch>();
-        l->eligible = eligible(p, S);
+        l->eligible = eligible(p, S, small);
         l->npos = p.npos;
         l->words_per_out = p.words_per_out;
         memo_put(key, l);
@@ -1388,6 +1394,17 @@ bool sparse_head_allc(const double *taps, int S, int C, bool f32) {
 // One layer through a generated sparse stencil: planar input (fp32 or fp16),
 // planar or HWC output.  Returns -1 when the layer does not take this path
 // (ineligible, or no run-time compiler), else a status code.
+// Does a launch of this shape fill less than two waves of the default tiles
+// (sparse_layer's `small` rule)?
+bool sparse_small_launch(int B, int H, int W, int C, bool allc) {
+    int cur_dev = 0, nsm = 148;
+    if (cudaGetDevice(&cur_dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cur_dev);
+    cudaGetLastError();
+    const int th_default = 8 * sp_wy() * sp_kr();
+    const long long ctas = (long long)ceil_div(W, kSpTW) * (allc ? 1 : C) * ceil_div(H, th_default) * B;
+    return sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1);
+}
+
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc) {
     // HWC input: the all-channel head (fp32 in, planar out), or with
@@ -1400,20 +1417,25 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (cudaGetDevice(&cur_dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cur_dev);
     const int th_default = 8 * sp_wy() * sp_kr();
     const long long ctas = (long long)ceil_div(W, kSpTW) * (allc ? 1 : C) * ceil_div(H, th_default) * B;
-    int wy = (sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1)) ? 1 : 0;
+    const bool small = sp_wy() == 2 && ctas < 2LL * nsm && env_int("SKC_SPARSE_SMALL", 1);
+    int wy = small ? 1 : 0;
     // all-channel heads run one-warp-row tiles (twice the resident CTAs, so
     // more tiles' loads in flight per SM: config 1's head 1.25 -> 1.12 ms;
     // SKC_SPARSE_HEAD_WY=2 keeps two warp rows)
     if (allc && sp_wy() == 2 && env_int("SKC_SPARSE_HEAD_WY", 1) == 1) wy = 1;
     // SKC_SPARSE_WY1=1: one-warp-row tiles for every generated layer (measurement switch)
     if (!allc && sp_wy() == 2 && env_int("SKC_SPARSE_WY1", 0) == 1) wy = 1;
+    // small launches: all-channel heads at one row per thread (three times the CTAs, each a
+    // third as long: config 0's head 7.5 -> 5.5 us; SKC_SPARSE_SMALL_KR=0 keeps the default)
+    const int kr_small = (small && allc) ? env_int("SKC_SPARSE_SMALL_KR", 1) : 0;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
-                                                  (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12));
+                                                  (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12) | ((small ? 1 : 0) << 14) |
+                                                  (kr_small << 15));
     std::shared_ptr<SpLaunch> l = memo_get(key);
     if (!l) {
-        SpPlan p = make_plan(taps, S, wy);
+        SpPlan p = make_plan(taps, S, wy, kr_small);
         l = std::make_shared<SpLaunch>();
-        l->eligible = eligible(p, S);
+        l->eligible = eligible(p, S, small);
         if (allc) l->eligible = allc_ok(p, S, allc, in_f32);
         l->npos = p.npos;
         l->TH = p.TH;

@@ -121,7 +121,8 @@ int fused_chain(const void *in, int idt, void *out, int odt, int B, int H, int W
 // planar input, planar or HWC output; -1 = not taken.
 int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_pl, int B, int H, int W, int C,
                  const double *taps, int S, int boundary, cudaStream_t s, bool in_hwc = false);
-bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out);
+bool sparse_plan(const double *taps, int S, int *npos, double *words_per_out, bool small = false);
+bool sparse_small_launch(int B, int H, int W, int C, bool allc);
 bool sparse_head_allc(const double *taps, int S, int C, bool f32);
 // A chain's layers 0 and 1 fused (fp32 HWC -> fp32 planar); -1 = not taken,
 // in == nullptr: plan query.
