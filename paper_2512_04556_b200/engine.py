@@ -222,6 +222,18 @@ def _pipelined_host_batch(host_in, cpx: KernelComplex, boundary: str, host_out, 
     taps = cpx.taps()
     layout = np.ascontiguousarray(cpx.layout, dtype=np.int32)
     bnd = _boundary(boundary)
+    if b <= chunk:
+        # one chunk: nothing to overlap -- copy in, filter, copy out on the caller's stream
+        # (three streams and six events cost more than a small frame's kernels)
+        din1 = t.empty((b, h, w, c), dtype=host_in.dtype, device=dev)
+        dout1 = t.empty((b, h, w, c), dtype=host_out.dtype, device=dev)
+        din1.copy_(host_in.view(b, h, w, c), non_blocking=True)
+        rc = lib.skc_chain_fwd(nat.ptr(din1), idt, nat.ptr(dout1), odt, b, h, w, c, nat.dbl(taps),
+                               nat.ints(layout), layout.size, bnd, nat.stream_ptr(cur))
+        if rc:
+            _raise(rc, "apply_complex_batch")
+        host_out.view(b, h, w, c).copy_(dout1, non_blocking=True)
+        return host_out
     s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(cur)

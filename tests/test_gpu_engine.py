@@ -599,6 +599,10 @@ def test_pinned_host_batch_path(skc, orc):
         assert got is out
         dev = skc.apply_complex_batch(host.cuda(), cpx)
         assert torch.equal(out, dev.cpu())
+        # a batch that fits one chunk runs on the caller's stream (no pipeline)
+        out1 = torch.empty_like(host).pin_memory()
+        assert skc.apply_complex_batch(host, cpx, out=out1, chunk=8) is out1
+        assert torch.equal(out1, dev.cpu())
     # bf16 / uint8 pinned frames: generic path, compared with the fp32 result
     host = torch.from_numpy((rng.random((3, 40, 36, 3)) * 255).astype(np.uint8)).pin_memory()
     out = torch.empty((3, 40, 36, 3), dtype=torch.float32).pin_memory()
