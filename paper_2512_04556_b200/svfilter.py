@@ -117,15 +117,105 @@ def stacked_params(basis: FilterBasis) -> np.ndarray:
     return out
 
 
-def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero", out=None):
+def sv_vertical_reach(basis: FilterBasis) -> int:
+    """Rows above / below a pixel that the whole SV chain can read: per layer
+    floor(max |oy| over the basis entries) + 2 (the bilinear corner and one
+    texel for the rounding of the lerped offset), summed over the layers.
+    Lerping between entries never exceeds the larger |oy| of the two."""
+    reach = 0
+    for l in range(len(basis.layout)):
+        m = max(float(np.abs(f.layers[l].offsets[:, 1]).max()) for f in basis.filters)
+        reach += int(np.floor(m)) + 2
+    return reach
+
+
+def _sv_filter_strips(host_img, basis: FilterBasis, host_pmap, boundary: str, host_out, nstrips: int):
+    """Pinned host (H, W, C) frame and (H, W) map -> pinned host result in row
+    strips: the H2D copy of strip i+1, the passes on strip i and the D2H copy
+    of strip i-1 overlap on three streams.  A strip is filtered as an image of
+    its own rows plus sv_vertical_reach halo rows each side (real image rows,
+    so the artefacts of its artificial edges stay inside the halo and the kept
+    rows equal the whole-frame result bit for bit)."""
+    t = torch()
+    lib = nat.lib()
+    dev = t.device("cuda", t.cuda.current_device())
+    cur = t.cuda.current_stream(dev)
+    h, w = int(host_img.shape[0]), int(host_img.shape[1])
+    c = int(host_img.shape[2]) if host_img.dim() == 3 else 1
+    dt = nat.SKC_F16 if host_img.dtype == t.float16 else nat.SKC_F32
+    halo = sv_vertical_reach(basis)
+    stack = np.ascontiguousarray(stacked_params(basis))
+    ps = np.ascontiguousarray(basis.params, dtype=np.float64)
+    layout = np.ascontiguousarray(basis.layout, dtype=np.int32)
+    rows = -(-h // nstrips)
+    cap = min(h, rows + 2 * halo)
+    s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
+    for s in (s_in, s_cmp, s_out):
+        s.wait_stream(cur)
+    din = [t.empty((cap, w, c), dtype=host_img.dtype, device=dev) for _ in range(2)]
+    dpm = [t.empty((cap, w), dtype=t.float32, device=dev) for _ in range(2)]
+    dout = [t.empty((cap, w, c), dtype=host_img.dtype, device=dev) for _ in range(2)]
+    h2d = [t.cuda.Event() for _ in range(2)]
+    cmp = [t.cuda.Event() for _ in range(2)]
+    d2h = [t.cuda.Event() for _ in range(2)]
+    src = host_img.view(h, w, c)
+    dst = host_out.view(h, w, c)
+    for i, y0 in enumerate(range(0, h, rows)):
+        k = i & 1
+        y1 = min(h, y0 + rows)
+        e0, e1 = max(0, y0 - halo), min(h, y1 + halo)
+        n = e1 - e0
+        with t.cuda.stream(s_in):
+            if i >= 2:
+                s_in.wait_event(cmp[k])
+            din[k][:n].copy_(src[e0:e1], non_blocking=True)
+            dpm[k][:n].copy_(host_pmap[e0:e1], non_blocking=True)
+            h2d[k].record(s_in)
+        s_cmp.wait_event(h2d[k])
+        if i >= 2:
+            s_cmp.wait_event(d2h[k])
+        rc = lib.skc_sv_fwd(nat.ptr(din[k]), dt, nat.ptr(dout[k]), dt, n, w, c, nat.ptr(dpm[k]), nat.dbl(ps),
+                            ps.size, nat.dbl(stack), stack.shape[2], nat.ints(layout), layout.size,
+                            BOUNDARIES[boundary], nat.stream_ptr(s_cmp))
+        if rc == nat.SKC_EBADARG:
+            raise EngineError(f"sv_filter: {nat.last_error()}")
+        nat.check(rc, "sv_filter")
+        cmp[k].record(s_cmp)
+        with t.cuda.stream(s_out):
+            s_out.wait_event(cmp[k])
+            dst[y0:y1].copy_(dout[k][y0 - e0:y1 - e0], non_blocking=True)
+            d2h[k].record(s_out)
+    cur.wait_stream(s_out)
+    for buf in din + dpm + dout:
+        buf.record_stream(cur)
+    return host_out
+
+
+def sv_filter(img, basis: FilterBasis, pmap, boundary: str = "zero", out=None, strips: int = 4):
     """Per-pixel blended sparse filtering guided by a parameter map (svfilter.py:171-203).
 
     Each pass re-interpolates that layer's taps per pixel between the two
     bracketing basis entries and gathers bilinearly from the previous pass.
-    Host torch tensors (pinned) with a pinned `out` move with async copies.
+    Host torch tensors (pinned) with a pinned `out` move with async copies;
+    a pinned float32 / float16 frame with a pinned float32 map and a pinned
+    `out` of the frame's shape and dtype streams through in `strips` row
+    strips (copies both ways overlapped with the passes; the call synchronises
+    before it returns).
     """
     t = torch()
     lib = nat.lib()
+    if boundary not in BOUNDARIES:
+        raise EngineError(f"boundary must be one of {sorted(BOUNDARIES)}, got {boundary!r}")
+    if (strips > 1 and isinstance(img, t.Tensor) and isinstance(pmap, t.Tensor) and isinstance(out, t.Tensor)
+            and not img.is_cuda and not pmap.is_cuda and not out.is_cuda and img.is_pinned() and pmap.is_pinned()
+            and out.is_pinned() and img.dim() in (2, 3) and img.dtype in (t.float32, t.float16)
+            and out.dtype == img.dtype and tuple(out.shape) == tuple(img.shape) and pmap.dtype == t.float32
+            and tuple(pmap.shape) == tuple(img.shape[:2]) and img.is_contiguous() and pmap.is_contiguous()
+            and out.is_contiguous()
+            and int(img.shape[0]) >= strips * max(64, 2 * sv_vertical_reach(basis))):
+        _sv_filter_strips(img, basis, pmap, boundary, out, strips)
+        t.cuda.current_stream().synchronize()
+        return out
     im = Image(img)
     b, h, w, c = im.dims
     pm_shape = tuple(pmap.shape)

@@ -286,3 +286,42 @@ def test_sv_pixel_pairs_on_smooth_maps(skc, orc):
                 subprocess.run([sys.executable, "-c", code, f"{td}/in.npz", f"{td}/o.npy", mode], check=True,
                                env=dict(os.environ, SKC_SV_PAIRS="0"), cwd=root)
                 assert normwise(ours, np.load(f"{td}/o.npy")) < 2e-6
+
+
+def test_sv_pinned_strips_equal_whole_frame(skc):
+    """sv_filter from pinned host memory streams the frame through in row strips
+    (svfilter._sv_filter_strips: each strip plus sv_vertical_reach halo rows,
+    copies overlapped with the passes).  The stitched result equals the
+    whole-frame device result bit for bit -- zero and clamp boundary, a height
+    that does not divide, fp32 and fp16 storage -- and the halo is not
+    oversized by accident: a strip run with a 4-row halo breaks the seams."""
+    import torch
+    from paper_2512_04556_b200 import svfilter, synth
+    basis = synth.c2_basis()
+    halo = svfilter.sv_vertical_reach(basis)
+    assert 40 <= halo <= 80
+    rng = np.random.default_rng(21)
+    h, w = 4 * max(64, 2 * halo) + 37, 200
+    yy, xx = np.mgrid[0:h, 0:w]
+    pm = np.clip(np.hypot(yy - h / 2, xx - w / 2) / (0.6 * h), 0, 1).astype(np.float32)
+    for dt in (torch.float32, torch.float16):
+        img = torch.from_numpy(rng.random((h, w, 3)).astype(np.float32)).to(dt)
+        for boundary in ("zero", "clamp"):
+            whole = skc.sv_filter(img.cuda(), basis, torch.from_numpy(pm).cuda(), boundary=boundary).cpu()
+            out = torch.empty_like(img).pin_memory()
+            got = skc.sv_filter(img.pin_memory(), basis, torch.from_numpy(pm).pin_memory(), boundary=boundary,
+                                out=out)
+            assert got is out
+            assert torch.equal(out, whole), (dt, boundary)
+    # an undersized halo is caught: the same strips with 4 halo rows differ at the seams
+    orig = svfilter.sv_vertical_reach
+    try:
+        svfilter.sv_vertical_reach = lambda b: 4
+        img = torch.from_numpy(rng.random((h, w, 3)).astype(np.float32))
+        out = torch.empty_like(img).pin_memory()
+        svfilter._sv_filter_strips(img.pin_memory(), basis, torch.from_numpy(pm).pin_memory(), "zero", out, 4)
+        torch.cuda.synchronize()
+        whole = skc.sv_filter(img.cuda(), basis, torch.from_numpy(pm).cuda()).cpu()
+        assert not torch.equal(out, whole)
+    finally:
+        svfilter.sv_vertical_reach = orig
