@@ -207,6 +207,69 @@ def apply_complex(img, cpx: KernelComplex, boundary: str = "zero"):
     return im.restore(_chain(im, cpx, boundary))
 
 
+_ROW_STRIP_MIN_BYTES = 64 << 20
+
+
+def _pipelined_host_rows(host_in, cpx: KernelComplex, boundary: str, host_out, strips: int):
+    """One large pinned host frame (1, H, W, C) in row strips: the H2D copy of
+    strip i+1, the chain on strip i and the D2H copy of strip i-1 overlap on
+    three streams.  A strip is filtered as an image of its own rows plus the
+    chain's composed corner reach (dist.corner_reach) of real image rows each
+    side, so the artefacts of its artificial edges stay inside the halo and
+    the kept rows equal the whole-frame result bit for bit (the same argument
+    as dist.StripPipeline's row strips across GPUs)."""
+    from .dist import corner_reach
+    t = torch()
+    lib = nat.lib()
+    dev = t.device("cuda", t.cuda.current_device())
+    cur = t.cuda.current_stream(dev)
+    h, w = (int(v) for v in host_in.shape[1:3])
+    c = int(host_in.shape[3]) if host_in.dim() == 4 else 1
+    idt = nat.SKC_F16 if host_in.dtype == t.float16 else nat.SKC_F32
+    top, bottom, _, _ = corner_reach(cpx)
+    taps = cpx.taps()
+    layout = np.ascontiguousarray(cpx.layout, dtype=np.int32)
+    bnd = _boundary(boundary)
+    rows = -(-h // strips)
+    cap = min(h, rows + top + bottom)
+    s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
+    for s in (s_in, s_cmp, s_out):
+        s.wait_stream(cur)
+    din = [t.empty((cap, w, c), dtype=host_in.dtype, device=dev) for _ in range(2)]
+    dout = [t.empty((cap, w, c), dtype=host_in.dtype, device=dev) for _ in range(2)]
+    h2d = [t.cuda.Event() for _ in range(2)]
+    cmp = [t.cuda.Event() for _ in range(2)]
+    d2h = [t.cuda.Event() for _ in range(2)]
+    src = host_in.view(h, w, c)
+    dst = host_out.view(h, w, c)
+    for i, y0 in enumerate(range(0, h, rows)):
+        k = i & 1
+        y1 = min(h, y0 + rows)
+        e0, e1 = max(0, y0 - top), min(h, y1 + bottom)
+        n = e1 - e0
+        with t.cuda.stream(s_in):
+            if i >= 2:
+                s_in.wait_event(cmp[k])
+            din[k][:n].copy_(src[e0:e1], non_blocking=True)
+            h2d[k].record(s_in)
+        s_cmp.wait_event(h2d[k])
+        if i >= 2:
+            s_cmp.wait_event(d2h[k])
+        rc = lib.skc_chain_fwd(nat.ptr(din[k]), idt, nat.ptr(dout[k]), idt, 1, n, w, c, nat.dbl(taps),
+                               nat.ints(layout), layout.size, bnd, nat.stream_ptr(s_cmp))
+        if rc:
+            _raise(rc, "apply_complex_batch")
+        cmp[k].record(s_cmp)
+        with t.cuda.stream(s_out):
+            s_out.wait_event(cmp[k])
+            dst[y0:y1].copy_(dout[k][y0 - e0:y1 - e0], non_blocking=True)
+            d2h[k].record(s_out)
+    cur.wait_stream(s_out)
+    for buf in din + dout:
+        buf.record_stream(cur)
+    return host_out
+
+
 def _pipelined_host_batch(host_in, cpx: KernelComplex, boundary: str, host_out, chunk: int):
     """Pinned host (B,H,W,C) -> device -> pinned host, overlapping the H2D copy
     of chunk i+1, the chain on chunk i and the D2H copy of chunk i-1 on three
@@ -222,6 +285,12 @@ def _pipelined_host_batch(host_in, cpx: KernelComplex, boundary: str, host_out, 
     taps = cpx.taps()
     layout = np.ascontiguousarray(cpx.layout, dtype=np.int32)
     bnd = _boundary(boundary)
+    if b == 1 and host_in.numel() * host_in.element_size() >= _ROW_STRIP_MIN_BYTES:
+        # one large frame (config 3's 16384^2 image): overlap the copies over row strips
+        from .dist import corner_reach
+        top, bottom, _, _ = corner_reach(cpx)
+        if h >= 8 * 8 * max(1, top + bottom):
+            return _pipelined_host_rows(host_in, cpx, boundary, host_out, 8)
     if b <= chunk:
         # one chunk: nothing to overlap -- copy in, filter, copy out on the caller's stream
         # (three streams and six events cost more than a small frame's kernels)

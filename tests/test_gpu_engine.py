@@ -609,3 +609,29 @@ def test_pinned_host_batch_path(skc, orc):
     skc.apply_complex_batch(host, cpx, out=out)
     ref = skc.apply_complex_batch(host.to(torch.float32).cuda(), cpx).cpu()
     assert torch.equal(out, ref)
+
+
+def test_pinned_single_frame_row_strips(skc, monkeypatch):
+    """One large pinned host frame streams through apply_complex_batch in row
+    strips with the chain's corner-reach halo (engine._pipelined_host_rows);
+    the stitched rows equal the whole-frame device result bit for bit -- the
+    generated-stencil chain (fp32, zero and clamp) and the fused Kawase chain
+    (fp16 RGBA)."""
+    import torch
+    from paper_2512_04556_b200 import engine, synth
+    monkeypatch.setattr(engine, "_ROW_STRIP_MIN_BYTES", 0)
+    rng = np.random.default_rng(8)
+    cases = ((synth.c0_complex(), (1, 4500, 70, 3), torch.float32, ("zero", "clamp")),
+             (synth.kawase_complex(), (1, 2750, 136, 4), torch.float16, ("zero",)))
+    for cpx, shape, dt, bounds in cases:
+        host = torch.from_numpy(rng.random(shape).astype(np.float32)).to(dt).pin_memory()
+        calls = []
+        orig = engine._pipelined_host_rows
+        monkeypatch.setattr(engine, "_pipelined_host_rows", lambda *a, **k: (calls.append(1), orig(*a, **k))[1])
+        for b in bounds:
+            out = torch.empty_like(host).pin_memory()
+            skc.apply_complex_batch(host, cpx, boundary=b, out=out)
+            whole = skc.apply_complex_batch(host.cuda(), cpx, boundary=b).cpu()
+            assert torch.equal(out, whole), (shape, b)
+        assert len(calls) == len(bounds)      # the strip route ran
+        monkeypatch.setattr(engine, "_pipelined_host_rows", orig)
