@@ -1427,7 +1427,9 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     if (!allc && sp_wy() == 2 && env_int("SKC_SPARSE_WY1", 0) == 1) wy = 1;
     // small launches: all-channel heads at one row per thread (three times the CTAs, each a
     // third as long: config 0's head 7.5 -> 5.5 us; SKC_SPARSE_SMALL_KR=0 keeps the default)
-    const int kr_small = (small && allc) ? env_int("SKC_SPARSE_SMALL_KR", 1) : 0;
+    int kr_small = (small && allc) ? env_int("SKC_SPARSE_SMALL_KR", 1) : 0;
+    // SKC_SPARSE_HEAD_KR: rows per thread of the all-channel head on large launches (measurement switch)
+    if (allc && !small) kr_small = env_int("SKC_SPARSE_HEAD_KR", 0);
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12) | ((small ? 1 : 0) << 14) |
                                                   (kr_small << 15));
