@@ -246,6 +246,12 @@ skc_sparse_stencil(const TI *__restrict__ in, TO *__restrict__ out, int H, int W
     extern __shared__ __align__(16) float smem[];
     const long long hw = (long long)H * W;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if PDL
+    // programmatic dependent launch (small launches): let the next layer's grid
+    // start launching now, then wait for the previous layer's grid and its writes
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 #if ALLC
     // all channels per CTA (HWC chain head): the interleaved halo tile lands
     // with coalesced 4-byte cp.async (RS = PITCH * CC + 1 words per row: odd, so
@@ -526,8 +532,10 @@ std::vector<float> kw_table(const SpPlan &p) {
     return t;
 }
 
-std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0) {
+std::string generate(const SpPlan &p, bool in_f32, bool out_f32, bool out_pl, bool in_hwc = false, int allc = 0,
+                     bool pdl = false) {
     std::ostringstream s;
+    s << "#define PDL " << (pdl ? 1 : 0) << "\n";
     s << "#define ALLC " << (allc ? 1 : 0) << "\n#define CC " << std::max(1, allc) << "\n#define RS "
       << p.pitch * std::max(1, allc) + 1 << "\n#define RSH " << p.pitch * std::max(1, allc) + 2 << "\n";
     s << "// generated by libskc (skc_sparse.cu): " << p.npos << " positions, footprint " << p.Dx << " x " << p.Dy
@@ -1430,9 +1438,12 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     int kr_small = (small && allc) ? env_int("SKC_SPARSE_SMALL_KR", 1) : 0;
     // SKC_SPARSE_HEAD_KR: rows per thread of the all-channel head on large launches (measurement switch)
     if (allc && !small) kr_small = env_int("SKC_SPARSE_HEAD_KR", 0);
+    // small launches chain through programmatic dependent launch: the next layer's CTAs are
+    // resident and past their prologue when the previous layer's grid drains (SKC_PDL=0: plain launches)
+    const bool pdl = small && env_int("SKC_PDL", 1) != 0;
     const std::string key = memo_key(taps, S, (in_f32 ? 1 : 0) | (out_f32 ? 2 : 0) | (out_pl ? 4 : 0) |
                                                   (in_hwc ? 8 : 0) | (allc << 4) | (wy << 12) | ((small ? 1 : 0) << 14) |
-                                                  (kr_small << 15));
+                                                  (kr_small << 15) | ((pdl ? 1 : 0) << 19));
     std::shared_ptr<SpLaunch> l = memo_get(key);
     if (!l) {
         SpPlan p = make_plan(taps, S, wy, kr_small);
@@ -1445,7 +1456,7 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
         l->words_per_out = p.words_per_out;
         l->smem = p.smem;
         if (l->eligible) {
-            l->src = generate(p, in_f32, out_f32, out_pl, in_hwc, allc);
+            l->src = generate(p, in_f32, out_f32, out_pl, in_hwc, allc, pdl);
             l->key = Key{fnv1a(l->src), l->src.size()};
             l->kw = kw_table(p);
         }
@@ -1470,7 +1481,22 @@ int sparse_layer(const void *in, bool in_f32, void *out, bool out_f32, bool out_
     int clamp = boundary == SKC_CLAMP ? 1 : 0;
     void *kwp = (void *)l->kw.data();
     void *args[] = {(void *)&in, (void *)&out, (void *)&H, (void *)&W, (void *)&C, (void *)&clamp, kwp};
-    const cudaError_t e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * l->WY), args, l->smem, s);
+    cudaError_t e;
+    if (pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(128 * l->WY);
+        cfg.dynamicSmemBytes = l->smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelExC(&cfg, (const void *)k->kern, args);
+    } else {
+        e = cudaLaunchKernel((const void *)k->kern, grid, dim3(128 * l->WY), args, l->smem, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "skc_sparse_stencil");
     return SKC_OK;
 }
