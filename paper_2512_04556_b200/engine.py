@@ -208,6 +208,18 @@ def apply_complex(img, cpx: KernelComplex, boundary: str = "zero"):
 
 
 _ROW_STRIP_MIN_BYTES = 64 << 20
+_SIDE_STREAMS = {}
+
+
+def side_streams(dev):
+    """The three side streams (H2D, compute, D2H) of the pinned-host pipelines,
+    created once per device: creating them per call costs as much as a small
+    frame's kernels."""
+    t = torch()
+    key = (dev.type, dev.index)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = tuple(t.cuda.Stream(dev) for _ in range(3))
+    return _SIDE_STREAMS[key]
 
 
 def _pipelined_host_rows(host_in, cpx: KernelComplex, boundary: str, host_out, strips: int):
@@ -232,7 +244,7 @@ def _pipelined_host_rows(host_in, cpx: KernelComplex, boundary: str, host_out, s
     bnd = _boundary(boundary)
     rows = -(-h // strips)
     cap = min(h, rows + top + bottom)
-    s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
+    s_in, s_cmp, s_out = side_streams(dev)
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(cur)
     din = [t.empty((cap, w, c), dtype=host_in.dtype, device=dev) for _ in range(2)]
@@ -303,7 +315,7 @@ def _pipelined_host_batch(host_in, cpx: KernelComplex, boundary: str, host_out, 
             _raise(rc, "apply_complex_batch")
         host_out.view(b, h, w, c).copy_(dout1, non_blocking=True)
         return host_out
-    s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
+    s_in, s_cmp, s_out = side_streams(dev)
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(cur)
     n = min(chunk, b)

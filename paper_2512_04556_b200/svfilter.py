@@ -149,7 +149,8 @@ def _sv_filter_strips(host_img, basis: FilterBasis, host_pmap, boundary: str, ho
     layout = np.ascontiguousarray(basis.layout, dtype=np.int32)
     rows = -(-h // nstrips)
     cap = min(h, rows + 2 * halo)
-    s_in, s_cmp, s_out = (t.cuda.Stream(dev) for _ in range(3))
+    from .engine import side_streams
+    s_in, s_cmp, s_out = side_streams(dev)
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(cur)
     din = [t.empty((cap, w, c), dtype=host_img.dtype, device=dev) for _ in range(2)]
